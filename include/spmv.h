@@ -1,0 +1,265 @@
+/* include/spmv.h — C ABI of the B200-native SpMV library (libspmv.so).
+ *
+ * The operation is the paper's problem statement: "finds the dense vector
+ * product Y of a sparse matrix A and a dense vector X such that Y = A × X"
+ * (PAPER.md P:145), extended to the BLAS form y <- alpha·A·x + beta·y
+ * (reading R1). Input arrives as COO, "the default sparse format
+ * ... in SuiteSparse". The library converts it on the device to the
+ * paper's formats — CSR, ELL, SELL (generalised to
+ * SELL-C-sigma), plus COO and HYB from the north star — extracts the Table 2
+ * sparsity features on the device, runs a hand-written sm_100a
+ * kernel per format, and implements the paper's two optimisation modes
+ * as a launch-configuration tuner and a feature-driven format
+ * selector with an overhead gate.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns spmv_status_t. Nothing throws, nothing aborts, no
+ *    call ever falls back to the CPU: compute runs only in this library's
+ *    CUDA kernels.
+ *  - Indices are 0-based int32 (rows, cols <= 2^31-1); nnz is int64.
+ *  - Device pointers are plain CUDA device addresses on the handle's device;
+ *    host pointers are ordinary (pageable or pinned) host memory.
+ *  - On any error, `*out` handles stay NULL and nothing leaks; the handle's
+ *    spmv_last_error() holds the detail (incl. CUDA error text).
+ *  - Calls on one handle must be externally serialised; distinct handles are
+ *    independent.
+ */
+#ifndef SPMV_H
+#define SPMV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct spmv_matrix* spmv_handle_t;
+
+typedef enum {
+  SPMV_OK = 0,
+  SPMV_ERR_INVALID_ARG = 1,        /* null pointer, negative size, bad enum, x == y */
+  SPMV_ERR_INDEX_OUT_OF_RANGE = 2, /* a triplet outside [0,rows) x [0,cols) */
+  SPMV_ERR_DUPLICATE = 3,          /* a repeated (row, col) — SPEC.md S:70 */
+  SPMV_ERR_INFEASIBLE = 4,         /* ELL/SELL slot guard exceeded; handle unchanged */
+  SPMV_ERR_OUT_OF_MEMORY = 5,
+  SPMV_ERR_UNSUPPORTED = 6,        /* rows/cols > 2^31-1, SELL C not in {32,64,128,256}, ... */
+  SPMV_ERR_CUDA = 7,               /* CUDA runtime error (sticky device faults surface here) */
+  SPMV_ERR_NOT_CONVERTED = 8       /* requested format has not been built on this handle */
+} spmv_status_t;
+
+typedef enum { SPMV_R32F = 0, SPMV_R64F = 1 } spmv_dtype_t;
+typedef enum { SPMV_MEM_HOST = 0, SPMV_MEM_DEVICE = 1 } spmv_mem_t;
+
+/* Storage formats: COO, CSR, ELL, HYB (ELL + COO
+ * tail; not in the paper, north star), SELL-C-sigma (P:165 generalised). */
+typedef enum {
+  SPMV_FMT_COO = 0,
+  SPMV_FMT_CSR = 1,
+  SPMV_FMT_ELL = 2,
+  SPMV_FMT_HYB = 3,
+  SPMV_FMT_SELL = 4
+} spmv_format_t;
+#define SPMV_NUM_FORMATS 5
+
+/* CSR kernel algorithms: scalar (thread per row), vector (T lanes per row,
+ * the "coordination among threads within a warp" of P:159), merge-path. */
+typedef enum {
+  SPMV_CSR_AUTO = 0,
+  SPMV_CSR_SCALAR = 1,
+  SPMV_CSR_VECTOR = 2,
+  SPMV_CSR_MERGE = 3
+} spmv_csr_alg_t;
+
+/* Format parameters (NULL = defaults). */
+typedef struct {
+  int32_t csr_alg;    /* spmv_csr_alg_t; AUTO = vector, T from the mean row length */
+  int32_t csr_T;      /* CSR-vector lanes per row in {2,4,8,16,32}; 0 = clamp(next_pow2(ceil(mean)),2,32) */
+  int32_t sell_C;     /* SELL slice height in {32,64,128,256}; 0 = 32·(16 B / sizeof(value)) */
+  int32_t sell_sigma; /* sorting window: 1 (no sort) or a multiple of sell_C; 0 = 1 */
+  int64_t hyb_K;      /* HYB ELL width; -1 = automatic (CUSP/Bell–Garland rule, R12) */
+} spmv_format_params_t;
+
+/* Table 2 features + the north star's max and bandwidth.
+ * Definitions (R5/R6): L_i = row length; population variance;
+ * even-n median = mean of the two middle order statistics; mode = smallest
+ * most frequent L; ell_ratio = nnz / (n_rows · max_len), 1 if max_len = 0;
+ * bw_lower = max(0, max_ij (i − j)), bw_upper = max(0, max_ij (j − i)). */
+typedef struct {
+  int64_t n_rows, n_cols, nnz, max_len, min_len, n_empty, mode, bw_lower, bw_upper, bandwidth;
+  double mean, var, std, ell_ratio, median;
+} spmv_features_t;
+
+/* One launch variant: the compile-time-mode knobs of P:376-400 recast for
+ * B200 — thread-block size, register cap (__maxnreg__) and the L1/shared
+ * carveout (percent shared) — plus a per-kernel knob (CSR-vector T,
+ * merge-path items per thread, ELL/SELL rows per warp). 0 = default. */
+typedef struct {
+  int32_t block;        /* 64, 128, 256, 512, 1024 */
+  int32_t maxreg;       /* 32, 64, 128, 255 */
+  int32_t carveout_pct; /* -1 = driver default, else 0..100 */
+  int32_t knob;
+} spmv_launch_t;
+
+/* spmv_tune flags */
+#define SPMV_TUNE_LAUNCH 1u /* compile-time-mode analog: sweep launch variants of the active format */
+#define SPMV_TUNE_FORMAT 2u /* run-time-mode analog: select a format from features, measure, gate */
+#define SPMV_TUNE_ALL 3u
+
+typedef struct {
+  int32_t format;                /* chosen spmv_format_t (active after the call) */
+  spmv_format_params_t params;   /* its parameters */
+  spmv_launch_t launch;          /* its chosen launch variant */
+  double t_csr_s;                /* measured default (CSR) SpMV time */
+  double t_best_s;               /* measured time of the chosen format/variant */
+  double f_latency_s;            /* feature-extraction time (on device) */
+  double c_latency_s;            /* conversion time of the chosen format (on device) */
+  int64_t expected_iterations;   /* gate input */
+  int32_t converted;             /* 1 iff the gate accepted the conversion */
+  int32_t n_candidates;          /* formats measured */
+  int32_t n_variants;            /* launch variants measured */
+} spmv_tune_report_t;
+
+/* Format introspection (sizes of what spmv_copy_array can export). */
+typedef struct {
+  int32_t present;       /* 1 if the format is built on this handle */
+  int32_t row_ptr_is64;  /* CSR row_ptr element width: 0 = int32, 1 = int64 */
+  int64_t K;             /* ELL width / HYB ELL width */
+  int64_t n_pad;         /* ELL / HYB row padding (multiple of 128) */
+  int64_t C, sigma;      /* SELL */
+  int64_t n_slices;      /* SELL */
+  int64_t slots;         /* ELL/SELL/HYB-ELL stored slots (incl. padding) */
+  int64_t tail_nnz;      /* HYB COO tail */
+  int64_t n_empty_rows;  /* COO: rows without entries */
+  int64_t stored_bytes;  /* bytes of the format's arrays (padding included) */
+} spmv_format_info_t;
+
+typedef enum {
+  SPMV_ARR_CSR_ROW_PTR = 0,  /* int32 or int64 [rows+1] */
+  SPMV_ARR_CSR_COL = 1,      /* int32 [nnz] (also the COO column array) */
+  SPMV_ARR_CSR_VAL = 2,      /* value [nnz] (also the COO value array) */
+  SPMV_ARR_COO_ROW = 3,      /* int32 [nnz] */
+  SPMV_ARR_ELL_COL = 4,      /* int32 [K·n_pad], column-major: (i,k) at k·n_pad + i, pad −1 */
+  SPMV_ARR_ELL_VAL = 5,      /* value [K·n_pad], pad +0.0 */
+  SPMV_ARR_SELL_PERM = 6,    /* int32 [rows] (identity when sigma = 1) */
+  SPMV_ARR_SELL_SLICE_PTR = 7, /* int64 [n_slices+1] */
+  SPMV_ARR_SELL_COL = 8,     /* int32 [slots]: (s,j,k) at slice_ptr[s] + k·C + j */
+  SPMV_ARR_SELL_VAL = 9,
+  SPMV_ARR_HYB_ELL_COL = 10,
+  SPMV_ARR_HYB_ELL_VAL = 11,
+  SPMV_ARR_HYB_TAIL_ROW = 12, /* int32 [tail_nnz], (row, col) order */
+  SPMV_ARR_HYB_TAIL_COL = 13,
+  SPMV_ARR_HYB_TAIL_VAL = 14,
+  SPMV_ARR_COO_EMPTY_ROWS = 15 /* int32 [n_empty_rows], ascending */
+} spmv_array_t;
+
+/* ---------------------------------------------------------------- core API */
+
+/* Ingest + validate + canonicalise COO and build CSR on the device
+ * (SURVEY.md §8(a) rows a1–a2). Copies the triplets (host or device memory,
+ * per `where`) so the caller may free them on return; synchronous.
+ * Unsorted input is radix-sorted by (row, col) on the device; explicit
+ * zeros are kept. Errors: INVALID_ARG (nulls with nnz > 0, negative sizes,
+ * bad dtype/where), UNSUPPORTED (rows/cols > 2^31-1), INDEX_OUT_OF_RANGE,
+ * DUPLICATE, OUT_OF_MEMORY, CUDA. `cuda_stream` (cudaStream_t, may be NULL
+ * = legacy default stream) becomes the handle's stream. Active format: CSR
+ * (the paper's default). */
+spmv_status_t spmv_create(spmv_handle_t* out, int64_t rows, int64_t cols, int64_t nnz,
+                          const int32_t* row_idx, const int32_t* col_idx, const void* vals,
+                          spmv_dtype_t dtype, spmv_mem_t where, int device, void* cuda_stream);
+
+/* Build (or re-activate, if cached) `fmt` on the device and make it the
+ * active format (§8(a) row a4). p = NULL uses defaults. Synchronous.
+ * INFEASIBLE if ELL/SELL/HYB padding would not fit the device-memory guard
+ * (the handle is unchanged); UNSUPPORTED for SELL C outside {32,64,128,256}. */
+spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format_params_t* p);
+
+/* Make an already-built format active without rebuilding. NOT_CONVERTED if absent. */
+spmv_status_t spmv_set_format(spmv_handle_t h, spmv_format_t fmt);
+
+/* Device feature extraction (§8(a) row a3): integer moments, histogram
+ * order statistics and bandwidth on the device; exact-integer -> fp64
+ * formulas on the host. Synchronous; result cached on the handle. */
+spmv_status_t spmv_features(spmv_handle_t h, spmv_features_t* out);
+
+/* y <- alpha·A·x + beta·y with the active format's kernel (§8(a) row a5).
+ * x: device, n_cols values; y: device, n_rows values; dtype = handle dtype;
+ * x and y must not alias (exact equality -> INVALID_ARG). beta == 0: y is
+ * not read (NaN in y cannot propagate); alpha == 0: A is not read.
+ * Asynchronous on the handle's stream; fp32 data accumulates in fp64. */
+spmv_status_t spmv_run(spmv_handle_t h, double alpha, const void* x, double beta, void* y);
+
+/* Same with an explicit format (must be built) — used by tests and bench. */
+spmv_status_t spmv_run_format(spmv_handle_t h, spmv_format_t fmt, double alpha, const void* x,
+                              double beta, void* y);
+
+/* Override the launch variant used for `fmt` (block/maxreg/carveout/knob). */
+spmv_status_t spmv_set_launch(spmv_handle_t h, spmv_format_t fmt, const spmv_launch_t* v);
+spmv_status_t spmv_get_launch(spmv_handle_t h, spmv_format_t fmt, spmv_launch_t* v);
+
+/* The paper's two optimisation modes on B200 (§8(a) a6–a7).
+ * LAUNCH: time every launch variant of the active format, keep the fastest.
+ * FORMAT: features -> candidate formats -> convert + measure each -> gate:
+ *   switch away from CSR iff expected_iterations·(t_csr − t_best) >
+ *   f_latency + c_latency(best) (strict >). Uses scratch x/y (never
+ *   the caller's). Synchronous. Decisions appended to the JSON log. */
+spmv_status_t spmv_tune(spmv_handle_t h, uint32_t flags, int64_t expected_iterations,
+                        spmv_tune_report_t* out);
+
+/* ---------------------------------------------------------------- power iteration
+ * Power iteration (not in the paper):
+ *   z_k = alpha_k · A · z_{k−1},  alpha_k = 1/‖z_{k−1}‖,  x_k = z_{k−1}/‖z_{k−1}‖,
+ *   lambda_k = x_k · z_k.
+ * spmv_power_step launches ONE SpMV of the active format whose epilogue
+ * reads alpha from sums_prev (device, 2 doubles: [Σz², Σ x·z] of the
+ * previous step; alpha = 1/sqrt(sums_prev[0])) and writes this step's
+ * rank-local [Σz_i², Σ z_{k−1,row_offset+i}·z_i] to sums_out (device) —
+ * deterministic order. For a row slab of a larger matrix, `row_offset` is
+ * the slab's first global row (x is the full replicated vector). */
+spmv_status_t spmv_power_step(spmv_handle_t h, const void* x, void* y, const double* sums_prev,
+                              double* sums_out, int64_t row_offset);
+/* sums_out[0] = Σ x_i², sums_out[1] = 0 over n values of x (device). */
+spmv_status_t spmv_norm2(spmv_handle_t h, const void* x, int64_t n, double* sums_out);
+
+/* ---------------------------------------------------------------- introspection */
+spmv_status_t spmv_format_info(spmv_handle_t h, spmv_format_t fmt, spmv_format_info_t* out);
+/* Copy a format array into dst (`where` = host or device), dst_bytes >= array bytes. */
+spmv_status_t spmv_copy_array(spmv_handle_t h, spmv_array_t which, void* dst, int64_t dst_bytes,
+                              spmv_mem_t where);
+spmv_status_t spmv_get_format(spmv_handle_t h, spmv_format_t* fmt);
+spmv_status_t spmv_set_stream(spmv_handle_t h, void* cuda_stream);
+spmv_status_t spmv_destroy(spmv_handle_t h); /* NULL is a no-op */
+const char* spmv_status_string(spmv_status_t s);
+const char* spmv_last_error(spmv_handle_t h);
+/* JSON decision log of spmv_tune (array of records); returns the needed
+ * length incl. the terminating NUL; copies min(len, needed) bytes. */
+size_t spmv_decision_log(spmv_handle_t h, char* buf, size_t len);
+/* Conversion timings measured on the device by the last spmv_create /
+ * spmv_convert / spmv_features calls, seconds (c_latency per format, f_latency). */
+spmv_status_t spmv_overheads(spmv_handle_t h, double* f_latency_s, double* c_latency_s /*[5]*/);
+
+/* Number of CUDA kernels this library has launched in this process. */
+uint64_t spmv_launch_count(void);
+/* Release memory cached by the library's stream-ordered pool. */
+spmv_status_t spmv_trim_pool(int device);
+
+/* ---------------------------------------------------------------- multi-GPU host logic
+ * nnz-balanced row partition: bounds[0] = 0,
+ * bounds[world] = rows, bounds[k] = first row i with row_ptr[i] >=
+ * ceil(k·nnz/world). row_ptr is HOST int64 [rows+1]. Pure host integer code. */
+spmv_status_t spmv_dist_partition(int64_t rows, const int64_t* row_ptr, int world,
+                                  int64_t* bounds);
+/* Same partition computed from per-row lengths given as a host int64 array. */
+spmv_status_t spmv_dist_partition_lengths(int64_t rows, const int64_t* lengths, int world,
+                                          int64_t* bounds);
+/* Remap global column indices of a row slab (host or device int32 array,
+ * in place) into the padded all-gather layout: column c owned by rank
+ * r (bounds[r] <= c < bounds[r+1]) maps to r·chunk + (c − bounds[r]),
+ * chunk = max_r (bounds[r+1] − bounds[r]). */
+spmv_status_t spmv_dist_remap_columns(int32_t* col, int64_t nnz, const int64_t* bounds, int world,
+                                      spmv_mem_t where, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,835 @@
+// api.cu — the extern "C" boundary of libspmv.so (include/spmv.h).
+// Argument validation, handle lifecycle, format dispatch, the launch tuner
+// (compile-time mode analog), the format selector with its
+// overhead gate (run-time mode analog), the power step, and the
+// multi-GPU host logic (partition, column remap).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <sstream>
+#include <unordered_map>
+#include <vector>
+
+#include "spmv_common.cuh"
+
+namespace spmv {
+
+std::atomic<uint64_t> g_launches{0};
+
+namespace {
+std::mutex g_mu;
+bool g_pool_ready[64] = {};
+std::unordered_map<const void*, int> g_carveout;
+thread_local std::string g_err;
+}  // namespace
+
+void* dalloc(size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev >= 0 && dev < 64 && !g_pool_ready[dev]) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    g_pool_ready[dev] = true;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, bytes, s);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    // give cached pool memory back and retry once
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaStreamSynchronize(s);
+      cudaMemPoolTrimTo(pool, 0);
+    }
+    e = cudaMallocAsync(&p, bytes, s);
+  }
+  cuda_check(e, "cudaMallocAsync");
+  return p;
+}
+
+void dfree(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+
+void set_carveout(const void* func, int pct) {
+  if (pct < 0) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_carveout.find(func);
+  if (it != g_carveout.end() && it->second == pct) return;
+  CK(cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  g_carveout[func] = pct;
+}
+
+void ensure_pi_scratch(spmv_matrix* h, size_t nblocks) {
+  if (h->pi_partials && h->pi_partials_n >= nblocks) return;
+  CK(cudaStreamSynchronize(h->stream));
+  dfree(h->pi_partials, h->stream);
+  size_t n = std::max<size_t>(nblocks, 4096);
+  h->pi_partials = dalloc_n<double>(2 * (int64_t)n, h->stream);
+  h->pi_partials_n = n;
+  if (!h->pi_counter) {
+    h->pi_counter = dalloc_n<unsigned>(1, h->stream);
+    CK(cudaMemsetAsync(h->pi_counter, 0, sizeof(unsigned), h->stream));
+  }
+}
+
+void* ensure_seg_scratch(spmv_matrix* h, size_t bytes) {
+  if (h->seg_scratch && h->seg_scratch_bytes >= bytes) return h->seg_scratch;
+  CK(cudaStreamSynchronize(h->stream));
+  dfree(h->seg_scratch, h->stream);
+  h->seg_scratch = dalloc(bytes, h->stream);
+  h->seg_scratch_bytes = bytes;
+  return h->seg_scratch;
+}
+
+static int csr_default_lanes(const spmv_matrix* h) {
+  if (h->csr_T > 0) return h->csr_T;
+  double mean = h->rows > 0 ? (double)h->nnz / (double)h->rows : 0.0;
+  int t = 1;
+  while (t < (int)std::ceil(mean) && t < 32) t <<= 1;
+  return std::min(32, std::max(2, t));
+}
+
+spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t& L) {
+  spmv_launch_t r = L;
+  if (r.block == 0) r.block = 256;
+  if (r.maxreg == 0) r.maxreg = 255;
+  if (r.knob == 0) {
+    switch (fmt) {
+      case SPMV_FMT_CSR:
+        if (h->csr_alg == SPMV_CSR_MERGE) r.knob = 8;
+        else if (h->csr_alg == SPMV_CSR_SCALAR) r.knob = 1;
+        else r.knob = csr_default_lanes(h);
+        break;
+      case SPMV_FMT_ELL: r.knob = h->dtype == SPMV_R64F ? 64 : 128; break;
+      case SPMV_FMT_SELL: r.knob = (int)h->sell_C; break;
+      case SPMV_FMT_COO: r.knob = 4; break;
+      case SPMV_FMT_HYB: r.knob = 4; break;
+    }
+  }
+  return r;
+}
+
+static bool built(const spmv_matrix* h, int fmt) {
+  switch (fmt) {
+    case SPMV_FMT_CSR: return true;
+    case SPMV_FMT_COO: return h->coo_built;
+    case SPMV_FMT_ELL: return h->ell_built;
+    case SPMV_FMT_SELL: return h->sell_built;
+    case SPMV_FMT_HYB: return h->hyb_built;
+  }
+  return false;
+}
+
+// Launch one SpMV of format fmt (no validation).
+static void dispatch(spmv_matrix* h, int fmt, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L0) {
+  spmv_launch_t L = resolve_launch(h, fmt, L0);
+  if (e.mode == 0 && e.alpha == 0.0) {  // A is not read
+    run_scale(h, y, e.beta);
+    return;
+  }
+  switch (fmt) {
+    case SPMV_FMT_CSR: run_csr(h, e, x, y, L); break;
+    case SPMV_FMT_ELL: run_ell(h, e, x, y, L); break;
+    case SPMV_FMT_SELL: run_sell(h, e, x, y, L); break;
+    case SPMV_FMT_COO: run_coo(h, e, x, y, L); break;
+    case SPMV_FMT_HYB: run_hyb(h, e, x, y, L); break;
+    default: fail(SPMV_ERR_INVALID_ARG, "bad format");
+  }
+}
+
+static bool fused_norms(const spmv_matrix* h, int fmt) {
+  return fmt == SPMV_FMT_ELL || fmt == SPMV_FMT_SELL || (fmt == SPMV_FMT_CSR && h->csr_alg != SPMV_CSR_MERGE);
+}
+
+static void power_step(spmv_matrix* h, int fmt, const void* x, void* y, const double* sums_prev, double* sums_out,
+                       int64_t row_offset) {
+  Epilogue e;
+  e.mode = 1;
+  e.sums_prev = sums_prev;
+  e.sums_out = sums_out;
+  e.row_offset = row_offset;
+  if (h->rows == 0) {
+    CK(cudaMemsetAsync(sums_out, 0, 2 * sizeof(double), h->stream));
+    return;
+  }
+  ensure_pi_scratch(h, 4096);
+  e.partials = h->pi_partials;
+  e.counter = h->pi_counter;
+  dispatch(h, fmt, e, x, y, h->launch[fmt]);
+  if (!fused_norms(h, fmt)) run_norms(h, e, x, y, h->rows);
+}
+
+// ------------------------------------------------------------------ timing
+struct Events {
+  cudaEvent_t a, b;
+  Events() {
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+  }
+  ~Events() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+// Median-of-3 time per SpMV (seconds) for one (format, launch) on scratch x/y.
+static double time_variant(spmv_matrix* h, int fmt, const spmv_launch_t& L, const void* x, void* y) {
+  Epilogue e;
+  e.alpha = 1.0;
+  e.beta = 0.0;
+  Events ev;
+  for (int w = 0; w < 2; ++w) dispatch(h, fmt, e, x, y, L);
+  CK(cudaEventRecord(ev.a, h->stream));
+  dispatch(h, fmt, e, x, y, L);
+  CK(cudaEventRecord(ev.b, h->stream));
+  CK(cudaEventSynchronize(ev.b));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, ev.a, ev.b));
+  int reps = (int)std::min(200.0, std::max(3.0, std::ceil(2.0 / std::max(ms, 1e-3f))));
+  double t[3];
+  for (int trial = 0; trial < 3; ++trial) {
+    CK(cudaEventRecord(ev.a, h->stream));
+    for (int r = 0; r < reps; ++r) dispatch(h, fmt, e, x, y, L);
+    CK(cudaEventRecord(ev.b, h->stream));
+    CK(cudaEventSynchronize(ev.b));
+    CK(cudaEventElapsedTime(&ms, ev.a, ev.b));
+    t[trial] = ms * 1e-3 / reps;
+  }
+  std::sort(t, t + 3);
+  return t[1];
+}
+
+template <class T>
+__global__ void k_fill_one(T* p, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] = T(1);
+}
+
+struct TuneScratch {
+  spmv_matrix* h;
+  void* x = nullptr;
+  void* y = nullptr;
+  explicit TuneScratch(spmv_matrix* hh) : h(hh) {
+    x = dalloc((size_t)std::max<int64_t>(h->cols, 1) * h->vbytes, h->stream);
+    y = dalloc((size_t)std::max<int64_t>(h->rows, 1) * h->vbytes, h->stream);
+    if (h->dtype == SPMV_R64F) LAUNCH(k_fill_one<double>, grid_for(h->cols, 256), 256, 0, h->stream, (double*)x, h->cols);
+    else LAUNCH(k_fill_one<float>, grid_for(h->cols, 256), 256, 0, h->stream, (float*)x, h->cols);
+  }
+  ~TuneScratch() {
+    dfree(x, h->stream);
+    dfree(y, h->stream);
+  }
+};
+
+static const char* fmt_name(int f) {
+  static const char* n[] = {"COO", "CSR", "ELL", "HYB", "SELL"};
+  return (f >= 0 && f < 5) ? n[f] : "?";
+}
+
+static void log_append(spmv_matrix* h, const std::string& rec) {
+  if (!h->log.empty()) h->log += ",";
+  h->log += rec;
+}
+
+// Knob values tried per format by the launch sweep.
+static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
+  switch (fmt) {
+    case SPMV_FMT_CSR:
+      if (h->csr_alg == SPMV_CSR_MERGE) return {4, 8, 16};
+      {
+        int t = csr_default_lanes(h);
+        std::vector<int> v{t};
+        if (t / 2 >= 1) v.push_back(t / 2);
+        if (t * 2 <= 32) v.push_back(t * 2);
+        return v;
+      }
+    case SPMV_FMT_ELL:
+      return h->dtype == SPMV_R64F ? std::vector<int>{32, 64, 128} : std::vector<int>{32, 64, 128};
+    case SPMV_FMT_SELL: return {(int)h->sell_C};
+    case SPMV_FMT_COO: return {2, 4, 8};
+    case SPMV_FMT_HYB: return {2, 4, 8};
+  }
+  return {0};
+}
+
+// Compile-time mode analog: sweep block × maxreg × carveout × knob
+// for the active format; keep the argmin of the median time.
+static void tune_launch(spmv_matrix* h, int fmt, TuneScratch& ts, spmv_tune_report_t* rep) {
+  static const int blocks[] = {64, 128, 256, 512, 1024};
+  static const int regs[] = {32, 64, 128, 255};
+  static const int carve[] = {0, 25, 50, 100};
+  spmv_launch_t best = resolve_launch(h, fmt, h->launch[fmt]);
+  double tbest = time_variant(h, fmt, best, ts.x, ts.y);
+  int n = 1;
+  std::ostringstream os;
+  os << "{\"kind\":\"launch_sweep\",\"format\":\"" << fmt_name(fmt) << "\",\"variants\":[";
+  bool first = true;
+  for (int knob : knob_set(h, fmt))
+    for (int b : blocks)
+      for (int r : regs)
+        for (int c : carve) {
+          spmv_launch_t L{b, r, c, knob};
+          double t;
+          try {
+            t = time_variant(h, fmt, L, ts.x, ts.y);
+          } catch (const SpmvError&) {
+            cudaGetLastError();
+            continue;
+          }
+          ++n;
+          os << (first ? "" : ",") << "[" << b << "," << r << "," << c << "," << knob << "," << t << "]";
+          first = false;
+          if (t < tbest) {
+            tbest = t;
+            best = L;
+          }
+        }
+  os << "],\"best\":[" << best.block << "," << best.maxreg << "," << best.carveout_pct << "," << best.knob
+     << "],\"t_best_s\":" << tbest << "}";
+  log_append(h, os.str());
+  h->launch[fmt] = best;
+  if (rep) {
+    rep->launch = best;
+    rep->t_best_s = tbest;
+    rep->n_variants += n;
+  }
+}
+
+static double sell_padding(const spmv_matrix* h) {
+  return h->sell_slots > 0 ? 1.0 - (double)h->nnz / (double)h->sell_slots : 0.0;
+}
+
+// Run-time mode analog: features -> candidates -> measure -> gate.
+static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tune_report_t* rep) {
+  if (!h->have_features) compute_features(h);
+  const spmv_features_t& f = h->feat;
+  const int orig_alg = h->csr_alg;
+  std::ostringstream os;
+  os.precision(9);
+  os << "{\"kind\":\"format_select\",\"features\":{\"n\":" << f.n_rows << ",\"nnz\":" << f.nnz
+     << ",\"mean\":" << f.mean << ",\"var\":" << f.var << ",\"std\":" << f.std << ",\"max\":" << f.max_len
+     << ",\"ell_ratio\":" << f.ell_ratio << ",\"median\":" << f.median << ",\"mode\":" << f.mode
+     << ",\"bandwidth\":" << f.bandwidth << "},\"candidates\":[";
+  struct Cand {
+    int fmt;
+    int alg;
+    double t, c;
+    std::string why;
+  };
+  std::vector<Cand> cands;
+  // CSR (paper default): CSR-vector with T from the mean.
+  h->csr_alg = SPMV_CSR_VECTOR;
+  double t_csr = time_variant(h, SPMV_FMT_CSR, resolve_launch(h, SPMV_FMT_CSR, spmv_launch_t{0, 0, -1, 0}), ts.x, ts.y);
+  cands.push_back({SPMV_FMT_CSR, SPMV_CSR_VECTOR, t_csr, 0.0, "default"});
+  const bool skewed = (f.mean > 0 && f.std / f.mean > 1.0) || (double)f.max_len > 32.0 * f.mean;
+  if (skewed) {
+    h->csr_alg = SPMV_CSR_MERGE;
+    double t = time_variant(h, SPMV_FMT_CSR, resolve_launch(h, SPMV_FMT_CSR, spmv_launch_t{0, 0, -1, 0}), ts.x, ts.y);
+    cands.push_back({SPMV_FMT_CSR, SPMV_CSR_MERGE, t, 0.0, "std/mean>1 or max>32*mean"});
+  }
+  h->csr_alg = orig_alg;
+  auto try_build = [&](int fmt, const char* why) {
+    bool was = built(h, fmt);
+    try {
+      if (!was) {
+        switch (fmt) {
+          case SPMV_FMT_ELL: build_ell(h); break;
+          case SPMV_FMT_SELL: build_sell(h, h->dtype == SPMV_R64F ? 64 : 128, 1); break;
+          case SPMV_FMT_HYB: build_hyb(h, -1); break;
+          case SPMV_FMT_COO: build_coo(h); break;
+        }
+      }
+    } catch (const SpmvError& e) {
+      cudaGetLastError();
+      os << "{\"format\":\"" << fmt_name(fmt) << "\",\"rejected\":\"" << e.msg << "\"},";
+      return;
+    }
+    if (fmt == SPMV_FMT_SELL && sell_padding(h) > 0.10) {
+      os << "{\"format\":\"SELL\",\"rejected\":\"padding " << sell_padding(h) << " > 0.10\"},";
+      if (!was) free_format(h, fmt);
+      return;
+    }
+    double t = time_variant(h, fmt, resolve_launch(h, fmt, h->launch[fmt]), ts.x, ts.y);
+    cands.push_back({fmt, 0, t, h->c_latency[fmt], why});
+  };
+  if (f.ell_ratio >= 0.9) try_build(SPMV_FMT_ELL, "ell_ratio>=0.9");
+  if (f.ell_ratio >= 0.5 || !skewed) try_build(SPMV_FMT_SELL, "sell padding<=10%");
+  if (skewed) {
+    try_build(SPMV_FMT_HYB, "skewed rows");
+    try_build(SPMV_FMT_COO, "skewed rows");
+  }
+  size_t bi = 0;
+  for (size_t i = 0; i < cands.size(); ++i) {
+    const Cand& c = cands[i];
+    os << "{\"format\":\"" << fmt_name(c.fmt) << "\"" << (c.alg == SPMV_CSR_MERGE ? ",\"alg\":\"merge\"" : "")
+       << ",\"t_s\":" << c.t << ",\"c_latency_s\":" << c.c << ",\"why\":\"" << c.why << "\"}"
+       << (i + 1 < cands.size() ? "," : "");
+    if (c.t < cands[bi].t) bi = i;
+  }
+  const Cand& best = cands[bi];
+  const double gain = (double)iters * (t_csr - best.t);
+  const double overhead = h->f_latency + best.c;
+  const bool convert = gain > overhead;  // strict
+  const int chosen = convert ? best.fmt : SPMV_FMT_CSR;
+  const int chosen_alg = convert ? best.alg : SPMV_CSR_VECTOR;
+  os << "],\"gate\":{\"expected_iterations\":" << iters << ",\"t_csr_s\":" << t_csr << ",\"t_best_s\":" << best.t
+     << ",\"gain_s\":" << gain << ",\"f_latency_s\":" << h->f_latency << ",\"c_latency_s\":" << best.c
+     << ",\"convert\":" << (convert ? "true" : "false") << "},\"chosen\":\"" << fmt_name(chosen)
+     << (chosen == SPMV_FMT_CSR && chosen_alg == SPMV_CSR_MERGE ? "-merge" : "") << "\"}";
+  log_append(h, os.str());
+  // release candidates that were built here and not chosen
+  for (const Cand& c : cands)
+    if (c.fmt != chosen && c.fmt != SPMV_FMT_CSR) free_format(h, c.fmt);
+  h->active = chosen;
+  if (chosen == SPMV_FMT_CSR) h->csr_alg = chosen_alg;
+  if (rep) {
+    rep->format = chosen;
+    rep->t_csr_s = t_csr;
+    rep->t_best_s = convert ? best.t : t_csr;
+    rep->f_latency_s = h->f_latency;
+    rep->c_latency_s = best.c;
+    rep->expected_iterations = iters;
+    rep->converted = convert ? 1 : 0;
+    rep->n_candidates = (int32_t)cands.size();
+    rep->params.csr_alg = h->csr_alg;
+    rep->params.csr_T = h->csr_T;
+    rep->params.sell_C = (int32_t)h->sell_C;
+    rep->params.sell_sigma = (int32_t)h->sell_sigma;
+    rep->params.hyb_K = h->hyb_K;
+  }
+}
+
+static void destroy_handle(spmv_matrix* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  for (int f = 0; f < SPMV_NUM_FORMATS; ++f) free_format(h, f);
+  dfree(h->seg_scratch, h->stream);
+  dfree(h->pi_partials, h->stream);
+  dfree(h->pi_counter, h->stream);
+  cudaStreamSynchronize(h->stream);
+  delete h;
+}
+
+struct DeviceGuard {
+  explicit DeviceGuard(int dev) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) CK(cudaSetDevice(dev));
+  }
+};
+
+}  // namespace spmv
+
+namespace spmv {
+__global__ void k_remap(int32_t* col, int64_t nnz, const int64_t* bounds, int world, int64_t chunk) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+    const int64_t c = col[i];
+    int lo = 0, hi = world - 1;  // owner: last r with bounds[r] <= c
+    while (lo < hi) {
+      int mid = (lo + hi + 1) / 2;
+      if (bounds[mid] <= c) lo = mid;
+      else hi = mid - 1;
+    }
+    col[i] = (int32_t)(lo * chunk + (c - bounds[lo]));
+  }
+}
+}  // namespace spmv
+
+using namespace spmv;
+
+#define API_TRY try {
+#define API_CATCH(h)                                          \
+  }                                                           \
+  catch (const SpmvError& e) {                                \
+    g_err = e.msg;                                            \
+    if (h) (h)->last_error = e.msg;                           \
+    return e.status;                                          \
+  }                                                           \
+  catch (const std::bad_alloc&) {                             \
+    g_err = "host allocation failed";                         \
+    return SPMV_ERR_OUT_OF_MEMORY;                            \
+  }                                                           \
+  return SPMV_OK;
+
+static spmv_matrix* const kNoHandle = nullptr;
+
+extern "C" {
+
+spmv_status_t spmv_create(spmv_handle_t* out, int64_t rows, int64_t cols, int64_t nnz, const int32_t* row_idx,
+                          const int32_t* col_idx, const void* vals, spmv_dtype_t dtype, spmv_mem_t where,
+                          int device, void* cuda_stream) {
+  if (!out) return SPMV_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (rows < 0 || cols < 0 || nnz < 0) return SPMV_ERR_INVALID_ARG;
+  if (dtype != SPMV_R32F && dtype != SPMV_R64F) return SPMV_ERR_INVALID_ARG;
+  if (where != SPMV_MEM_HOST && where != SPMV_MEM_DEVICE) return SPMV_ERR_INVALID_ARG;
+  if (nnz > 0 && (!row_idx || !col_idx || !vals)) return SPMV_ERR_INVALID_ARG;
+  if (rows > INT32_MAX || cols > INT32_MAX) return SPMV_ERR_UNSUPPORTED;
+  if (nnz > 0 && (rows == 0 || cols == 0)) return SPMV_ERR_INDEX_OUT_OF_RANGE;
+  spmv_matrix* h = nullptr;
+  API_TRY
+  DeviceGuard g(device);
+  h = new spmv_matrix();
+  h->device = device;
+  h->stream = static_cast<cudaStream_t>(cuda_stream);
+  h->dtype = dtype;
+  h->vbytes = dtype == SPMV_R64F ? 8 : 4;
+  h->rows = rows;
+  h->cols = cols;
+  h->nnz = nnz;
+  for (auto& L : h->launch) L = spmv_launch_t{0, 0, -1, 0};
+  try {
+    ingest(h, row_idx, col_idx, vals, where);
+  } catch (...) {
+    destroy_handle(h);
+    h = nullptr;
+    throw;
+  }
+  *out = h;
+  API_CATCH(kNoHandle)
+}
+
+spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format_params_t* p) {
+  if (!h) return SPMV_ERR_INVALID_ARG;
+  if (fmt < 0 || fmt >= SPMV_NUM_FORMATS) return SPMV_ERR_INVALID_ARG;
+  API_TRY
+  DeviceGuard g(h->device);
+  spmv_format_params_t q{};
+  q.hyb_K = -1;
+  if (p) q = *p;
+  switch (fmt) {
+    case SPMV_FMT_CSR:
+      if (q.csr_alg < 0 || q.csr_alg > SPMV_CSR_MERGE) fail(SPMV_ERR_INVALID_ARG, "bad csr_alg");
+      if (q.csr_T != 0 && (q.csr_T < 1 || q.csr_T > 32 || (q.csr_T & (q.csr_T - 1))))
+        fail(SPMV_ERR_INVALID_ARG, "csr_T must be a power of two in [1, 32]");
+      h->csr_alg = q.csr_alg;
+      h->csr_T = q.csr_T;
+      h->launch[SPMV_FMT_CSR].knob = 0;
+      break;
+    case SPMV_FMT_COO:
+      if (!h->coo_built) build_coo(h);
+      break;
+    case SPMV_FMT_ELL:
+      if (!h->ell_built) build_ell(h);
+      break;
+    case SPMV_FMT_SELL: {
+      int64_t C = q.sell_C ? q.sell_C : (h->dtype == SPMV_R64F ? 64 : 128);
+      int64_t sigma = q.sell_sigma ? q.sell_sigma : 1;
+      if (C != 32 && C != 64 && C != 128 && C != 256) fail(SPMV_ERR_UNSUPPORTED, "SELL C must be 32, 64, 128 or 256");
+      if (sigma < 1 || (sigma != 1 && sigma % C != 0)) fail(SPMV_ERR_INVALID_ARG, "SELL sigma must be 1 or a multiple of C");
+      if (!h->sell_built || h->sell_C != C || h->sell_sigma != sigma) {
+        if (h->sell_built) free_format(h, SPMV_FMT_SELL);
+        build_sell(h, C, sigma);
+      }
+      break;
+    }
+    case SPMV_FMT_HYB: {
+      int64_t K = q.hyb_K;
+      if (K < -1) fail(SPMV_ERR_INVALID_ARG, "hyb_K must be >= -1");
+      if (!h->have_features) compute_features(h);
+      int64_t want = K < 0 ? h->hyb_auto_K : std::min<int64_t>(K, h->feat.max_len);
+      if (!h->hyb_built || h->hyb_K != want) {
+        if (h->hyb_built) free_format(h, SPMV_FMT_HYB);
+        build_hyb(h, want);
+      }
+      break;
+    }
+  }
+  h->active = fmt;
+  CK(cudaStreamSynchronize(h->stream));
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_set_format(spmv_handle_t h, spmv_format_t fmt) {
+  if (!h || fmt < 0 || fmt >= SPMV_NUM_FORMATS) return SPMV_ERR_INVALID_ARG;
+  if (!built(h, fmt)) return SPMV_ERR_NOT_CONVERTED;
+  h->active = fmt;
+  return SPMV_OK;
+}
+
+spmv_status_t spmv_get_format(spmv_handle_t h, spmv_format_t* fmt) {
+  if (!h || !fmt) return SPMV_ERR_INVALID_ARG;
+  *fmt = (spmv_format_t)h->active;
+  return SPMV_OK;
+}
+
+spmv_status_t spmv_features(spmv_handle_t h, spmv_features_t* out) {
+  if (!h || !out) return SPMV_ERR_INVALID_ARG;
+  API_TRY
+  DeviceGuard g(h->device);
+  compute_features(h);
+  *out = h->feat;
+  API_CATCH(h)
+}
+
+static spmv_status_t run_common(spmv_handle_t h, int fmt, double alpha, const void* x, double beta, void* y) {
+  if (!h) return SPMV_ERR_INVALID_ARG;
+  if (fmt < 0 || fmt >= SPMV_NUM_FORMATS) return SPMV_ERR_INVALID_ARG;
+  if ((!x && h->cols > 0 && alpha != 0.0) || (!y && h->rows > 0)) return SPMV_ERR_INVALID_ARG;
+  if (x && x == y) return SPMV_ERR_INVALID_ARG;
+  if (!built(h, fmt)) return SPMV_ERR_NOT_CONVERTED;
+  if (h->rows == 0) return SPMV_OK;
+  API_TRY
+  DeviceGuard g(h->device);
+  Epilogue e;
+  e.alpha = alpha;
+  e.beta = beta;
+  dispatch(h, fmt, e, x, y, h->launch[fmt]);
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_run(spmv_handle_t h, double alpha, const void* x, double beta, void* y) {
+  if (!h) return SPMV_ERR_INVALID_ARG;
+  return run_common(h, h->active, alpha, x, beta, y);
+}
+
+spmv_status_t spmv_run_format(spmv_handle_t h, spmv_format_t fmt, double alpha, const void* x, double beta, void* y) {
+  return run_common(h, fmt, alpha, x, beta, y);
+}
+
+spmv_status_t spmv_set_launch(spmv_handle_t h, spmv_format_t fmt, const spmv_launch_t* v) {
+  if (!h || !v || fmt < 0 || fmt >= SPMV_NUM_FORMATS) return SPMV_ERR_INVALID_ARG;
+  API_TRY
+  spmv_launch_t L = *v;
+  if (L.block) block_index(L.block);
+  if (L.maxreg) reg_index(L.maxreg);
+  if (L.carveout_pct > 100) fail(SPMV_ERR_INVALID_ARG, "carveout must be -1 or 0..100");
+  h->launch[fmt] = L;
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_get_launch(spmv_handle_t h, spmv_format_t fmt, spmv_launch_t* v) {
+  if (!h || !v || fmt < 0 || fmt >= SPMV_NUM_FORMATS) return SPMV_ERR_INVALID_ARG;
+  API_TRY
+  *v = resolve_launch(h, fmt, h->launch[fmt]);
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_tune(spmv_handle_t h, uint32_t flags, int64_t expected_iterations, spmv_tune_report_t* out) {
+  if (!h || (flags & ~SPMV_TUNE_ALL) || flags == 0 || expected_iterations < 0) return SPMV_ERR_INVALID_ARG;
+  if (h->rows == 0 || h->nnz == 0) return SPMV_ERR_INVALID_ARG;
+  API_TRY
+  DeviceGuard g(h->device);
+  spmv_tune_report_t rep{};
+  rep.format = h->active;
+  rep.expected_iterations = expected_iterations;
+  TuneScratch ts(h);
+  if (flags & SPMV_TUNE_FORMAT) tune_format(h, expected_iterations, ts, &rep);
+  if (flags & SPMV_TUNE_LAUNCH) tune_launch(h, h->active, ts, &rep);
+  rep.format = h->active;
+  rep.launch = resolve_launch(h, h->active, h->launch[h->active]);
+  CK(cudaStreamSynchronize(h->stream));
+  if (out) *out = rep;
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_power_step(spmv_handle_t h, const void* x, void* y, const double* sums_prev, double* sums_out,
+                              int64_t row_offset) {
+  if (!h || !x || !y || !sums_prev || !sums_out || x == y || row_offset < 0) return SPMV_ERR_INVALID_ARG;
+  if (!built(h, h->active)) return SPMV_ERR_NOT_CONVERTED;
+  API_TRY
+  DeviceGuard g(h->device);
+  power_step(h, h->active, x, y, sums_prev, sums_out, row_offset);
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_norm2(spmv_handle_t h, const void* x, int64_t n, double* sums_out) {
+  if (!h || !sums_out || n < 0 || (n > 0 && !x)) return SPMV_ERR_INVALID_ARG;
+  API_TRY
+  DeviceGuard g(h->device);
+  if (n == 0) {
+    CK(cudaMemsetAsync(sums_out, 0, 2 * sizeof(double), h->stream));
+  } else {
+    Epilogue e;
+    e.mode = 1;
+    e.sums_out = sums_out;
+    run_norms(h, e, nullptr, x, n);
+  }
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_format_info(spmv_handle_t h, spmv_format_t fmt, spmv_format_info_t* o) {
+  if (!h || !o || fmt < 0 || fmt >= SPMV_NUM_FORMATS) return SPMV_ERR_INVALID_ARG;
+  std::memset(o, 0, sizeof(*o));
+  o->present = built(h, fmt) ? 1 : 0;
+  o->row_ptr_is64 = h->rp64 ? 1 : 0;
+  switch (fmt) {
+    case SPMV_FMT_ELL: o->K = h->ell_K; o->n_pad = h->ell_npad; o->slots = h->ell_K * h->ell_npad; break;
+    case SPMV_FMT_SELL:
+      o->C = h->sell_C; o->sigma = h->sell_sigma; o->n_slices = h->sell_ns; o->slots = h->sell_slots;
+      break;
+    case SPMV_FMT_HYB:
+      o->K = h->hyb_K; o->n_pad = h->hyb_npad; o->slots = h->hyb_K * h->hyb_npad; o->tail_nnz = h->hyb_tail;
+      break;
+    case SPMV_FMT_COO: o->n_empty_rows = h->coo_n_empty; break;
+    default: break;
+  }
+  o->stored_bytes = o->present ? format_stored_bytes(h, fmt) : 0;
+  return SPMV_OK;
+}
+
+spmv_status_t spmv_copy_array(spmv_handle_t h, spmv_array_t which, void* dst, int64_t dst_bytes, spmv_mem_t where) {
+  if (!h || (!dst && dst_bytes > 0) || (where != SPMV_MEM_HOST && where != SPMV_MEM_DEVICE)) return SPMV_ERR_INVALID_ARG;
+  const void* src = nullptr;
+  int64_t bytes = 0;
+  const int64_t vb = h->vbytes;
+  bool need = true;
+  switch (which) {
+    case SPMV_ARR_CSR_ROW_PTR: src = h->row_ptr; bytes = (h->rows + 1) * (h->rp64 ? 8 : 4); break;
+    case SPMV_ARR_CSR_COL: src = h->col; bytes = h->nnz * 4; break;
+    case SPMV_ARR_CSR_VAL: src = h->val; bytes = h->nnz * vb; break;
+    case SPMV_ARR_COO_ROW: need = h->coo_built; src = h->coo_row; bytes = h->nnz * 4; break;
+    case SPMV_ARR_COO_EMPTY_ROWS: need = h->coo_built; src = h->coo_empty; bytes = h->coo_n_empty * 4; break;
+    case SPMV_ARR_ELL_COL: need = h->ell_built; src = h->ell_col; bytes = h->ell_K * h->ell_npad * 4; break;
+    case SPMV_ARR_ELL_VAL: need = h->ell_built; src = h->ell_val; bytes = h->ell_K * h->ell_npad * vb; break;
+    case SPMV_ARR_SELL_PERM: need = h->sell_built; src = h->sell_perm; bytes = h->rows * 4; break;
+    case SPMV_ARR_SELL_SLICE_PTR: need = h->sell_built; src = h->sell_sp; bytes = (h->sell_ns + 1) * 8; break;
+    case SPMV_ARR_SELL_COL: need = h->sell_built; src = h->sell_col; bytes = h->sell_slots * 4; break;
+    case SPMV_ARR_SELL_VAL: need = h->sell_built; src = h->sell_val; bytes = h->sell_slots * vb; break;
+    case SPMV_ARR_HYB_ELL_COL: need = h->hyb_built; src = h->hyb_ecol; bytes = h->hyb_K * h->hyb_npad * 4; break;
+    case SPMV_ARR_HYB_ELL_VAL: need = h->hyb_built; src = h->hyb_eval; bytes = h->hyb_K * h->hyb_npad * vb; break;
+    case SPMV_ARR_HYB_TAIL_ROW: need = h->hyb_built; src = h->hyb_trow; bytes = h->hyb_tail * 4; break;
+    case SPMV_ARR_HYB_TAIL_COL: need = h->hyb_built; src = h->hyb_tcol; bytes = h->hyb_tail * 4; break;
+    case SPMV_ARR_HYB_TAIL_VAL: need = h->hyb_built; src = h->hyb_tval; bytes = h->hyb_tail * vb; break;
+    default: return SPMV_ERR_INVALID_ARG;
+  }
+  if (!need) return SPMV_ERR_NOT_CONVERTED;
+  if (dst_bytes < bytes) return SPMV_ERR_INVALID_ARG;
+  API_TRY
+  DeviceGuard g(h->device);
+  if (which == SPMV_ARR_SELL_PERM && !h->sell_perm) {
+    // sigma == 1: identity permutation
+    std::vector<int32_t> id((size_t)h->rows);
+    for (int64_t i = 0; i < h->rows; ++i) id[(size_t)i] = (int32_t)i;
+    CK(cudaMemcpyAsync(dst, id.data(), bytes, where == SPMV_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice,
+                       h->stream));
+  } else if (bytes > 0) {
+    CK(cudaMemcpyAsync(dst, src, bytes, where == SPMV_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                       h->stream));
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_set_stream(spmv_handle_t h, void* s) {
+  if (!h) return SPMV_ERR_INVALID_ARG;
+  API_TRY
+  DeviceGuard g(h->device);
+  CK(cudaStreamSynchronize(h->stream));
+  h->stream = static_cast<cudaStream_t>(s);
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_destroy(spmv_handle_t h) {
+  if (!h) return SPMV_OK;
+  destroy_handle(h);
+  return SPMV_OK;
+}
+
+const char* spmv_status_string(spmv_status_t s) {
+  switch (s) {
+    case SPMV_OK: return "SPMV_OK";
+    case SPMV_ERR_INVALID_ARG: return "SPMV_ERR_INVALID_ARG";
+    case SPMV_ERR_INDEX_OUT_OF_RANGE: return "SPMV_ERR_INDEX_OUT_OF_RANGE";
+    case SPMV_ERR_DUPLICATE: return "SPMV_ERR_DUPLICATE";
+    case SPMV_ERR_INFEASIBLE: return "SPMV_ERR_INFEASIBLE";
+    case SPMV_ERR_OUT_OF_MEMORY: return "SPMV_ERR_OUT_OF_MEMORY";
+    case SPMV_ERR_UNSUPPORTED: return "SPMV_ERR_UNSUPPORTED";
+    case SPMV_ERR_CUDA: return "SPMV_ERR_CUDA";
+    case SPMV_ERR_NOT_CONVERTED: return "SPMV_ERR_NOT_CONVERTED";
+  }
+  return "SPMV_ERR_UNKNOWN";
+}
+
+const char* spmv_last_error(spmv_handle_t h) { return h ? h->last_error.c_str() : g_err.c_str(); }
+
+size_t spmv_decision_log(spmv_handle_t h, char* buf, size_t len) {
+  if (!h) return 0;
+  std::string s = "[" + h->log + "]";
+  size_t need = s.size() + 1;
+  if (buf && len > 0) {
+    size_t n = std::min(len - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  }
+  return need;
+}
+
+spmv_status_t spmv_overheads(spmv_handle_t h, double* f_latency_s, double* c_latency_s) {
+  if (!h) return SPMV_ERR_INVALID_ARG;
+  if (f_latency_s) *f_latency_s = h->f_latency;
+  if (c_latency_s)
+    for (int i = 0; i < SPMV_NUM_FORMATS; ++i) c_latency_s[i] = h->c_latency[i];
+  return SPMV_OK;
+}
+
+uint64_t spmv_launch_count(void) { return g_launches.load(); }
+
+spmv_status_t spmv_trim_pool(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return SPMV_ERR_CUDA;
+  cudaDeviceSynchronize();
+  if (cudaMemPoolTrimTo(pool, 0) != cudaSuccess) return SPMV_ERR_CUDA;
+  return SPMV_OK;
+}
+
+// ------------------------------------------------------------------ multi-GPU host logic
+spmv_status_t spmv_dist_partition(int64_t rows, const int64_t* row_ptr, int world, int64_t* bounds) {
+  if (rows < 0 || !row_ptr || world < 1 || !bounds) return SPMV_ERR_INVALID_ARG;
+  const int64_t nnz = row_ptr[rows];
+  bounds[0] = 0;
+  bounds[world] = rows;
+  for (int k = 1; k < world; ++k) {
+    const unsigned __int128 num = (unsigned __int128)k * (unsigned __int128)(nnz < 0 ? 0 : nnz);
+    const int64_t target = (int64_t)((num + (unsigned)world - 1) / (unsigned)world);
+    bounds[k] = std::lower_bound(row_ptr, row_ptr + rows + 1, target) - row_ptr;
+  }
+  return SPMV_OK;
+}
+
+spmv_status_t spmv_dist_partition_lengths(int64_t rows, const int64_t* lengths, int world, int64_t* bounds) {
+  if (rows < 0 || !lengths || world < 1 || !bounds) return SPMV_ERR_INVALID_ARG;
+  try {
+    std::vector<int64_t> rp((size_t)rows + 1);
+    rp[0] = 0;
+    for (int64_t i = 0; i < rows; ++i) rp[(size_t)i + 1] = rp[(size_t)i] + lengths[i];
+    return spmv_dist_partition(rows, rp.data(), world, bounds);
+  } catch (const std::bad_alloc&) {
+    return SPMV_ERR_OUT_OF_MEMORY;
+  }
+}
+
+
+spmv_status_t spmv_dist_remap_columns(int32_t* col, int64_t nnz, const int64_t* bounds, int world, spmv_mem_t where,
+                                      void* cuda_stream) {
+  if ((!col && nnz > 0) || !bounds || world < 1 || nnz < 0) return SPMV_ERR_INVALID_ARG;
+  int64_t chunk = 0;
+  for (int r = 0; r < world; ++r) chunk = std::max(chunk, bounds[r + 1] - bounds[r]);
+  if (chunk * world > INT32_MAX) return SPMV_ERR_UNSUPPORTED;
+  if (where == SPMV_MEM_HOST) {
+    for (int64_t i = 0; i < nnz; ++i) {
+      const int64_t c = col[i];
+      const int r = (int)(std::upper_bound(bounds, bounds + world, c) - bounds) - 1;
+      col[i] = (int32_t)(r * chunk + (c - bounds[r]));
+    }
+    return SPMV_OK;
+  }
+  API_TRY
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  int64_t* db = dalloc_n<int64_t>(world + 1, s);
+  CK(cudaMemcpyAsync(db, bounds, (world + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  if (nnz > 0) LAUNCH(k_remap, grid_for(nnz, 256), 256, 0, s, col, nnz, (const int64_t*)db, world, chunk);
+  dfree(db, s);
+  CK(cudaStreamSynchronize(s));
+  API_CATCH(kNoHandle)
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// common.cuh — shared internals of libspmv.so (product side only).
+// Error model: internal C++ code throws SpmvError; every extern "C" entry
+// point in api.cu catches it and returns the status code (include/spmv.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "../../include/spmv.h"
+
+namespace spmv {
+
+struct SpmvError {
+  spmv_status_t status;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(spmv_status_t s, const std::string& m) { throw SpmvError{s, m}; }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      fail(SPMV_ERR_OUT_OF_MEMORY, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+    fail(SPMV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define CK(call) ::spmv::cuda_check((call), #call)
+
+// Every kernel launch of the library goes through LAUNCH so the process-wide
+// launch counter (spmv_launch_count) is exact.
+extern std::atomic<uint64_t> g_launches;
+#define LAUNCH(kern, grid, block, smem, stream, ...)                                  \
+  do {                                                                                \
+    kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                         \
+    ::spmv::g_launches.fetch_add(1, std::memory_order_relaxed);                       \
+    ::spmv::cuda_check(cudaGetLastError(), #kern);                                    \
+  } while (0)
+
+// Stream-ordered device allocation from the device's default pool (release
+// threshold raised once per device so repeated create/destroy reuses memory).
+void* dalloc(size_t bytes, cudaStream_t s);
+void dfree(void* p, cudaStream_t s);
+
+template <class T>
+T* dalloc_n(int64_t n, cudaStream_t s) {
+  return static_cast<T*>(dalloc((size_t)(n > 0 ? n : 1) * sizeof(T), s));
+}
+
+// Stream-ordered scratch buffers released when the scope ends (also on throw).
+struct Scratch {
+  cudaStream_t s;
+  void* p[16] = {};
+  int n = 0;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  template <class T>
+  T* get(int64_t count) {
+    T* q = dalloc_n<T>(count, s);
+    p[n++] = q;
+    return q;
+  }
+  void keep(void* q) {  // ownership moved elsewhere
+    for (int i = 0; i < n; ++i)
+      if (p[i] == q) p[i] = nullptr;
+  }
+  ~Scratch() {
+    for (int i = 0; i < n; ++i)
+      if (p[i]) dfree(p[i], s);
+  }
+};
+
+inline unsigned grid_for(int64_t n, int block, int64_t cap = 148LL * 32) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+constexpr int kNumSMs = 148;
+
+// ---------------------------------------------------------------- device helpers
+
+// Streaming loads of the matrix arrays: read once per SpMV, so do not allocate
+// in L1 and mark evict-first in L2 (x stays resident instead).
+__device__ __forceinline__ int ld_stream(const int* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int2 ld_stream(const int2* p) {
+  int2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0,%1}, [%2];"
+               : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float2 ld_stream(const float2* p) {
+  float2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];"
+               : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+               : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+
+// Gathers of x: read-only path, keep in L1, evict-last in L2 (x is reused by
+// every row that touches the column).
+__device__ __forceinline__ double ld_x(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_x(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+
+template <class T>
+__device__ __forceinline__ double widen(T v) {
+  return (double)v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace spmv

@@ -1,0 +1,427 @@
+// convert.cu — on-device format builds, spmv_convert.
+// The paper converts COO to each format on the CPU (c_latency);
+// here every build is a handful of bandwidth-bound kernels over the CSR:
+//   ELL: column-major [K][n_pad], n_pad = ceil(rows/128)·128,
+//        padding (col −1, +0.0) so padding never multiplies x (reading R9);
+//   SELL (generalised to SELL-C-sigma, reading R10): sigma-window
+//        sort of rows by length (descending, ties by row) via the stable
+//        radix sort, slice widths, exclusive scan -> int64 slice_ptr, fill;
+//   HYB  (north star; Bell–Garland): ELL part of width K_h + COO tail;
+//   COO: expanded row array + the list of empty rows.
+#include <algorithm>
+
+#include "handle.cuh"
+#include "primitives.cuh"
+
+namespace spmv {
+namespace {
+
+// ---------------------------------------------------------------- ELL
+template <class RP, class V>
+__global__ void k_ell_fill(const RP* __restrict__ rp, const int32_t* __restrict__ col,
+                           const V* __restrict__ val, int64_t rows, int64_t K, int64_t n_pad,
+                           int32_t* __restrict__ colE, V* __restrict__ valE) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
+    int64_t a = 0, L = 0;
+    if (i < rows) {
+      a = rp[i];
+      L = rp[i + 1] - a;
+      if (L > K) L = K;
+    }
+    for (int64_t k = 0; k < K; ++k) {
+      int64_t pos = k * n_pad + i;
+      if (k < L) {
+        colE[pos] = col[a + k];
+        valE[pos] = val[a + k];
+      } else {
+        colE[pos] = -1;
+        valE[pos] = V(0);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- SELL
+template <class RP>
+__global__ void k_sell_keys(const RP* __restrict__ rp, int64_t rows, int64_t sigma, int lenbits,
+                            int64_t maxlen, uint64_t* __restrict__ keys) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
+    int64_t L = rp[i + 1] - rp[i];
+    keys[i] = ((uint64_t)(i / sigma) << lenbits) | (uint64_t)(maxlen - L);
+  }
+}
+
+template <class RP>
+__global__ void k_sell_widths(const RP* __restrict__ rp, const int32_t* __restrict__ perm, int64_t rows,
+                              int64_t C, int64_t ns, int64_t* __restrict__ cw) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += stride) {
+    int64_t w = 0;
+    for (int64_t j = 0; j < C; ++j) {
+      int64_t q = s * C + j;
+      if (q >= rows) break;
+      int64_t i = perm ? perm[q] : q;
+      int64_t L = rp[i + 1] - rp[i];
+      w = L > w ? L : w;
+    }
+    cw[s] = C * w;
+  }
+}
+
+template <class RP, class V>
+__global__ void k_sell_fill(const RP* __restrict__ rp, const int32_t* __restrict__ col,
+                            const V* __restrict__ val, const int32_t* __restrict__ perm, int64_t rows,
+                            int64_t C, int64_t ns, const int64_t* __restrict__ sp,
+                            int32_t* __restrict__ colS, V* __restrict__ valS) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t total = ns * C;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    int64_t s = t / C, j = t - s * C;
+    int64_t base = sp[s], w = (sp[s + 1] - base) / C;
+    int64_t a = 0, L = 0;
+    if (t < rows) {
+      int64_t i = perm ? perm[t] : t;
+      a = rp[i];
+      L = rp[i + 1] - a;
+    }
+    for (int64_t k = 0; k < w; ++k) {
+      int64_t pos = base + k * C + j;
+      if (k < L) {
+        colS[pos] = col[a + k];
+        valS[pos] = val[a + k];
+      } else {
+        colS[pos] = -1;
+        valS[pos] = V(0);
+      }
+    }
+  }
+}
+
+__global__ void k_u32_to_i32(const uint32_t* __restrict__ in, int32_t* __restrict__ out, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = (int32_t)in[i];
+}
+
+// ---------------------------------------------------------------- per-nnz row lookup
+// Row containing entry k: the largest i with rp[i] <= k (empty rows skipped).
+template <class RP>
+__device__ __forceinline__ int64_t row_of(const RP* rp, int64_t lo, int64_t hi, int64_t k) {
+  while (lo < hi) {  // invariant: answer in [lo, hi]
+    int64_t mid = lo + (hi - lo + 1) / 2;
+    if ((int64_t)rp[mid] <= k) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+constexpr int kExpandThreads = 256;
+constexpr int kExpandTile = kExpandThreads * 8;
+
+// mode 0: COO row expansion (out_row[k] = row of k).
+// mode 1: HYB tail (entries with in-row rank >= K go to toff[row] + rank − K).
+template <class RP, class V>
+__global__ void __launch_bounds__(kExpandThreads)
+    k_expand(const RP* __restrict__ rp, const int32_t* __restrict__ col, const V* __restrict__ val,
+             int64_t rows, int64_t nnz, int mode, int64_t K, const int64_t* __restrict__ toff,
+             int32_t* __restrict__ out_row, int32_t* __restrict__ out_col, V* __restrict__ out_val) {
+  __shared__ int64_t s_r[2];
+  const int64_t k0 = (int64_t)blockIdx.x * kExpandTile;
+  const int64_t k1 = min(k0 + kExpandTile, nnz);
+  if (threadIdx.x < 2) s_r[threadIdx.x] = row_of(rp, 0, rows - 1, threadIdx.x == 0 ? k0 : k1 - 1);
+  __syncthreads();
+  const int64_t r0 = s_r[0], r1 = s_r[1];
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += kExpandThreads) {
+    int64_t r = row_of(rp, r0, r1, k);
+    if (mode == 0) {
+      out_row[k] = (int32_t)r;
+    } else {
+      int64_t rank = k - (int64_t)rp[r];
+      if (rank >= K) {
+        int64_t pos = toff[r] + rank - K;
+        out_row[pos] = (int32_t)r;
+        out_col[pos] = col[k];
+        out_val[pos] = val[k];
+      }
+    }
+  }
+}
+
+template <class RP>
+__global__ void k_row_counts(const RP* __restrict__ rp, int64_t rows, int mode, int64_t K,
+                             int64_t* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
+    int64_t L = rp[i + 1] - rp[i];
+    out[i] = mode == 0 ? (L == 0 ? 1 : 0) : (L > K ? L - K : 0);
+  }
+}
+
+template <class RP>
+__global__ void k_compact_empty(const RP* __restrict__ rp, const int64_t* __restrict__ off, int64_t rows,
+                                int32_t* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride)
+    if (rp[i + 1] == rp[i]) out[off[i]] = (int32_t)i;
+}
+
+int64_t read_i64(const int64_t* d, cudaStream_t s) {
+  int64_t v = 0;
+  CK(cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return v;
+}
+
+void guard_bytes(double bytes, const char* what) {
+  size_t fr = 0, tot = 0;
+  CK(cudaMemGetInfo(&fr, &tot));
+  if (bytes > 0.9 * (double)fr)
+    fail(SPMV_ERR_INFEASIBLE, std::string(what) + ": padded layout needs " + std::to_string(bytes / 1e9) +
+                                  " GB, more than 90% of free device memory");
+}
+
+struct EventTimer {
+  cudaEvent_t a, b;
+  cudaStream_t s;
+  explicit EventTimer(cudaStream_t st) : s(st) {
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, s));
+  }
+  double stop() {
+    CK(cudaEventRecord(b, s));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms * 1e-3;
+  }
+  ~EventTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+template <class RP, class V>
+void ell_typed(spmv_matrix* h) {
+  cudaStream_t s = h->stream;
+  const int64_t K = h->feat.max_len, n_pad = (h->rows + 127) / 128 * 128;
+  guard_bytes((double)K * n_pad * (4.0 + sizeof(V)), "ELL");
+  EventTimer tm(s);
+  Scratch sc(s);
+  int32_t* colE = sc.get<int32_t>(K * n_pad);
+  V* valE = sc.get<V>(K * n_pad);
+  LAUNCH((k_ell_fill<RP, V>), grid_for(n_pad, 256), 256, 0, s, static_cast<const RP*>(h->row_ptr), h->col,
+         static_cast<const V*>(h->val), h->rows, K, n_pad, colE, valE);
+  h->c_latency[SPMV_FMT_ELL] = tm.stop();
+  sc.keep(colE);
+  sc.keep(valE);
+  h->ell_K = K;
+  h->ell_npad = n_pad;
+  h->ell_col = colE;
+  h->ell_val = valE;
+  h->ell_built = true;
+}
+
+template <class RP, class V>
+void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma) {
+  cudaStream_t s = h->stream;
+  const int64_t rows = h->rows, ns = (rows + C - 1) / C;
+  EventTimer tm(s);
+  Scratch sc(s);
+  const RP* rp = static_cast<const RP*>(h->row_ptr);
+  int32_t* perm = nullptr;
+  if (sigma > 1 && rows > 0) {
+    const int64_t maxlen = h->feat.max_len;
+    int lenbits = bits_for((uint64_t)maxlen);
+    int winbits = bits_for((uint64_t)((rows - 1) / sigma));
+    uint64_t* keys = sc.get<uint64_t>(rows);
+    uint64_t* keys_s = sc.get<uint64_t>(rows);
+    uint32_t* p32 = sc.get<uint32_t>(rows);
+    perm = sc.get<int32_t>(rows);
+    LAUNCH(k_sell_keys<RP>, grid_for(rows, 256), 256, 0, s, rp, rows, sigma, lenbits, maxlen, keys);
+    radix_sort_pairs(keys, nullptr, keys_s, p32, rows, lenbits + winbits, s);
+    LAUNCH(k_u32_to_i32, grid_for(rows, 256), 256, 0, s, (const uint32_t*)p32, perm, rows);
+  }
+  int64_t* cw = sc.get<int64_t>(ns);
+  int64_t* sp = sc.get<int64_t>(ns + 1);
+  LAUNCH(k_sell_widths<RP>, grid_for(ns, 256), 256, 0, s, rp, (const int32_t*)perm, rows, C, ns, cw);
+  exclusive_scan_i64(cw, sp, ns, s);
+  const int64_t slots = read_i64(sp + ns, s);
+  guard_bytes((double)slots * (4.0 + sizeof(V)), "SELL");
+  int32_t* colS = sc.get<int32_t>(slots);
+  V* valS = sc.get<V>(slots);
+  LAUNCH((k_sell_fill<RP, V>), grid_for(ns * C, 256), 256, 0, s, rp, h->col, static_cast<const V*>(h->val),
+         (const int32_t*)perm, rows, C, ns, (const int64_t*)sp, colS, valS);
+  h->c_latency[SPMV_FMT_SELL] = tm.stop();
+  for (void* p : {(void*)perm, (void*)sp, (void*)colS, (void*)valS})
+    if (p) sc.keep(p);
+  h->sell_C = C;
+  h->sell_sigma = sigma;
+  h->sell_ns = ns;
+  h->sell_slots = slots;
+  h->sell_perm = perm;
+  h->sell_sp = sp;
+  h->sell_col = colS;
+  h->sell_val = valS;
+  h->sell_built = true;
+}
+
+template <class RP, class V>
+void hyb_typed(spmv_matrix* h, int64_t K) {
+  cudaStream_t s = h->stream;
+  const int64_t rows = h->rows, n_pad = (rows + 127) / 128 * 128;
+  guard_bytes((double)K * n_pad * (4.0 + sizeof(V)), "HYB");
+  EventTimer tm(s);
+  Scratch sc(s);
+  const RP* rp = static_cast<const RP*>(h->row_ptr);
+  int32_t* colE = sc.get<int32_t>(K * n_pad);
+  V* valE = sc.get<V>(K * n_pad);
+  LAUNCH((k_ell_fill<RP, V>), grid_for(n_pad, 256), 256, 0, s, rp, h->col, static_cast<const V*>(h->val),
+         rows, K, n_pad, colE, valE);
+  int64_t* cnt = sc.get<int64_t>(rows);
+  int64_t* toff = sc.get<int64_t>(rows + 1);
+  LAUNCH(k_row_counts<RP>, grid_for(rows, 256), 256, 0, s, rp, rows, 1, K, cnt);
+  exclusive_scan_i64(cnt, toff, rows, s);
+  const int64_t tail = read_i64(toff + rows, s);
+  int32_t* trow = sc.get<int32_t>(tail);
+  int32_t* tcol = sc.get<int32_t>(tail);
+  V* tval = sc.get<V>(tail);
+  if (h->nnz > 0 && tail > 0)
+    LAUNCH((k_expand<RP, V>), (unsigned)((h->nnz + kExpandTile - 1) / kExpandTile), kExpandThreads, 0, s, rp,
+           h->col, static_cast<const V*>(h->val), rows, h->nnz, 1, K, (const int64_t*)toff, trow, tcol, tval);
+  h->c_latency[SPMV_FMT_HYB] = tm.stop();
+  for (void* p : {(void*)colE, (void*)valE, (void*)trow, (void*)tcol, (void*)tval}) sc.keep(p);
+  h->hyb_K = K;
+  h->hyb_npad = n_pad;
+  h->hyb_tail = tail;
+  h->hyb_ecol = colE;
+  h->hyb_eval = valE;
+  h->hyb_trow = trow;
+  h->hyb_tcol = tcol;
+  h->hyb_tval = tval;
+  h->hyb_built = true;
+}
+
+template <class RP, class V>
+void coo_typed(spmv_matrix* h) {
+  cudaStream_t s = h->stream;
+  const int64_t rows = h->rows;
+  EventTimer tm(s);
+  Scratch sc(s);
+  const RP* rp = static_cast<const RP*>(h->row_ptr);
+  int32_t* crow = sc.get<int32_t>(h->nnz);
+  if (h->nnz > 0)
+    LAUNCH((k_expand<RP, V>), (unsigned)((h->nnz + kExpandTile - 1) / kExpandTile), kExpandThreads, 0, s, rp,
+           h->col, static_cast<const V*>(h->val), rows, h->nnz, 0, (int64_t)0, (const int64_t*)nullptr, crow,
+           (int32_t*)nullptr, (V*)nullptr);
+  int64_t* flag = sc.get<int64_t>(rows);
+  int64_t* off = sc.get<int64_t>(rows + 1);
+  LAUNCH(k_row_counts<RP>, grid_for(rows, 256), 256, 0, s, rp, rows, 0, (int64_t)0, flag);
+  exclusive_scan_i64(flag, off, rows, s);
+  const int64_t n_empty = read_i64(off + rows, s);
+  int32_t* empty = sc.get<int32_t>(n_empty);
+  if (n_empty > 0)
+    LAUNCH(k_compact_empty<RP>, grid_for(rows, 256), 256, 0, s, rp, (const int64_t*)off, rows, empty);
+  h->c_latency[SPMV_FMT_COO] = tm.stop();
+  sc.keep(crow);
+  sc.keep(empty);
+  h->coo_row = crow;
+  h->coo_empty = empty;
+  h->coo_n_empty = n_empty;
+  h->coo_built = true;
+}
+
+template <class F>
+void dispatch(spmv_matrix* h, F&& f) {
+  if (h->dtype == SPMV_R64F) {
+    if (h->rp64) f((int64_t*)nullptr, (double*)nullptr);
+    else f((int32_t*)nullptr, (double*)nullptr);
+  } else {
+    if (h->rp64) f((int64_t*)nullptr, (float*)nullptr);
+    else f((int32_t*)nullptr, (float*)nullptr);
+  }
+}
+
+}  // namespace
+
+void build_ell(spmv_matrix* h) {
+  if (!h->have_features) compute_features(h);
+  dispatch(h, [&](auto rpt, auto vt) {
+    using RP = std::remove_pointer_t<decltype(rpt)>;
+    using V = std::remove_pointer_t<decltype(vt)>;
+    ell_typed<RP, V>(h);
+  });
+}
+
+void build_sell(spmv_matrix* h, int64_t C, int64_t sigma) {
+  if (!h->have_features) compute_features(h);
+  dispatch(h, [&](auto rpt, auto vt) {
+    using RP = std::remove_pointer_t<decltype(rpt)>;
+    using V = std::remove_pointer_t<decltype(vt)>;
+    sell_typed<RP, V>(h, C, sigma);
+  });
+}
+
+void build_hyb(spmv_matrix* h, int64_t K) {
+  if (!h->have_features) compute_features(h);
+  if (K < 0) K = h->hyb_auto_K;
+  if (K > h->feat.max_len) K = h->feat.max_len;
+  dispatch(h, [&](auto rpt, auto vt) {
+    using RP = std::remove_pointer_t<decltype(rpt)>;
+    using V = std::remove_pointer_t<decltype(vt)>;
+    hyb_typed<RP, V>(h, K);
+  });
+}
+
+void build_coo(spmv_matrix* h) {
+  dispatch(h, [&](auto rpt, auto vt) {
+    using RP = std::remove_pointer_t<decltype(rpt)>;
+    using V = std::remove_pointer_t<decltype(vt)>;
+    coo_typed<RP, V>(h);
+  });
+}
+
+void free_format(spmv_matrix* h, int fmt) {
+  cudaStream_t s = h->stream;
+  auto F = [&](auto*& p) {
+    if (p) dfree((void*)p, s);
+    p = nullptr;
+  };
+  switch (fmt) {
+    case SPMV_FMT_COO:
+      F(h->coo_row); F(h->coo_empty);
+      h->coo_built = false;
+      break;
+    case SPMV_FMT_ELL:
+      F(h->ell_col); F(h->ell_val);
+      h->ell_built = false;
+      break;
+    case SPMV_FMT_SELL:
+      F(h->sell_perm); F(h->sell_sp); F(h->sell_col); F(h->sell_val);
+      h->sell_built = false;
+      break;
+    case SPMV_FMT_HYB:
+      F(h->hyb_ecol); F(h->hyb_eval); F(h->hyb_trow); F(h->hyb_tcol); F(h->hyb_tval);
+      h->hyb_built = false;
+      break;
+    case SPMV_FMT_CSR:
+      F(h->row_ptr); F(h->col); F(h->val);
+      break;
+  }
+}
+
+int64_t format_stored_bytes(const spmv_matrix* h, int fmt) {
+  const int64_t vb = h->vbytes, rpb = h->rp64 ? 8 : 4;
+  switch (fmt) {
+    case SPMV_FMT_CSR: return (h->rows + 1) * rpb + h->nnz * (4 + vb);
+    case SPMV_FMT_COO: return h->nnz * (8 + vb) + h->coo_n_empty * 4;
+    case SPMV_FMT_ELL: return h->ell_K * h->ell_npad * (4 + vb);
+    case SPMV_FMT_SELL:
+      return h->sell_slots * (4 + vb) + (h->sell_ns + 1) * 8 + (h->sell_perm ? h->rows * 4 : 0);
+    case SPMV_FMT_HYB: return h->hyb_K * h->hyb_npad * (4 + vb) + h->hyb_tail * (8 + vb);
+  }
+  return 0;
+}
+
+}  // namespace spmv

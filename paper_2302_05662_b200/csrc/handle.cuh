@@ -1,0 +1,126 @@
+// handle.cuh — the spmv_matrix handle and the internal entry points shared
+// by the translation units of libspmv.so.
+#pragma once
+#include <string>
+
+#include "common.cuh"
+
+struct spmv_matrix {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  spmv_dtype_t dtype = SPMV_R64F;
+  int vbytes = 8;
+  int64_t rows = 0, cols = 0, nnz = 0;
+
+  // CSR (canonical COO columns/values in (row, col) order + row pointers).
+  bool rp64 = false;        // row_ptr element type: int64 iff nnz >= 2^31
+  void* row_ptr = nullptr;  // [rows+1]
+  int32_t* col = nullptr;   // [nnz]
+  void* val = nullptr;      // [nnz]
+
+  // COO (rows expanded; columns/values shared with CSR).
+  bool coo_built = false;
+  int32_t* coo_row = nullptr;
+  int32_t* coo_empty = nullptr;  // rows without entries, ascending
+  int64_t coo_n_empty = 0;
+
+  // ELL: column-major [K][n_pad].
+  bool ell_built = false;
+  int64_t ell_K = 0, ell_npad = 0;
+  int32_t* ell_col = nullptr;
+  void* ell_val = nullptr;
+
+  // SELL-C-sigma.
+  bool sell_built = false;
+  int64_t sell_C = 0, sell_sigma = 1, sell_ns = 0, sell_slots = 0;
+  int32_t* sell_perm = nullptr;  // nullptr when sigma == 1
+  int64_t* sell_sp = nullptr;    // [ns+1]
+  int32_t* sell_col = nullptr;
+  void* sell_val = nullptr;
+
+  // HYB: ELL part [K][n_pad] + COO tail.
+  bool hyb_built = false;
+  int64_t hyb_K = 0, hyb_npad = 0, hyb_tail = 0;
+  int32_t* hyb_ecol = nullptr;
+  void* hyb_eval = nullptr;
+  int32_t* hyb_trow = nullptr;
+  int32_t* hyb_tcol = nullptr;
+  void* hyb_tval = nullptr;
+
+  // CSR kernel choice.
+  int csr_alg = SPMV_CSR_AUTO;
+  int csr_T = 0;
+
+  spmv_launch_t launch[SPMV_NUM_FORMATS];
+  int active = SPMV_FMT_CSR;
+
+  bool have_features = false;
+  spmv_features_t feat{};
+  int64_t hyb_auto_K = -1;  // from the feature histogram
+
+  double f_latency = 0.0;
+  double c_latency[SPMV_NUM_FORMATS] = {0, 0, 0, 0, 0};
+
+  // Scratch (grow-only) for segmented-reduction chunk records and for the
+  // power-step block partials.
+  void* seg_scratch = nullptr;
+  size_t seg_scratch_bytes = 0;
+  double* pi_partials = nullptr;
+  unsigned* pi_counter = nullptr;
+  size_t pi_partials_n = 0;
+
+  std::string last_error;
+  std::string log;  // JSON records, comma separated (wrapped in [] on export)
+};
+
+namespace spmv {
+
+// ingest.cu
+void ingest(spmv_matrix* h, const int32_t* row_idx, const int32_t* col_idx, const void* vals,
+            spmv_mem_t where);
+
+// features.cu
+void compute_features(spmv_matrix* h);
+
+// convert.cu
+void build_coo(spmv_matrix* h);
+void build_ell(spmv_matrix* h);
+void build_sell(spmv_matrix* h, int64_t C, int64_t sigma);
+void build_hyb(spmv_matrix* h, int64_t K);
+void free_format(spmv_matrix* h, int fmt);
+int64_t format_stored_bytes(const spmv_matrix* h, int fmt);
+
+// Epilogue parameters shared by every SpMV kernel.
+struct Epilogue {
+  double alpha = 1.0, beta = 0.0;
+  int mode = 0;  // 0: y = alpha·Ax + beta·y; 1: power step; 2: y += alpha·Ax; 3: y += alpha_dev·Ax
+  const double* sums_prev = nullptr;   // mode 1: alpha = 1/sqrt(sums_prev[0])
+  double* sums_out = nullptr;          // mode 1: [Σy², Σ x_own·y]
+  double* partials = nullptr;          // mode 1: per-block partials (2 per block)
+  unsigned* counter = nullptr;         // mode 1: last-block counter (zero at rest)
+  int64_t row_offset = 0;              // mode 1: x_own = x[row_offset + i]
+};
+
+// spmv kernels (launchers). All asynchronous on h->stream.
+void run_csr(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
+void run_ell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
+void run_ell_arrays(spmv_matrix* h, const int32_t* col, const void* val, int64_t K, int64_t n_pad,
+                    const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
+// y <- beta·y over all rows (alpha == 0: A is not read).
+void run_scale(spmv_matrix* h, void* y, double beta);
+void run_sell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
+void run_coo(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
+void run_hyb(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
+// Σ y_i², Σ x_own_i·y_i over rows (power mode for formats without a fused epilogue).
+void run_norms(spmv_matrix* h, const Epilogue& e, const void* x, const void* y, int64_t n);
+
+// Make sure the power-step partial buffers hold >= nblocks entries.
+void ensure_pi_scratch(spmv_matrix* h, size_t nblocks);
+void* ensure_seg_scratch(spmv_matrix* h, size_t bytes);
+
+// Resolve a launch variant to the defaults of its kernel.
+spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t& L);
+// Carveout attribute (cached per function pointer).
+void set_carveout(const void* func, int pct);
+
+}  // namespace spmv

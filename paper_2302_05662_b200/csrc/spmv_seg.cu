@@ -1,0 +1,307 @@
+// spmv_seg.cu — COO SpMV via warp-shuffle segmented reduction (north star),
+// the HYB tail (same kernel in accumulate mode), the chunk fixup shared
+// with merge-path CSR, and small helper kernels (row scaling, norms).
+//
+// COO: a warp owns a chunk of 32·W consecutive entries sorted by
+// (row, col); lane l loads W of them with vector loads (row/col as int2/int4,
+// values as double2/float4), reduces its own runs, then a 5-step warp
+// segmented scan keyed by row combines runs that cross lanes. Rows entirely
+// inside the chunk are written by the chunk; rows crossing chunk boundaries
+// leave head/tail partials that k_seg_fixup combines in chunk order.
+#include "spmv_common.cuh"
+
+namespace spmv {
+namespace {
+
+struct CooParams {
+  const int32_t* row;
+  const int32_t* col;
+  const void* val;
+  int64_t nnz;
+  const void* x;
+  void* y;
+  Epilogue e;
+  ChunkRec* recs;
+};
+
+template <class T, int W>
+__device__ __forceinline__ void load_w(const T* p, T (&v)[W]) {
+  if constexpr (W == 2 && sizeof(T) == 8) {
+    double2 a = ld_stream(reinterpret_cast<const double2*>(p));
+    v[0] = a.x; v[1] = a.y;
+  } else if constexpr (W == 4 && sizeof(T) == 8) {
+    double2 a = ld_stream(reinterpret_cast<const double2*>(p));
+    double2 b = ld_stream(reinterpret_cast<const double2*>(p + 2));
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  } else if constexpr (W == 2) {
+    float2 a = ld_stream(reinterpret_cast<const float2*>(p));
+    v[0] = a.x; v[1] = a.y;
+  } else if constexpr (W == 4) {
+    float4 a = ld_stream(reinterpret_cast<const float4*>(p));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; q += 4) load_w<T, 4>(p + q, *reinterpret_cast<T(*)[4]>(&v[q]));
+  }
+}
+template <int W>
+__device__ __forceinline__ void load_wi(const int* p, int (&v)[W]) {
+  if constexpr (W == 2) {
+    int2 a = ld_stream(reinterpret_cast<const int2*>(p));
+    v[0] = a.x; v[1] = a.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; q += 4) {
+      int4 a = ld_stream(reinterpret_cast<const int4*>(p + q));
+      v[q] = a.x; v[q + 1] = a.y; v[q + 2] = a.z; v[q + 3] = a.w;
+    }
+  }
+}
+
+template <int B, int R, class T, int W>
+__global__ void __launch_bounds__(B) __maxnreg__(R) k_coo(const CooParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t chunk = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
+  const int64_t base = chunk * 32 * W;
+  if (base >= p.nnz) return;  // warp-uniform
+  const T* __restrict__ val = static_cast<const T*>(p.val);
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  T* __restrict__ y = static_cast<T*>(p.y);
+  const double alpha = epi_alpha(p.e);
+  const int64_t k0 = base + (int64_t)lane * W;
+  int r[W], c[W];
+  T v[W];
+  if (k0 + W <= p.nnz) {
+    load_wi<W>(p.row + k0, r);
+    load_wi<W>(p.col + k0, c);
+    load_w<T, W>(val + k0, v);
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const bool ok = k0 + q < p.nnz;
+      r[q] = ok ? p.row[k0 + q] : INT_MAX;  // sentinel row after the last entry
+      c[q] = ok ? p.col[k0 + q] : 0;
+      v[q] = ok ? val[k0 + q] : T(0);
+    }
+  }
+  double prod[W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) prod[q] = r[q] != INT_MAX ? (double)v[q] * (double)ld_x(x + c[q]) : 0.0;
+  const int64_t end = base + 32 * W;
+  const int chunk_first = __shfl_sync(0xffffffffu, r[0], 0);
+  const bool cont_in = base > 0 && p.row[base - 1] == chunk_first;
+  // lane-local runs: rows strictly inside the lane are complete here
+  const int first = r[0];
+  double first_sum = 0.0, run = 0.0;
+  bool first_closed = false;
+  int cur = r[0];
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    if (r[q] != cur) {
+      if (!first_closed) {
+        first_sum = run;
+        first_closed = true;
+      } else {
+        y[cur] = epi_value<T>(p.e, alpha, run, y, cur);
+      }
+      cur = r[q];
+      run = 0.0;
+    }
+    run += prod[q];
+  }
+  const int last = cur;
+  if (!first_closed) first_sum = run;  // single-run lane
+  // warp inclusive segmented scan of the last run (key = row)
+  double s = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double su = __shfl_up_sync(0xffffffffu, s, o);
+    int ku = __shfl_up_sync(0xffffffffu, last, o);
+    if (lane >= o && ku == last) s += su;
+  }
+  const double s_prev = __shfl_up_sync(0xffffffffu, s, 1);
+  const int k_prev = __shfl_up_sync(0xffffffffu, last, 1);
+  const double carry_in = (lane > 0 && k_prev == first) ? s_prev : 0.0;
+  int next_first = __shfl_down_sync(0xffffffffu, r[0], 1);
+  if (lane == 31) next_first = end < p.nnz ? p.row[end] : INT_MAX;
+  // first run closed inside this lane
+  if (first_closed && first != INT_MAX) {
+    const double tot = carry_in + first_sum;
+    if (cont_in && first == chunk_first) p.recs[chunk].head = tot;
+    else y[first] = epi_value<T>(p.e, alpha, tot, y, first);
+  }
+  // last run: closes at the lane end if the next entry starts another row
+  if (last != INT_MAX) {
+    if (next_first != last) {
+      if (cont_in && last == chunk_first) p.recs[chunk].head = s;
+      else y[last] = epi_value<T>(p.e, alpha, s, y, last);
+    } else if (lane == 31) {
+      p.recs[chunk].tail = s;
+      if (cont_in && last == chunk_first) p.recs[chunk].head = s;
+    }
+  }
+  // chunk record: the last valid row of the chunk
+  int chunk_last = last;
+  {
+    unsigned valid = __ballot_sync(0xffffffffu, r[0] != INT_MAX);
+    int src = 31 - __clz((int)valid);
+    int lastv = __shfl_sync(0xffffffffu, last, src);
+    chunk_last = lastv;
+  }
+  if (lane == 31) {
+    ChunkRec& rec = p.recs[chunk];
+    rec.first_row = chunk_first;
+    rec.cont_in = cont_in;
+    rec.last_row = chunk_last;
+    rec.cont_out = (next_first == last) && last != INT_MAX;
+  }
+}
+
+// Rows crossing chunk boundaries: the chunk where the row starts (cont_out
+// and not a single-row continuation chunk) walks forward adding heads.
+template <class T>
+__global__ void k_seg_fixup(const ChunkRec* __restrict__ recs, int64_t n, Epilogue e, T* __restrict__ y) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double alpha = epi_alpha(e);
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride) {
+    const ChunkRec rc = recs[c];
+    if (!rc.cont_out || (rc.cont_in && rc.first_row == rc.last_row)) continue;
+    const int r = rc.last_row;
+    double sum = rc.tail;
+    for (int64_t q = c + 1; q < n; ++q) {
+      const ChunkRec rq = recs[q];
+      sum += rq.head;
+      if (!(rq.cont_out && rq.cont_in && rq.first_row == rq.last_row)) break;
+    }
+    y[r] = epi_value<T>(e, alpha, sum, y, r);
+  }
+}
+
+template <class T>
+__global__ void k_rows_scale(const int32_t* __restrict__ rows, int64_t n, Epilogue e, T* __restrict__ y) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double alpha = epi_alpha(e);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int r = rows[i];
+    y[r] = epi_value<T>(e, alpha, 0.0, y, r);
+  }
+}
+
+template <class T>
+__global__ void k_norms(const T* __restrict__ x, const T* __restrict__ y, int64_t n, Epilogue e) {
+  double yy = 0.0, xy = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double v = (double)y[i];
+    yy += v * v;
+    if (x) xy += (double)x[e.row_offset + i] * v;
+  }
+  power_reduce(e, yy, xy);
+}
+
+template <class T>
+__global__ void k_scale(T* __restrict__ y, int64_t n, double beta) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    y[i] = beta == 0.0 ? T(0) : (T)(beta * (double)y[i]);
+}
+
+template <class T>
+using CooFn = void (*)(const CooParams);
+#define COO_ROW(B, W) {&k_coo<B, 32, T, W>, &k_coo<B, 64, T, W>, &k_coo<B, 128, T, W>, &k_coo<B, 255, T, W>}
+#define COO_TAB(W) {COO_ROW(64, W), COO_ROW(128, W), COO_ROW(256, W), COO_ROW(512, W), COO_ROW(1024, W)}
+template <class T, int W>
+CooFn<T> coo_fn(int bi, int ri) {
+  static const CooFn<T> tab[5][4] = COO_TAB(W);
+  return tab[bi][ri];
+}
+#undef COO_TAB
+#undef COO_ROW
+
+template <class T>
+void coo_launch(spmv_matrix* h, const int32_t* row, const int32_t* col, const void* val, int64_t nnz,
+                const Epilogue& e, const void* x, void* y, const spmv_launch_t& L) {
+  if (nnz <= 0) return;
+  const int W = L.knob;
+  const int bi = block_index(L.block), ri = reg_index(L.maxreg);
+  const void* fn;
+  switch (W) {
+    case 2: fn = (const void*)coo_fn<T, 2>(bi, ri); break;
+    case 4: fn = (const void*)coo_fn<T, 4>(bi, ri); break;
+    case 8: fn = (const void*)coo_fn<T, 8>(bi, ri); break;
+    default: fail(SPMV_ERR_INVALID_ARG, "COO entries per lane must be 2, 4 or 8");
+  }
+  set_carveout(fn, L.carveout_pct);
+  const int64_t nchunks = (nnz + 32LL * W - 1) / (32LL * W);
+  CooParams p{};
+  p.row = row;
+  p.col = col;
+  p.val = val;
+  p.nnz = nnz;
+  p.x = x;
+  p.y = y;
+  p.e = e;
+  p.recs = static_cast<ChunkRec*>(ensure_seg_scratch(h, (size_t)nchunks * sizeof(ChunkRec)));
+  const int64_t grid = (nchunks * 32 + L.block - 1) / L.block;
+  void* args[] = {&p};
+  CK(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  run_seg_fixup(h, p.recs, nchunks, e, y);
+}
+
+}  // namespace
+
+void run_seg_fixup(spmv_matrix* h, const ChunkRec* recs, int64_t nchunks, const Epilogue& e, void* y) {
+  if (nchunks <= 1) return;
+  const unsigned g = grid_for(nchunks, 256);
+  if (h->dtype == SPMV_R64F) LAUNCH(k_seg_fixup<double>, g, 256, 0, h->stream, recs, nchunks, e, (double*)y);
+  else LAUNCH(k_seg_fixup<float>, g, 256, 0, h->stream, recs, nchunks, e, (float*)y);
+}
+
+void run_rows_scale(spmv_matrix* h, const int32_t* rows_list, int64_t n, const Epilogue& e, void* y) {
+  if (n <= 0) return;
+  const unsigned g = grid_for(n, 256);
+  if (h->dtype == SPMV_R64F) LAUNCH(k_rows_scale<double>, g, 256, 0, h->stream, rows_list, n, e, (double*)y);
+  else LAUNCH(k_rows_scale<float>, g, 256, 0, h->stream, rows_list, n, e, (float*)y);
+}
+
+void run_norms(spmv_matrix* h, const Epilogue& e0, const void* x, const void* y, int64_t n) {
+  Epilogue e = e0;
+  const unsigned g = grid_for(n, 256, (int64_t)kNumSMs * 4);
+  ensure_pi_scratch(h, g);
+  e.partials = h->pi_partials;
+  e.counter = h->pi_counter;
+  if (h->dtype == SPMV_R64F)
+    LAUNCH(k_norms<double>, g, 256, 0, h->stream, (const double*)x, (const double*)y, n, e);
+  else
+    LAUNCH(k_norms<float>, g, 256, 0, h->stream, (const float*)x, (const float*)y, n, e);
+}
+
+void run_scale(spmv_matrix* h, void* y, double beta) {
+  if (h->rows <= 0) return;
+  const unsigned g = grid_for(h->rows, 256);
+  if (h->dtype == SPMV_R64F) LAUNCH(k_scale<double>, g, 256, 0, h->stream, (double*)y, h->rows, beta);
+  else LAUNCH(k_scale<float>, g, 256, 0, h->stream, (float*)y, h->rows, beta);
+}
+
+void run_coo(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L) {
+  // empty rows first (they are disjoint from every row the chunks write)
+  run_rows_scale(h, h->coo_empty, h->coo_n_empty, e, y);
+  if (h->dtype == SPMV_R64F) coo_launch<double>(h, h->coo_row, h->col, h->val, h->nnz, e, x, y, L);
+  else coo_launch<float>(h, h->coo_row, h->col, h->val, h->nnz, e, x, y, L);
+}
+
+void run_hyb(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L) {
+  // ELL part writes every row (alpha·s_ell + beta·y); the COO tail then adds
+  // alpha·s_tail to the rows that have one (mode 2, or 3 with device alpha).
+  spmv_launch_t le = L;
+  le.knob = h->dtype == SPMV_R64F ? 64 : 128;
+  run_ell_arrays(h, h->hyb_ecol, h->hyb_eval, h->hyb_K, h->hyb_npad, e, x, y, le);
+  Epilogue et = e;
+  et.mode = (e.mode == 1) ? 3 : 2;
+  spmv_launch_t lt = L;
+  if (h->dtype == SPMV_R64F) coo_launch<double>(h, h->hyb_trow, h->hyb_tcol, h->hyb_tval, h->hyb_tail, et, x, y, lt);
+  else coo_launch<float>(h, h->hyb_trow, h->hyb_tcol, h->hyb_tval, h->hyb_tail, et, x, y, lt);
+}
+
+}  // namespace spmv

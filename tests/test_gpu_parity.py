@@ -1,0 +1,366 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bit-exact: canonical COO/CSR, features, ELL/SELL/HYB/COO layouts.
+Tolerance O9: |y − y_ref| <= tau·(|α|·Σ|a·x| + |β|·|y_in|),
+tau = 1e-12 (fp64) / 1e-5 (fp32, north star), per row."""
+import numpy as np
+import pytest
+
+import oracle
+import spmv_inputs as si
+from gpu_cases import corpus, oracle_csr, small_corpus, to_device, vec
+
+torch = pytest.importorskip("torch")
+P = pytest.importorskip("paper_2302_05662_b200")
+
+pytestmark = pytest.mark.gpu
+
+TAU = {"f64": 1e-12, "f32": 1e-5}
+AB = [(1.0, 0.0), (2.5, -0.5), (0.0, 1.0), (1.0, 1.0)]
+CASES = {name: coo for name, coo in corpus()}
+
+
+def tdt(dtype):
+    return torch.float64 if dtype == "f64" else torch.float32
+
+
+def create(coo, dtype="f64", where="device", shuffle=False):
+    if shuffle:
+        coo = si.shuffled(coo, 77)
+    if where == "device":
+        r, c, v = to_device(coo, dtype)
+    else:
+        r, c = np.ascontiguousarray(coo.row), np.ascontiguousarray(coo.col)
+        v = np.ascontiguousarray(coo.val.astype(np.float32 if dtype == "f32" else np.float64))
+    return P.spmv_create(coo.rows, coo.cols, r, c, v)
+
+
+def fetch(h, which, n, np_dtype):
+    out = np.empty(n, np_dtype)
+    if n:
+        P.spmv_copy_array(h, which, out)
+    return out
+
+
+def check_y(h, coo, dtype, fmt, alpha, beta, ref=None, nan_y=False):
+    rp, R, C, V = ref if ref is not None else oracle_csr(coo)
+    x = vec(coo.cols, 11, dtype)
+    yin = vec(coo.rows, 12, dtype)
+    y_ref, a_ref = oracle.spmv_csr(coo.rows, rp, C, V, x.astype(np.float64), alpha, beta, yin.astype(np.float64))
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.from_numpy(yin).cuda()
+    if nan_y:
+        yd.fill_(float("nan"))
+    P.spmv_run(h, alpha, xd, beta, yd, fmt=fmt)
+    torch.cuda.synchronize()
+    y = yd.cpu().numpy().astype(np.float64)
+    ok, worst, bad = oracle.parity_check(y, y_ref, a_ref, alpha, beta, None if nan_y else yin, TAU[dtype])
+    assert ok, (P.FORMAT_NAMES[fmt], alpha, beta, worst, bad[:8], y[bad[:4]], y_ref[bad[:4]])
+    return y
+
+
+# ------------------------------------------------------------------ inputs module
+
+def test_generators_host_device_identical():
+    for kind, N in ((si.LAP2D, 17), (si.STENCIL27, 7)):
+        for rv in (False, True):
+            h = si.stencil(kind, N, random_values=rv)
+            d = si.stencil_device(kind, N, random_values=rv)
+            assert (d.row.cpu().numpy() == h.row).all() and (d.col.cpu().numpy() == h.col).all()
+            assert (d.val.cpu().numpy() == h.val).all()
+    h = si.stencil(si.STENCIL27, 8, r0=100, r1=300)
+    d = si.stencil_device(si.STENCIL27, 8, r0=100, r1=300)
+    assert (d.row.cpu().numpy() == h.row).all() and (d.col.cpu().numpy() == h.col).all()
+    u, ud = si.uniform_k(1 << 12, 32), si.uniform_k_device(1 << 12, 32)
+    assert (ud.col.cpu().numpy() == u.col).all() and (ud.val.cpu().numpy() == u.val).all()
+    r, rd = si.rmat(12, dtype=np.float64), si.rmat_device(12, dtype=torch.float64)
+    assert (rd.row.cpu().numpy() == r.row).all() and (rd.col.cpu().numpy() == r.col).all()
+    assert (rd.val.cpu().numpy() == r.val).all()
+    assert (si.vector_device(1000).cpu().numpy() == si.vector(1000)).all()
+
+
+# ------------------------------------------------------------------ a1/a2 ingest + CSR
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("where,shuffle", [("device", False), ("host", False), ("device", True)])
+def test_create_csr_bit_exact(name, dtype, where, shuffle):
+    coo = CASES[name]
+    if shuffle and coo.nnz > 20000:
+        pytest.skip("large shuffled case covered elsewhere")
+    h = create(coo, dtype, where, shuffle)
+    try:
+        rp, R, C, V = oracle_csr(coo)
+        info = P.spmv_format_info(h, P.FMT_CSR)
+        rpd = fetch(h, P.ARR_CSR_ROW_PTR, coo.rows + 1, np.int64 if info["row_ptr_is64"] else np.int32)
+        assert (rpd.astype(np.int64) == rp).all()
+        assert (fetch(h, P.ARR_CSR_COL, coo.nnz, np.int32) == C).all()
+        vd = fetch(h, P.ARR_CSR_VAL, coo.nnz, np.float32 if dtype == "f32" else np.float64)
+        assert (vd.astype(np.float64) == V).all()
+    finally:
+        P.spmv_destroy(h)
+
+
+def test_create_large_unsorted_rmat():
+    coo = si.rmat(16, dtype=np.float64)
+    h = create(coo, "f64", "device", shuffle=True)
+    try:
+        rp, R, C, V = oracle_csr(coo)
+        assert (fetch(h, P.ARR_CSR_ROW_PTR, coo.rows + 1, np.int32) == rp).all()
+        assert (fetch(h, P.ARR_CSR_COL, coo.nnz, np.int32) == C).all()
+        assert (fetch(h, P.ARR_CSR_VAL, coo.nnz, np.float64) == V).all()
+    finally:
+        P.spmv_destroy(h)
+
+
+def test_create_errors():
+    r = torch.tensor([0, 1, 1], dtype=torch.int32, device="cuda")
+    c = torch.tensor([0, 2, 2], dtype=torch.int32, device="cuda")
+    v = torch.ones(3, dtype=torch.float64, device="cuda")
+    with pytest.raises(P.SpmvError) as e:
+        P.spmv_create(3, 3, r, c, v)
+    assert e.value.status == P.ERR_DUPLICATE
+    r2 = torch.tensor([1, 0, 1], dtype=torch.int32, device="cuda")
+    c2 = torch.tensor([2, 0, 2], dtype=torch.int32, device="cuda")
+    with pytest.raises(P.SpmvError) as e:                       # unsorted + duplicate
+        P.spmv_create(3, 3, r2, c2, v)
+    assert e.value.status == P.ERR_DUPLICATE
+    c3 = torch.tensor([0, 1, 3], dtype=torch.int32, device="cuda")
+    with pytest.raises(P.SpmvError) as e:
+        P.spmv_create(3, 3, r, c3, v)
+    assert e.value.status == P.ERR_INDEX_OUT_OF_RANGE
+    r4 = torch.tensor([0, -1, 1], dtype=torch.int32, device="cuda")
+    with pytest.raises(P.SpmvError) as e:
+        P.spmv_create(3, 3, r4, c, v)
+    assert e.value.status == P.ERR_INDEX_OUT_OF_RANGE
+
+
+# ------------------------------------------------------------------ a3 features
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_features_bit_exact(name):
+    coo = CASES[name]
+    h = create(coo)
+    try:
+        rp, R, C, V = oracle_csr(coo)
+        st, fo = oracle.features(coo.rows, coo.cols, rp, C)
+        fd = P.spmv_features(h)
+        for k, v in fo.items():
+            assert np.float64(fd[k]).tobytes() == np.float64(v).tobytes() if isinstance(v, float) else fd[k] == v, \
+                (k, fd[k], v)
+    finally:
+        P.spmv_destroy(h)
+
+
+# ------------------------------------------------------------------ a4 layouts
+
+@pytest.mark.parametrize("name", [n for n, _ in small_corpus()])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_layouts_bit_exact(name, dtype):
+    coo = CASES[name]
+    npv = np.float32 if dtype == "f32" else np.float64
+    h = create(coo, dtype)
+    try:
+        rp, R, C, V = oracle_csr(coo)
+        if coo.rows == 0:
+            return
+        # ELL
+        P.spmv_convert(h, P.FMT_ELL)
+        K, n_pad, colE, valE = oracle.ell(coo.rows, rp, C, V)
+        info = P.spmv_format_info(h, P.FMT_ELL)
+        assert (info["K"], info["n_pad"]) == (K, n_pad)
+        assert (fetch(h, P.ARR_ELL_COL, K * n_pad, np.int32) == colE).all()
+        assert (fetch(h, P.ARR_ELL_VAL, K * n_pad, npv).astype(np.float64) == valE).all()
+        # SELL-C-sigma
+        for Cs, sigma in ((32, 1), (64, 1), (128, 1), (256, 1), (64, 64), (32, 256), (128, 512)):
+            P.spmv_convert(h, P.FMT_SELL, sell_C=Cs, sell_sigma=sigma)
+            perm, sp, colS, valS = oracle.sell(coo.rows, rp, C, V, Cs, sigma)
+            info = P.spmv_format_info(h, P.FMT_SELL)
+            assert info["n_slices"] == len(sp) - 1 and info["slots"] == sp[-1]
+            assert (fetch(h, P.ARR_SELL_PERM, coo.rows, np.int32) == perm).all()
+            assert (fetch(h, P.ARR_SELL_SLICE_PTR, len(sp), np.int64) == sp).all()
+            assert (fetch(h, P.ARR_SELL_COL, sp[-1], np.int32) == colS).all()
+            assert (fetch(h, P.ARR_SELL_VAL, sp[-1], npv).astype(np.float64) == valS).all()
+        # HYB (auto rule and an explicit width)
+        for Kh in (-1, 2):
+            P.spmv_convert(h, P.FMT_HYB, hyb_K=Kh)
+            K, n_pad, colE, valE, tr, tc, tv = oracle.hyb(coo.rows, rp, C, V, None if Kh < 0 else Kh)
+            info = P.spmv_format_info(h, P.FMT_HYB)
+            assert (info["K"], info["n_pad"], info["tail_nnz"]) == (K, n_pad, tr.shape[0])
+            assert (fetch(h, P.ARR_HYB_ELL_COL, K * n_pad, np.int32) == colE).all()
+            assert (fetch(h, P.ARR_HYB_ELL_VAL, K * n_pad, npv).astype(np.float64) == valE).all()
+            assert (fetch(h, P.ARR_HYB_TAIL_ROW, tr.shape[0], np.int32) == tr).all()
+            assert (fetch(h, P.ARR_HYB_TAIL_COL, tr.shape[0], np.int32) == tc).all()
+            assert (fetch(h, P.ARR_HYB_TAIL_VAL, tr.shape[0], npv).astype(np.float64) == tv).all()
+        # COO
+        P.spmv_convert(h, P.FMT_COO)
+        assert (fetch(h, P.ARR_COO_ROW, coo.nnz, np.int32) == R).all()
+        L = np.diff(rp)
+        empty = np.nonzero(L == 0)[0]
+        assert P.spmv_format_info(h, P.FMT_COO)["n_empty_rows"] == empty.shape[0]
+        assert (fetch(h, P.ARR_COO_EMPTY_ROWS, empty.shape[0], np.int32) == empty).all()
+    finally:
+        P.spmv_destroy(h)
+
+
+# ------------------------------------------------------------------ a5 SpMV parity
+
+FMTS = [("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)),
+        ("CSR-scalar", P.FMT_CSR, dict(csr_alg=P.CSR_SCALAR)),
+        ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE)),
+        ("ELL", P.FMT_ELL, {}),
+        ("SELL", P.FMT_SELL, {}),
+        ("SELL-sigma", P.FMT_SELL, dict(sell_C=32, sell_sigma=256)),
+        ("HYB", P.FMT_HYB, {}),
+        ("HYB-K2", P.FMT_HYB, dict(hyb_K=2)),
+        ("COO", P.FMT_COO, {})]
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("fname,fmt,params", FMTS, ids=[f[0] for f in FMTS])
+def test_spmv_parity(name, dtype, fname, fmt, params):
+    coo = CASES[name]
+    h = create(coo, dtype)
+    try:
+        ref = oracle_csr(coo)
+        P.spmv_convert(h, fmt, **params)
+        for alpha, beta in AB:
+            check_y(h, coo, dtype, fmt, alpha, beta, ref)
+        check_y(h, coo, dtype, fmt, 2.5, 0.0, ref, nan_y=True)    # beta = 0: y never read
+    finally:
+        P.spmv_destroy(h)
+
+
+@pytest.mark.parametrize("fname,fmt,params,knobs", [
+    ("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR), [1, 2, 4, 8, 16, 32]),
+    ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), [4, 8, 16]),
+    ("ELL", P.FMT_ELL, {}, [32, 64, 128]),
+    ("SELL", P.FMT_SELL, {}, [0]),
+    ("COO", P.FMT_COO, {}, [2, 4, 8]),
+    ("HYB", P.FMT_HYB, {}, [2, 4, 8])])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_launch_variants_parity(fname, fmt, params, knobs, dtype):
+    coo = CASES["ragged_empty"]
+    h = create(coo, dtype)
+    try:
+        ref = oracle_csr(coo)
+        P.spmv_convert(h, fmt, **params)
+        for block in (64, 128, 256, 512, 1024):
+            for maxreg in (32, 64, 128, 255):
+                for knob in knobs:
+                    P.spmv_set_launch(h, fmt, block, maxreg, 25 if block == 128 else -1, knob)
+                    check_y(h, coo, dtype, fmt, 2.5, -0.5, ref)
+    finally:
+        P.spmv_destroy(h)
+
+
+def test_determinism_bitwise():
+    coo = CASES["long_rows"]
+    h = create(coo)
+    try:
+        x = torch.from_numpy(vec(coo.cols, 3, "f64")).cuda()
+        for fmt, params in ((P.FMT_CSR, dict(csr_alg=P.CSR_MERGE)), (P.FMT_COO, {}), (P.FMT_HYB, {}),
+                            (P.FMT_SELL, {})):
+            P.spmv_convert(h, fmt, **params)
+            ys = []
+            for _ in range(3):
+                y = torch.empty(coo.rows, dtype=torch.float64, device="cuda")
+                P.spmv_run(h, 1.0, x, 0.0, y)
+                ys.append(y.cpu().numpy().tobytes())
+            assert ys[0] == ys[1] == ys[2]
+    finally:
+        P.spmv_destroy(h)
+
+
+def test_alpha_zero_does_not_read_A_or_x():
+    coo = CASES["uniform_rand"]
+    h = create(coo)
+    try:
+        x = torch.full((coo.cols,), float("nan"), dtype=torch.float64, device="cuda")
+        yin = torch.from_numpy(vec(coo.rows, 5, "f64")).cuda()
+        for fmt in (P.FMT_CSR, P.FMT_ELL, P.FMT_SELL, P.FMT_COO, P.FMT_HYB):
+            P.spmv_convert(h, fmt)
+            y = yin.clone()
+            P.spmv_run(h, 0.0, x, 0.5, y)
+            assert torch.equal(y, 0.5 * yin)
+    finally:
+        P.spmv_destroy(h)
+
+
+def test_run_argument_errors():
+    coo = CASES["uniform_rand"]
+    h = create(coo)
+    try:
+        x = torch.zeros(coo.cols, dtype=torch.float64, device="cuda")
+        with pytest.raises(P.SpmvError) as e:
+            P.spmv_run(h, 1.0, x, 0.0, x)          # x == y
+        assert e.value.status == P.ERR_INVALID_ARG
+        with pytest.raises(P.SpmvError) as e:
+            P.spmv_run(h, 1.0, x, 0.0, torch.zeros(coo.rows, dtype=torch.float64, device="cuda"), fmt=P.FMT_ELL)
+        assert e.value.status == P.ERR_NOT_CONVERTED
+        with pytest.raises(P.SpmvError) as e:
+            P.spmv_convert(h, P.FMT_SELL, sell_C=48)
+        assert e.value.status == P.ERR_UNSUPPORTED
+    finally:
+        P.spmv_destroy(h)
+
+
+# ------------------------------------------------------------------ a8 power step
+
+@pytest.mark.parametrize("fname,fmt,params", FMTS, ids=[f[0] for f in FMTS])
+def test_power_step_parity(fname, fmt, params):
+    coo = si.lap2d(40, random_values=True)
+    h = create(coo)
+    try:
+        rp, R, C, V = oracle_csr(coo)
+        P.spmv_convert(h, fmt, **params)
+        n = coo.rows
+        z_prev = torch.from_numpy(vec(n, 9, "f64")).cuda()          # unnormalised z_{k-1}
+        sums_prev = torch.zeros(2, dtype=torch.float64, device="cuda")
+        P.spmv_norm2(h, z_prev, sums_prev)
+        zp = z_prev.cpu().numpy()
+        s_prev = float(sums_prev[0].item())
+        assert abs(s_prev - np.dot(zp, zp)) <= 1e-13 * np.dot(zp, zp)
+        for step in range(3):
+            z = torch.empty(n, dtype=torch.float64, device="cuda")
+            sums = torch.zeros(2, dtype=torch.float64, device="cuda")
+            P.spmv_power_step(h, z_prev, z, sums_prev, sums)
+            torch.cuda.synchronize()
+            xk = z_prev.cpu().numpy() / np.sqrt(float(sums_prev[0].item()))   # the GPU's own x_k
+            y_ref, xn, lam, s = oracle.power_step(n, rp, C, V, xk)
+            _, a_ref = oracle.spmv_csr(n, rp, C, V, xk)
+            ok, worst, bad = oracle.parity_check(z.cpu().numpy(), y_ref, a_ref, 1.0, 0.0, None, 1e-12)
+            assert ok, (step, worst)
+            lam_gpu = float(sums[1].item()) / np.sqrt(float(sums_prev[0].item()))
+            assert abs(lam_gpu - lam) <= 1e-10 * abs(lam)
+            assert abs(float(sums[0].item()) - s) <= 1e-10 * s
+            z_prev, sums_prev = z, sums
+    finally:
+        P.spmv_destroy(h)
+
+
+# ------------------------------------------------------------------ a6/a7 tuner + selector
+
+def test_tune_invariants():
+    coo = si.stencil27(24, random_values=True)
+    h = create(coo)
+    try:
+        rep = P.spmv_tune(h, P.TUNE_ALL, expected_iterations=10 ** 6)
+        log = P.spmv_decision_log(h)
+        sel = [r for r in log if r["kind"] == "format_select"][0]
+        names = [c["format"] for c in sel["candidates"] if "t_s" in c]
+        assert P.FORMAT_NAMES[rep.format] in names
+        g = sel["gate"]
+        assert g["convert"] == (g["expected_iterations"] * (g["t_csr_s"] - g["t_best_s"]) >
+                                g["f_latency_s"] + g["c_latency_s"])
+        best = min(c["t_s"] for c in sel["candidates"] if "t_s" in c)
+        assert g["t_best_s"] == best
+        sweep = [r for r in log if r["kind"] == "launch_sweep"][-1]
+        assert sweep["t_best_s"] <= min(v[4] for v in sweep["variants"]) + 1e-15
+        check_y(h, coo, "f64", rep.format, 2.5, -0.5)
+        # gate with zero iterations never converts
+        rep0 = P.spmv_tune(h, P.TUNE_FORMAT, expected_iterations=0)
+        assert rep0.converted == 0 and rep0.format == P.FMT_CSR
+    finally:
+        P.spmv_destroy(h)
