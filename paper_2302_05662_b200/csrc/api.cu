@@ -535,7 +535,7 @@ spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format
       int64_t K = q.hyb_K;
       if (K < -1) fail(SPMV_ERR_INVALID_ARG, "hyb_K must be >= -1");
       if (!h->have_features) compute_features(h);
-      int64_t want = K < 0 ? h->hyb_auto_K : std::min<int64_t>(K, h->feat.max_len);
+      int64_t want = K < 0 ? h->hyb_auto_K : K;
       if (!h->hyb_built || h->hyb_K != want) {
         if (h->hyb_built) free_format(h, SPMV_FMT_HYB);
         build_hyb(h, want);

@@ -41,6 +41,15 @@ extern std::atomic<uint64_t> g_launches;
     ::spmv::cuda_check(cudaGetLastError(), #kern);                                    \
   } while (0)
 
+// Launch through the runtime API; a failed launch is cleared from the
+// runtime's last-error slot so it cannot poison the next LAUNCH check.
+inline void launch_checked(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaLaunchKernel(fn, grid, block, args, smem, s);
+  if (e != cudaSuccess) cudaGetLastError();
+  cuda_check(e, "cudaLaunchKernel");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 // Stream-ordered device allocation from the device's default pool (release
 // threshold raised once per device so repeated create/destroy reuses memory).
 void* dalloc(size_t bytes, cudaStream_t s);

@@ -365,8 +365,7 @@ void build_sell(spmv_matrix* h, int64_t C, int64_t sigma) {
 
 void build_hyb(spmv_matrix* h, int64_t K) {
   if (!h->have_features) compute_features(h);
-  if (K < 0) K = h->hyb_auto_K;
-  if (K > h->feat.max_len) K = h->feat.max_len;
+  if (K < 0) K = h->hyb_auto_K;  // an explicit K is used as given (O6), even above max_len
   dispatch(h, [&](auto rpt, auto vt) {
     using RP = std::remove_pointer_t<decltype(rpt)>;
     using V = std::remove_pointer_t<decltype(vt)>;

@@ -7,6 +7,9 @@
 namespace spmv {
 
 constexpr int kBlocks[5] = {64, 128, 256, 512, 1024};
+// Register cap actually compiled for a (block, maxreg) variant: never more
+// than the 64K-register file allows for one block of B threads.
+constexpr int regcap(int B, int R) { return R < ((65536 / B) & ~7) ? R : ((65536 / B) & ~7); }
 constexpr int kRegs[4] = {32, 64, 128, 255};
 
 inline int block_index(int b) {

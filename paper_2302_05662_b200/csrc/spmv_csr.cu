@@ -26,7 +26,7 @@ struct CsrParams {
 };
 
 template <int B, int R, class T, int LANES, class RP>
-__global__ void __launch_bounds__(B) __maxnreg__(R) k_csr_vector(const CsrParams p) {
+__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_vector(const CsrParams p) {
   constexpr int U = LANES >= 16 ? 2 : 4;
   const RP* __restrict__ rp = static_cast<const RP*>(p.rp);
   const T* __restrict__ val = static_cast<const T*>(p.val);
@@ -85,7 +85,7 @@ __device__ __forceinline__ void merge_search(const RP* rp, int64_t rows, int64_t
 }
 
 template <int B, int R, class T, int IPT, class RP>
-__global__ void __launch_bounds__(B) __maxnreg__(R) k_csr_merge(const CsrParams p) {
+__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_merge(const CsrParams p) {
   const RP* __restrict__ rp = static_cast<const RP*>(p.rp);
   const T* __restrict__ val = static_cast<const T*>(p.val);
   const T* __restrict__ x = static_cast<const T*>(p.x);
@@ -215,8 +215,7 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
       p.e.counter = h->pi_counter;
     }
     void* args[] = {&p};
-    CK(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream));
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
     return;
   }
   const int ipt = L.knob;
@@ -236,8 +235,7 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
   // afterwards by run_norms because boundary rows finish in the fixup.
   const int64_t grid = (nchunks * 32 + L.block - 1) / L.block;
   void* args[] = {&p};
-  CK(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
   run_seg_fixup(h, p.recs, nchunks, e, y);
 }
 

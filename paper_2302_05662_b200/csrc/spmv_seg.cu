@@ -59,7 +59,7 @@ __device__ __forceinline__ void load_wi(const int* p, int (&v)[W]) {
 }
 
 template <int B, int R, class T, int W>
-__global__ void __launch_bounds__(B) __maxnreg__(R) k_coo(const CooParams p) {
+__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_coo(const CooParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t chunk = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
   const int64_t base = chunk * 32 * W;
@@ -244,8 +244,7 @@ void coo_launch(spmv_matrix* h, const int32_t* row, const int32_t* col, const vo
   p.recs = static_cast<ChunkRec*>(ensure_seg_scratch(h, (size_t)nchunks * sizeof(ChunkRec)));
   const int64_t grid = (nchunks * 32 + L.block - 1) / L.block;
   void* args[] = {&p};
-  CK(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
   run_seg_fixup(h, p.recs, nchunks, e, y);
 }
 

@@ -27,7 +27,7 @@ struct SlicedParams {
 };
 
 template <int B, int R, class T, int C>
-__global__ void __launch_bounds__(B) __maxnreg__(R) k_sliced(const SlicedParams p) {
+__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const SlicedParams p) {
   constexpr int RPL = C / 32;                                       // rows per lane
   constexpr int VW = (int)(16 / sizeof(T)) < RPL ? (int)(16 / sizeof(T)) : RPL;  // elems per vector load
   constexpr int NV = RPL / VW;
@@ -146,8 +146,7 @@ void launch_sliced(spmv_matrix* h, SlicedParams& p, int C, const spmv_launch_t& 
     p.e.counter = h->pi_counter;
   }
   void* args[] = {&p};
-  CK(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
 }
 
 }  // namespace
