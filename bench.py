@@ -39,7 +39,7 @@ METRIC = "SpMV GFLOP/s & HBM GB/s vs 8 TB/s per format at 1/2/4/8 B200; MFLOPS/W
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--format", default="auto", help="auto (spmv_tune) or COO/CSR/ELL/HYB/SELL")
     ap.add_argument("--no-tune-launch", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-kernels", action="store_true", help="short run for ncu")
+    ap.add_argument("--launch", default="", help="block,maxreg,carveout,knob (skips the launch sweep)")
+    ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
 
@@ -318,7 +319,9 @@ def run_ours(args):
         fmt = P.FORMATS[args.format]
         params = {}
         P.spmv_convert(h, fmt)
-        if not args.no_tune_launch:
+        if args.launch:
+            P.spmv_set_launch(h, fmt, *[int(v) for v in args.launch.split(",")])
+        elif not args.no_tune_launch:
             P.spmv_tune(h, P.TUNE_LAUNCH, expected_iterations=E)
         launch = P.spmv_get_launch(h, fmt)
         decision = P.spmv_decision_log(h)
@@ -355,16 +358,29 @@ def run_ours(args):
     pi = PowerIteration(layout, rank, local_step, local_norm2)
     bufs = pi.make_buffers(tdt, dev, E)
 
+    phases = {} if os.environ.get("BENCH_PHASES") else None
+
+    def mark(name):
+        if phases is not None:
+            torch.cuda.synchronize()
+            phases.setdefault(name, []).append(time.perf_counter())
+
     def one_step(coo_in, host=False):
+        mark("0_start")
         h = P.spmv_create(coo_in.rows, coo_in.cols, coo_in.row, coo_in.col, coo_in.val)
         state["h"] = h
+        mark("1_create")
         P.spmv_features(h)
+        mark("2_features")
         P.spmv_convert(h, fmt, **params)
         P.spmv_set_launch(h, fmt, *launch)
         info = P.spmv_format_info(h, fmt)
+        mark("3_convert")
         pi.run(x0, E, bufs)
+        mark("4_power")
         P.spmv_destroy(h)
         state["h"] = None
+        mark("5_destroy")
         return info
 
     def barrier():
@@ -377,7 +393,7 @@ def run_ours(args):
         info = one_step(coo)
     barrier()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local) if not os.environ.get("BENCH_NO_CLOCKS") else None
     energy = Energy(local)
     state["time_kernels"] = True
     state["events"] = []
@@ -393,9 +409,18 @@ def run_ours(args):
     barrier()
     e_j1 = energy.read_j()
     launches = P.launch_count() - l0
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else None
     state["time_kernels"] = False
     ms = t_start.elapsed_time(t_end)
+    if phases is not None and rank == 0:
+        keys = sorted(phases)
+        n = min(len(phases[k]) for k in keys)
+        rep = {}
+        for a, b in zip(keys[:-1], keys[1:]):
+            d = [phases[b][i] - phases[a][i] for i in range(n)]
+            rep[b] = {"first_ms": round(d[0] * 1e3, 3), "last_ms": round(d[-1] * 1e3, 3),
+                      "median_ms": round(statistics.median(d) * 1e3, 3)}
+        print("PHASES", json.dumps(rep), file=sys.stderr, flush=True)
     kernel_ms = [a.elapsed_time(b) for a, b in state["events"]]
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -430,6 +455,8 @@ def run_ours(args):
     # ---- e2e: same metric through the C ABI with HOST buffers (rank 0 .. all ranks)
     e2e = None
     try:
+        if args.no_e2e:
+            raise RuntimeError("e2e skipped (--no-e2e)")
         host_row = coo.row.cpu().pin_memory()
         host_col = coo.col.cpu().pin_memory()
         host_val = coo.val.cpu().pin_memory()

@@ -58,6 +58,30 @@ void dfree(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
 }
 
+int64_t persistent_grid(const void* func, int block, int64_t needed_blocks) {
+  static std::unordered_map<uint64_t, int> occ;
+  static int sms = 0;
+  int per_sm;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (sms == 0) {
+      int dev = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const uint64_t key = (uint64_t)(uintptr_t)func ^ ((uint64_t)block << 48);
+    auto it = occ.find(key);
+    if (it == occ.end()) {
+      int nb = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, func, block, 0));
+      it = occ.emplace(key, std::max(nb, 1)).first;
+    }
+    per_sm = it->second;
+  }
+  const int64_t cap = (int64_t)sms * per_sm;
+  return needed_blocks < cap ? needed_blocks : cap;
+}
+
 void set_carveout(const void* func, int pct) {
   if (pct < 0) return;
   std::lock_guard<std::mutex> lk(g_mu);

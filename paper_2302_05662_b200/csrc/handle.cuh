@@ -120,6 +120,8 @@ void* ensure_seg_scratch(spmv_matrix* h, size_t bytes);
 
 // Resolve a launch variant to the defaults of its kernel.
 spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t& L);
+// Grid for a persistent (grid-stride) kernel: min(needed, SMs × resident blocks per SM).
+int64_t persistent_grid(const void* func, int block, int64_t needed_blocks);
 // Carveout attribute (cached per function pointer).
 void set_carveout(const void* func, int pct);
 

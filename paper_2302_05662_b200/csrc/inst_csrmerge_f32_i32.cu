@@ -1,0 +1,9 @@
+// instantiation unit: merge-path CSR variants, float values, int32_t row pointers
+#include "kern_csr.cuh"
+namespace spmv {
+namespace kern {
+template CsrFn csr_merge_fn<float, int32_t, 4>(int, int);
+template CsrFn csr_merge_fn<float, int32_t, 8>(int, int);
+template CsrFn csr_merge_fn<float, int32_t, 16>(int, int);
+}  // namespace kern
+}  // namespace spmv

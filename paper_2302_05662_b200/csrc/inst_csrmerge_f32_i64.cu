@@ -1,0 +1,9 @@
+// instantiation unit: merge-path CSR variants, float values, int64_t row pointers
+#include "kern_csr.cuh"
+namespace spmv {
+namespace kern {
+template CsrFn csr_merge_fn<float, int64_t, 4>(int, int);
+template CsrFn csr_merge_fn<float, int64_t, 8>(int, int);
+template CsrFn csr_merge_fn<float, int64_t, 16>(int, int);
+}  // namespace kern
+}  // namespace spmv

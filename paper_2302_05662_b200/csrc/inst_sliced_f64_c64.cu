@@ -1,0 +1,7 @@
+// instantiation unit: ELL/SELL variants, double values, C = 64
+#include "kern_sliced.cuh"
+namespace spmv {
+namespace kern {
+template SlicedFn sliced_fn<double, 64>(int, int);
+}  // namespace kern
+}  // namespace spmv

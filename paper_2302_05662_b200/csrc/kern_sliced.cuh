@@ -1,0 +1,118 @@
+// kern_sliced.cuh — ELL and SELL-C-sigma SpMV on sm_100a.
+// One kernel serves both layouts: a warp owns a slice of C rows; lane l owns
+// rows l·(C/32) .. l·(C/32)+C/32−1 of the slice, so each step k of the slice
+// width reads C consecutive values and C consecutive column indices —
+// 128-bit coalesced loads (double2/int2 for fp64 C=64, float4/int4 for fp32
+// C=128) — then gathers x through L1/L2 and accumulates in fp64.
+//   ELL : element (i, k) at k·n_pad + i     -> base = s·C,        stride = n_pad, width = K
+//   SELL: element (s,j,k) at sp[s] + k·C + j -> base = sp[s],      stride = C,     width = (sp[s+1]−sp[s])/C
+// Padding slots carry col −1 and are skipped (never multiply x, reading R9).
+// The power-step epilogue (mode 1) fuses Σy² and Σx·y into the same pass.
+#include "spmv_common.cuh"
+
+#pragma once
+#include "kern_sliced_decl.cuh"
+
+namespace spmv {
+namespace kern {
+
+
+
+template <int B, int R, class T, int C>
+__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const SlicedParams p) {
+  constexpr int RPL = C / 32;                                       // rows per lane
+  constexpr int VW = (int)(16 / sizeof(T)) < RPL ? (int)(16 / sizeof(T)) : RPL;  // elems per vector load
+  constexpr int NV = RPL / VW;
+  constexpr int U = RPL >= 8 ? 1 : 8 / RPL;                         // k-unroll (loads in flight)
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * (B / 32);
+  const T* __restrict__ val = static_cast<const T*>(p.val);
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  T* __restrict__ y = static_cast<T*>(p.y);
+  const double alpha = epi_alpha(p.e);
+  double yy = 0.0, xy = 0.0;
+  // persistent: each warp walks slices warp0, warp0 + nwarps, ... so the
+  // per-block epilogue (power-step partial sums) is paid once per block.
+  for (int64_t slice = warp0; slice < p.nslices; slice += nwarps) {
+    int64_t base, stride, width;
+    if (p.sp) {
+      base = p.sp[slice];
+      width = (p.sp[slice + 1] - base) / C;
+      stride = C;
+    } else {
+      base = slice * C;
+      width = p.ell_K;
+      stride = p.ell_stride;
+    }
+    const int32_t* __restrict__ cp = p.col + base + lane * RPL;
+    const T* __restrict__ vp = val + base + lane * RPL;
+    double acc[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) acc[r] = 0.0;
+    for (int64_t k = 0; k < width; k += U) {
+      T v[U][RPL];
+      int c[U][RPL];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = k + u < width;  // predicated tail batch
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          T tv[VW];
+          int tc[VW];
+          if (ok) {
+            load_vals<T, VW>(vp + (k + u) * stride + q * VW, tv);
+            load_cols<VW>(cp + (k + u) * stride + q * VW, tc);
+          } else {
+#pragma unroll
+            for (int w = 0; w < VW; ++w) {
+              tv[w] = T(0);
+              tc[w] = -1;
+            }
+          }
+#pragma unroll
+          for (int w = 0; w < VW; ++w) {
+            v[u][q * VW + w] = tv[w];
+            c[u][q * VW + w] = tc[w];
+          }
+        }
+      }
+      T xv[U][RPL];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) xv[u][r] = c[u][r] >= 0 ? ld_x(x + c[u][r]) : T(0);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) acc[r] = fma((double)v[u][r], (double)xv[u][r], acc[r]);
+    }
+    const int64_t r0 = slice * C + lane * RPL;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int64_t ri = r0 + r;
+      if (ri < p.rows) {
+        const int64_t row = p.perm ? (int64_t)p.perm[ri] : ri;
+        const T out = epi_value<T>(p.e, alpha, acc[r], y, row);
+        y[row] = out;
+        if (p.e.mode == 1) {
+          yy += (double)out * (double)out;
+          xy += (double)x[p.e.row_offset + row] * (double)out;
+        }
+      }
+    }
+  }
+  if (p.e.mode == 1) power_reduce(p.e, yy, xy);
+}
+
+
+#define SL_ROW(B) {&k_sliced<B, 32, T, C>, &k_sliced<B, 64, T, C>, &k_sliced<B, 128, T, C>, &k_sliced<B, 255, T, C>}
+template <class T, int C>
+SlicedFn sliced_fn(int bi, int ri) {
+  static const SlicedFn tab[5][4] = {SL_ROW(64), SL_ROW(128), SL_ROW(256), SL_ROW(512), SL_ROW(1024)};
+  return tab[bi][ri];
+}
+#undef SL_ROW
+
+}  // namespace kern
+}  // namespace spmv

@@ -1,189 +1,10 @@
-// spmv_csr.cu — CSR SpMV kernels on sm_100a ("This format requires
-// coordination among threads within a warp to accumulate per-thread results
-// together").
-//   k_csr_vector<LANES>: LANES ∈ {1 (scalar), 2, 4, 8, 16, 32} consecutive
-//     lanes per row, strided coalesced loads of col/val, shuffle reduction;
-//     LANES picked from the mean row length (reading R13).
-//   k_csr_merge<IPT>: merge-path CSR (Merrill & Garland) for skewed rows:
-//     every lane consumes exactly IPT items of the merged (row-end, nnz)
-//     sequence, so one 150K-entry row and 4M empty rows cost the same per
-//     item; rows crossing lanes are combined with a warp segmented scan, rows
-//     crossing warps through chunk records + k_seg_fixup (deterministic).
-#include "spmv_common.cuh"
+// spmv_csr.cu — CSR launchers (kernels: kern_csr.cuh).
+#include "kern_csr_decl.cuh"
 
 namespace spmv {
-namespace {
-
-struct CsrParams {
-  const void* rp;
-  const int32_t* col;
-  const void* val;
-  int64_t rows, nnz;
-  const void* x;
-  void* y;
-  Epilogue e;
-  ChunkRec* recs;
-};
-
-template <int B, int R, class T, int LANES, class RP>
-__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_vector(const CsrParams p) {
-  constexpr int U = LANES >= 16 ? 2 : 4;
-  const RP* __restrict__ rp = static_cast<const RP*>(p.rp);
-  const T* __restrict__ val = static_cast<const T*>(p.val);
-  const T* __restrict__ x = static_cast<const T*>(p.x);
-  T* __restrict__ y = static_cast<T*>(p.y);
-  const int64_t gt = (int64_t)blockIdx.x * B + threadIdx.x;
-  const int64_t row = gt / LANES;
-  const int li = (int)(threadIdx.x & (LANES - 1));
-  const double alpha = epi_alpha(p.e);
-  double acc = 0.0;
-  if (row < p.rows) {
-    const int64_t a = rp[row], b = rp[row + 1];
-    int64_t k = a + li;
-    for (; k + (U - 1) * LANES < b; k += U * LANES) {
-      int c[U];
-      T v[U], xv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        c[u] = ld_stream(p.col + k + u * LANES);
-        v[u] = ld_stream(val + k + u * LANES);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u]);
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc = fma((double)v[u], (double)xv[u], acc);
-    }
-    for (; k < b; k += LANES) acc = fma((double)ld_stream(val + k), (double)ld_x(x + ld_stream(p.col + k)), acc);
-  }
-#pragma unroll
-  for (int o = LANES / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  double yy = 0.0, xy = 0.0;
-  if (row < p.rows && li == 0) {
-    const T out = epi_value<T>(p.e, alpha, acc, y, row);
-    y[row] = out;
-    if (p.e.mode == 1) {
-      yy = (double)out * (double)out;
-      xy = (double)x[p.e.row_offset + row] * (double)out;
-    }
-  }
-  if (p.e.mode == 1) power_reduce(p.e, yy, xy);
-}
-
-// ------------------------------------------------------------------ merge-path
-template <class RP>
-__device__ __forceinline__ void merge_search(const RP* rp, int64_t rows, int64_t nnz, int64_t d, int64_t& x,
-                                             int64_t& yk) {
-  int64_t lo = d - nnz > 0 ? d - nnz : 0;
-  int64_t hi = d < rows ? d : rows;
-  while (lo < hi) {
-    int64_t pivot = (lo + hi) >> 1;
-    if ((int64_t)rp[pivot + 1] <= d - pivot - 1) lo = pivot + 1;
-    else hi = pivot;
-  }
-  x = lo < rows ? lo : rows;
-  yk = d - lo;
-}
-
-template <int B, int R, class T, int IPT, class RP>
-__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_merge(const CsrParams p) {
-  const RP* __restrict__ rp = static_cast<const RP*>(p.rp);
-  const T* __restrict__ val = static_cast<const T*>(p.val);
-  const T* __restrict__ x = static_cast<const T*>(p.x);
-  T* __restrict__ y = static_cast<T*>(p.y);
-  const int lane = threadIdx.x & 31;
-  const int64_t chunk = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
-  const int64_t total = p.rows + p.nnz;
-  const int64_t d0 = chunk * 32 * IPT;
-  if (d0 >= total) return;  // whole warp exits together
-  const double alpha = epi_alpha(p.e);
-  const int64_t d = d0 + (int64_t)lane * IPT;
-  int64_t xr, yk;
-  merge_search(rp, p.rows, p.nnz, d < total ? d : total, xr, yk);
-  // chunk start coordinate (lane 0's) and whether its first row began earlier
-  const int64_t x0 = __shfl_sync(0xffffffffu, xr, 0);
-  const int64_t y0 = __shfl_sync(0xffffffffu, yk, 0);
-  const bool cont_in = x0 < p.rows && y0 > (int64_t)rp[x0];
-  const int64_t xs = xr;  // this lane's start row
-  double acc = 0.0, first_part = 0.0;
-  int64_t first_row = -1;  // first row completed by this lane
-  int64_t row_end = xr < p.rows ? (int64_t)rp[xr + 1] : 0;
-#pragma unroll 4
-  for (int i = 0; i < IPT; ++i) {
-    if (d + i >= total) break;
-    if (yk < row_end) {
-      acc = fma((double)ld_stream(val + yk), (double)ld_x(x + ld_stream(p.col + yk)), acc);
-      ++yk;
-    } else {
-      if (first_row < 0) {
-        first_row = xr;
-        first_part = acc;
-      } else {
-        y[xr] = epi_value<T>(p.e, alpha, acc, y, xr);
-      }
-      acc = 0.0;
-      ++xr;
-      row_end = xr < p.rows ? (int64_t)rp[xr + 1] : 0;
-    }
-  }
-  // lane carry-out: (row xr in progress, acc). Warp inclusive segmented scan.
-  double s = acc;
-  const int64_t key = xr;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    double su = __shfl_up_sync(0xffffffffu, s, o);
-    int64_t ku = __shfl_up_sync(0xffffffffu, key, o);
-    if (lane >= o && ku == key) s += su;
-  }
-  const double s_prev = __shfl_up_sync(0xffffffffu, s, 1);
-  const int64_t k_prev = __shfl_up_sync(0xffffffffu, key, 1);
-  const double carry_in = (lane > 0 && k_prev == xs) ? s_prev : 0.0;
-  if (first_row >= 0) {
-    const double tot = carry_in + first_part;
-    if (cont_in && first_row == x0) p.recs[chunk].head = tot;
-    else y[first_row] = epi_value<T>(p.e, alpha, tot, y, first_row);
-  }
-  if (lane == 31) {
-    ChunkRec& rec = p.recs[chunk];
-    rec.first_row = (int32_t)x0;
-    rec.cont_in = cont_in;
-    const bool cont_out = xr < p.rows && yk > (int64_t)rp[xr];
-    rec.last_row = (int32_t)(xr < p.rows ? xr : p.rows - 1);
-    rec.cont_out = cont_out;
-    if (cont_out) {
-      rec.tail = s;
-      if (cont_in && xr == x0) rec.head = s;
-    }
-  }
-}
-
-template <class T, class RP>
-using CsrFn = void (*)(const CsrParams);
-
-#define CSRV_ROW(B, L) {&k_csr_vector<B, 32, T, L, RP>, &k_csr_vector<B, 64, T, L, RP>, \
-                        &k_csr_vector<B, 128, T, L, RP>, &k_csr_vector<B, 255, T, L, RP>}
-#define CSRV_TAB(L) {CSRV_ROW(64, L), CSRV_ROW(128, L), CSRV_ROW(256, L), CSRV_ROW(512, L), CSRV_ROW(1024, L)}
-template <class T, class RP, int L>
-CsrFn<T, RP> csr_vector_fn(int bi, int ri) {
-  static const CsrFn<T, RP> tab[5][4] = CSRV_TAB(L);
-  return tab[bi][ri];
-}
-#undef CSRV_TAB
-#undef CSRV_ROW
-
-#define CSRM_ROW(B, I) {&k_csr_merge<B, 32, T, I, RP>, &k_csr_merge<B, 64, T, I, RP>, \
-                        &k_csr_merge<B, 128, T, I, RP>, &k_csr_merge<B, 255, T, I, RP>}
-#define CSRM_TAB(I) {CSRM_ROW(64, I), CSRM_ROW(128, I), CSRM_ROW(256, I), CSRM_ROW(512, I), CSRM_ROW(1024, I)}
-template <class T, class RP, int I>
-CsrFn<T, RP> csr_merge_fn(int bi, int ri) {
-  static const CsrFn<T, RP> tab[5][4] = CSRM_TAB(I);
-  return tab[bi][ri];
-}
-#undef CSRM_TAB
-#undef CSRM_ROW
-
 template <class T, class RP>
 void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L) {
-  CsrParams p{};
+  kern::CsrParams p{};
   p.rp = h->row_ptr;
   p.col = h->col;
   p.val = h->val;
@@ -198,16 +19,18 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     const int lanes = L.knob;
     const void* fn;
     switch (lanes) {
-      case 1: fn = (const void*)csr_vector_fn<T, RP, 1>(bi, ri); break;
-      case 2: fn = (const void*)csr_vector_fn<T, RP, 2>(bi, ri); break;
-      case 4: fn = (const void*)csr_vector_fn<T, RP, 4>(bi, ri); break;
-      case 8: fn = (const void*)csr_vector_fn<T, RP, 8>(bi, ri); break;
-      case 16: fn = (const void*)csr_vector_fn<T, RP, 16>(bi, ri); break;
-      case 32: fn = (const void*)csr_vector_fn<T, RP, 32>(bi, ri); break;
+      case 1: fn = (const void*)kern::csr_vector_fn<T, RP, 1>(bi, ri); break;
+      case 2: fn = (const void*)kern::csr_vector_fn<T, RP, 2>(bi, ri); break;
+      case 4: fn = (const void*)kern::csr_vector_fn<T, RP, 4>(bi, ri); break;
+      case 8: fn = (const void*)kern::csr_vector_fn<T, RP, 8>(bi, ri); break;
+      case 16: fn = (const void*)kern::csr_vector_fn<T, RP, 16>(bi, ri); break;
+      case 32: fn = (const void*)kern::csr_vector_fn<T, RP, 32>(bi, ri); break;
       default: fail(SPMV_ERR_INVALID_ARG, "CSR-vector lanes per row must be 1,2,4,8,16 or 32");
     }
     set_carveout(fn, L.carveout_pct);
-    const int64_t grid = (h->rows * lanes + L.block - 1) / L.block;
+    const int ur = lanes >= 16 ? 4 : (lanes >= 4 ? 2 : 1);
+    const int64_t groups = (h->rows + ur - 1) / ur;
+    const int64_t grid = persistent_grid(fn, L.block, (groups * lanes + L.block - 1) / L.block);
     if (grid <= 0) return;
     if (e.mode == 1) {
       ensure_pi_scratch(h, (size_t)grid);
@@ -221,9 +44,9 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
   const int ipt = L.knob;
   const void* fn;
   switch (ipt) {
-    case 4: fn = (const void*)csr_merge_fn<T, RP, 4>(bi, ri); break;
-    case 8: fn = (const void*)csr_merge_fn<T, RP, 8>(bi, ri); break;
-    case 16: fn = (const void*)csr_merge_fn<T, RP, 16>(bi, ri); break;
+    case 4: fn = (const void*)kern::csr_merge_fn<T, RP, 4>(bi, ri); break;
+    case 8: fn = (const void*)kern::csr_merge_fn<T, RP, 8>(bi, ri); break;
+    case 16: fn = (const void*)kern::csr_merge_fn<T, RP, 16>(bi, ri); break;
     default: fail(SPMV_ERR_INVALID_ARG, "merge-path items per thread must be 4, 8 or 16");
   }
   set_carveout(fn, L.carveout_pct);
@@ -238,8 +61,6 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
   launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
   run_seg_fixup(h, p.recs, nchunks, e, y);
 }
-
-}  // namespace
 
 void run_csr(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L) {
   if (h->dtype == SPMV_R64F) {

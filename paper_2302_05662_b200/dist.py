@@ -106,10 +106,14 @@ class PowerIteration:
         self.local_norm2(cur[self.rank * L.chunk: self.rank * L.chunk + nloc], sums[0])
         self._allreduce(sums[0])
         for k in range(steps):
-            y_local = chunk_buf[:nloc]
-            self.local_step(cur, y_local, sums[k], sums[k + 1], self.rank * L.chunk)
-            self._allreduce(sums[k + 1])
-            self._allgather(nxt, chunk_buf)
+            if self.dist is None and L.world == 1:
+                # single rank: the SpMV writes the next iterate in place (no gather)
+                self.local_step(cur, nxt[:nloc], sums[k], sums[k + 1], 0)
+            else:
+                y_local = chunk_buf[:nloc]
+                self.local_step(cur, y_local, sums[k], sums[k + 1], self.rank * L.chunk)
+                self._allreduce(sums[k + 1])
+                self._allgather(nxt, chunk_buf)
             cur, nxt = nxt, cur
             if on_step is not None:
                 on_step(k)
