@@ -55,48 +55,56 @@ def parse():
 # ----------------------------------------------------------------------------- clocks / energy
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled DURING the timed
+    region by an in-process NVML thread (an nvidia-smi -lms subprocess
+    measurably stalls the CUDA launch path, so it is not used)."""
 
-    def __init__(self, index=0):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+
+    def __init__(self, index=0, period_s=0.25):
+        import threading
+        self.samples = []
+        self.stop_ev = threading.Event()
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.p = None
+            self.h = None
+            return
+        self.period = period_s
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                try:
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            self.stop_ev.wait(self.period)
 
     def stop(self):
-        if self.p is None:
+        if self.h is None:
             return None
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.flush()
-        rows = []
-        for line in open(self.f.name):
-            parts = [s.strip() for s in line.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
-        os.unlink(self.f.name)
-        if not rows:
-            return None
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for n, v in zip(names, r[5:9]):
-                if v.strip().lower() == "active":
-                    reasons.add(n)
-        loaded = [s for s in sm if s > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(rows)}
+        self.stop_ev.set()
+        self.t.join(timeout=2)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        loaded = [s for s in sm if s > 0.5 * self.max_mhz] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm), "source": "NVML thread, 250 ms"}
 
 
 class Energy:
@@ -275,7 +283,7 @@ def stored_bytes_power(info_bytes, rows, cols, vb):
 def run_ours(args):
     import torch
     import paper_2302_05662_b200 as P
-    from paper_2302_05662_b200.dist import Layout, PowerIteration
+    from paper_2302_05662_b200.dist import Layout, NativeComm, PowerIteration, native_power_iteration
     import spmv_inputs as si
 
     world, rank, local = setup_dist(args)
@@ -338,25 +346,20 @@ def run_ours(args):
         params = {}
 
     stream = torch.cuda.current_stream()
-    kernel_ms = []
-    state = {}
+    state = {"kms": []}
+    comm = NativeComm(rank, world, local) if world > 1 else None
+    bufs = {
+        "cur": torch.zeros(layout.padded_n if world > 1 else n_global, dtype=tdt, device=dev),
+        "nxt": torch.zeros(layout.padded_n if world > 1 else n_global, dtype=tdt, device=dev),
+        "chunk": torch.zeros(layout.chunk, dtype=tdt, device=dev),
+        "sums": torch.zeros(E + 1, 2, dtype=torch.float64, device=dev)}
 
-    def local_step(x, y, sp, so, off):
-        if state.get("time_kernels"):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            P.spmv_power_step(state["h"], x, y, sp, so, off)
-            e1.record(stream)
-            state["events"].append((e0, e1))
-        else:
-            P.spmv_power_step(state["h"], x, y, sp, so, off)
-
-    def local_norm2(xl, so):
-        P.spmv_norm2(state["h"], xl, so)
-
-    pi = PowerIteration(layout, rank, local_step, local_norm2)
-    bufs = pi.make_buffers(tdt, dev, E)
+    def power(h, x_start):
+        z, sums, kms = native_power_iteration(h, layout, rank, x_start, bufs, E, comm,
+                                              time_kernels=state.get("time_kernels", False))
+        if kms:
+            state["kms"].extend(kms)
+        return z, sums
 
     phases = {} if os.environ.get("BENCH_PHASES") else None
 
@@ -376,7 +379,7 @@ def run_ours(args):
         P.spmv_set_launch(h, fmt, *launch)
         info = P.spmv_format_info(h, fmt)
         mark("3_convert")
-        pi.run(x0, E, bufs)
+        power(h, x0)
         mark("4_power")
         P.spmv_destroy(h)
         state["h"] = None
@@ -395,13 +398,14 @@ def run_ours(args):
 
     clocks = ClockSampler(local) if not os.environ.get("BENCH_NO_CLOCKS") else None
     energy = Energy(local)
-    state["time_kernels"] = True
-    state["events"] = []
+    state["time_kernels"] = not os.environ.get("BENCH_NO_KEVENTS")
+    state["kms"] = []
     l0 = P.launch_count()
     e_j0 = energy.read_j()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     barrier()
+    state["host_t0"] = time.perf_counter()
     t_start.record(stream)
     for _ in range(args.steps):
         info = one_step(coo)
@@ -412,6 +416,7 @@ def run_ours(args):
     clk = clocks.stop() if clocks else None
     state["time_kernels"] = False
     ms = t_start.elapsed_time(t_end)
+    host_s = time.perf_counter() - state.get("host_t0", time.perf_counter())
     if phases is not None and rank == 0:
         keys = sorted(phases)
         n = min(len(phases[k]) for k in keys)
@@ -421,7 +426,7 @@ def run_ours(args):
             rep[b] = {"first_ms": round(d[0] * 1e3, 3), "last_ms": round(d[-1] * 1e3, 3),
                       "median_ms": round(statistics.median(d) * 1e3, 3)}
         print("PHASES", json.dumps(rep), file=sys.stderr, flush=True)
-    kernel_ms = [a.elapsed_time(b) for a, b in state["events"]]
+    kernel_ms = list(state["kms"])
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
@@ -472,7 +477,7 @@ def run_ours(args):
             P.spmv_set_launch(h, fmt, *launch)
             xdev = torch.empty_like(x0)
             xdev.copy_(host_x0, non_blocking=True)
-            z, sums = pi.run(xdev, E, bufs)
+            z, sums = power(h, xdev)
             y_host.copy_(z, non_blocking=True)
             s_host.copy_(sums, non_blocking=True)
             torch.cuda.synchronize()
@@ -531,11 +536,14 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "host_ms_per_step": round(host_s * 1e3 / args.steps, 3),
             "clocks": clk,
             "lambda_last": float(lam[-1]) if lam is not None and len(lam) else None,
             "tuner": summarize_decisions(decision),
         }
         print(json.dumps(out), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

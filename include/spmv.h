@@ -45,7 +45,8 @@ typedef enum {
   SPMV_ERR_OUT_OF_MEMORY = 5,
   SPMV_ERR_UNSUPPORTED = 6,        /* rows/cols > 2^31-1, SELL C not in {32,64,128,256}, ... */
   SPMV_ERR_CUDA = 7,               /* CUDA runtime error (sticky device faults surface here) */
-  SPMV_ERR_NOT_CONVERTED = 8       /* requested format has not been built on this handle */
+  SPMV_ERR_NOT_CONVERTED = 8,      /* requested format has not been built on this handle */
+  SPMV_ERR_NCCL = 9                /* NCCL missing or a collective failed */
 } spmv_status_t;
 
 typedef enum { SPMV_R32F = 0, SPMV_R64F = 1 } spmv_dtype_t;
@@ -221,6 +222,20 @@ spmv_status_t spmv_power_step(spmv_handle_t h, const void* x, void* y, const dou
 /* sums_out[0] = Σ x_i², sums_out[1] = 0 over n values of x (device). */
 spmv_status_t spmv_norm2(spmv_handle_t h, const void* x, int64_t n, double* sums_out);
 
+/* The whole E-step power iteration on the handle's stream (no host round
+ * trips): buf0 <- x0 (n_full values, may alias buf0), S_0 = Σ over ranks of
+ * ||own rows of buf0||², then per step k: one spmv_power_step into the next
+ * buffer (comm = NULL) or into chunk_buf followed by ncclAllReduce(sums[k+1])
+ * and ncclAllGather(chunk_buf -> next buffer, chunk values per rank).
+ * sums: device double[(steps+1)·2] (row k = [S_k, D_k]); lambda_k =
+ * D_k / sqrt(S_{k-1}). buf0/buf1: device, n_full values (n_full = rows for a
+ * single rank, world·chunk in the padded multi-GPU layout). kernel_ms: host
+ * float[steps] (optional) receives each SpMV launch's CUDA-event time (the
+ * call then synchronises). *final_buf (optional) = 0/1: which buffer holds z_E. */
+spmv_status_t spmv_power_iterate(spmv_handle_t h, const void* x0, void* buf0, void* buf1, int64_t n_full,
+                                 int64_t steps, double* sums, void* comm, int64_t chunk, void* chunk_buf,
+                                 float* kernel_ms, int* final_buf);
+
 /* ---------------------------------------------------------------- introspection */
 spmv_status_t spmv_format_info(spmv_handle_t h, spmv_format_t fmt, spmv_format_info_t* out);
 /* Copy a format array into dst (`where` = host or device), dst_bytes >= array bytes. */
@@ -242,6 +257,14 @@ spmv_status_t spmv_overheads(spmv_handle_t h, double* f_latency_s, double* c_lat
 uint64_t spmv_launch_count(void);
 /* Release memory cached by the library's stream-ordered pool. */
 spmv_status_t spmv_trim_pool(int device);
+
+/* ---------------------------------------------------------------- multi-GPU (NCCL)
+ * One process per GPU. Rank 0 creates the 128-byte NCCL unique id; the caller
+ * broadcasts it (e.g. torch.distributed); every rank then calls
+ * spmv_dist_init. libnccl.so.2 is loaded on first use (dlopen). */
+spmv_status_t spmv_dist_unique_id(uint8_t out[128]);
+spmv_status_t spmv_dist_init(void** comm, const uint8_t unique_id[128], int rank, int world, int device);
+spmv_status_t spmv_dist_destroy(void* comm); /* NULL is a no-op */
 
 /* ---------------------------------------------------------------- multi-GPU host logic
  * nnz-balanced row partition: bounds[0] = 0,

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libspmv.so")
 
 # ---------------------------------------------------------------- enums (spmv.h)
 OK, ERR_INVALID_ARG, ERR_INDEX_OUT_OF_RANGE, ERR_DUPLICATE, ERR_INFEASIBLE, ERR_OUT_OF_MEMORY, \
-    ERR_UNSUPPORTED, ERR_CUDA, ERR_NOT_CONVERTED = range(9)
+    ERR_UNSUPPORTED, ERR_CUDA, ERR_NOT_CONVERTED, ERR_NCCL = range(10)
 R32F, R64F = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
 FMT_COO, FMT_CSR, FMT_ELL, FMT_HYB, FMT_SELL = 0, 1, 2, 3, 4
@@ -114,6 +114,11 @@ def lib():
         "spmv_overheads": ([H, ctypes.POINTER(d), ctypes.POINTER(d)], i32),
         "spmv_launch_count": ([], ctypes.c_uint64),
         "spmv_trim_pool": ([i32], i32),
+        "spmv_power_iterate": ([H, vp, vp, vp, i64, i64, vp, vp, i64, vp, ctypes.POINTER(ctypes.c_float),
+                                ctypes.POINTER(ctypes.c_int)], i32),
+        "spmv_dist_unique_id": ([ctypes.c_char_p], i32),
+        "spmv_dist_init": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, i32, i32], i32),
+        "spmv_dist_destroy": ([vp], i32),
         "spmv_dist_partition": ([i64, vp, i32, vp], i32),
         "spmv_dist_partition_lengths": ([i64, vp, i32, vp], i32),
         "spmv_dist_remap_columns": ([vp, i64, vp, i32, i32, vp], i32),
@@ -230,6 +235,34 @@ def spmv_tune(h, flags=TUNE_ALL, expected_iterations=100):
 
 def spmv_power_step(h, x, y, sums_prev, sums_out, row_offset=0):
     _check(lib().spmv_power_step(h, _ptr(x), _ptr(y), _ptr(sums_prev), _ptr(sums_out), int(row_offset)), h)
+
+
+def spmv_power_iterate(h, x0, buf0, buf1, steps, sums, comm=None, chunk=0, chunk_buf=None,
+                       time_kernels=False):
+    """Native E-step power iteration (see spmv.h). Returns (final_buf_index,
+    per-launch kernel ms list or None)."""
+    km = (ctypes.c_float * max(int(steps), 1))() if time_kernels else None
+    fb = ctypes.c_int(0)
+    _check(lib().spmv_power_iterate(h, _ptr(x0), _ptr(buf0), _ptr(buf1), int(buf0.numel()), int(steps),
+                                    _ptr(sums), comm, int(chunk), _ptr(chunk_buf), km, ctypes.byref(fb)), h)
+    return fb.value, (list(km)[:int(steps)] if km is not None else None)
+
+
+def spmv_dist_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().spmv_dist_unique_id(buf))
+    return buf.raw[:128]
+
+
+def spmv_dist_init(uid: bytes, rank: int, world: int, device: int):
+    c = ctypes.c_void_p()
+    _check(lib().spmv_dist_init(ctypes.byref(c), uid, rank, world, device))
+    return c
+
+
+def spmv_dist_destroy(comm):
+    if comm is not None:
+        lib().spmv_dist_destroy(comm)
 
 
 def spmv_norm2(h, x, sums_out):

@@ -173,8 +173,9 @@ static bool fused_norms(const spmv_matrix* h, int fmt) {
   return fmt == SPMV_FMT_ELL || fmt == SPMV_FMT_SELL || (fmt == SPMV_FMT_CSR && h->csr_alg != SPMV_CSR_MERGE);
 }
 
-static void power_step(spmv_matrix* h, int fmt, const void* x, void* y, const double* sums_prev, double* sums_out,
-                       int64_t row_offset) {
+void power_step_internal(spmv_matrix* h, const void* x, void* y, const double* sums_prev, double* sums_out,
+                         int64_t row_offset) {
+  const int fmt = h->active;
   Epilogue e;
   e.mode = 1;
   e.sums_prev = sums_prev;
@@ -189,6 +190,17 @@ static void power_step(spmv_matrix* h, int fmt, const void* x, void* y, const do
   e.counter = h->pi_counter;
   dispatch(h, fmt, e, x, y, h->launch[fmt]);
   if (!fused_norms(h, fmt)) run_norms(h, e, x, y, h->rows);
+}
+
+void spmv_norm2_internal(spmv_matrix* h, const void* x, int64_t n, double* sums_out) {
+  if (n == 0) {
+    CK(cudaMemsetAsync(sums_out, 0, 2 * sizeof(double), h->stream));
+    return;
+  }
+  Epilogue e;
+  e.mode = 1;
+  e.sums_out = sums_out;
+  run_norms(h, e, nullptr, x, n);
 }
 
 // ------------------------------------------------------------------ timing
@@ -661,7 +673,7 @@ spmv_status_t spmv_power_step(spmv_handle_t h, const void* x, void* y, const dou
   if (!built(h, h->active)) return SPMV_ERR_NOT_CONVERTED;
   API_TRY
   DeviceGuard g(h->device);
-  power_step(h, h->active, x, y, sums_prev, sums_out, row_offset);
+  power_step_internal(h, x, y, sums_prev, sums_out, row_offset);
   API_CATCH(h)
 }
 
@@ -669,15 +681,41 @@ spmv_status_t spmv_norm2(spmv_handle_t h, const void* x, int64_t n, double* sums
   if (!h || !sums_out || n < 0 || (n > 0 && !x)) return SPMV_ERR_INVALID_ARG;
   API_TRY
   DeviceGuard g(h->device);
-  if (n == 0) {
-    CK(cudaMemsetAsync(sums_out, 0, 2 * sizeof(double), h->stream));
-  } else {
-    Epilogue e;
-    e.mode = 1;
-    e.sums_out = sums_out;
-    run_norms(h, e, nullptr, x, n);
-  }
+  spmv_norm2_internal(h, x, n, sums_out);
   API_CATCH(h)
+}
+
+spmv_status_t spmv_power_iterate(spmv_handle_t h, const void* x0, void* buf0, void* buf1, int64_t n_full,
+                                 int64_t steps, double* sums, void* comm, int64_t chunk, void* chunk_buf,
+                                 float* kernel_ms, int* final_buf) {
+  if (!h || !x0 || !buf0 || !buf1 || !sums || steps < 0 || n_full < h->rows || buf0 == buf1) return SPMV_ERR_INVALID_ARG;
+  if (comm && (!chunk_buf || chunk < h->rows)) return SPMV_ERR_INVALID_ARG;
+  if (!built(h, h->active)) return SPMV_ERR_NOT_CONVERTED;
+  API_TRY
+  DeviceGuard g(h->device);
+  power_iterate(h, x0, buf0, buf1, n_full, steps, sums, comm, chunk, chunk_buf, kernel_ms, final_buf);
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_dist_unique_id(uint8_t out[128]) {
+  if (!out) return SPMV_ERR_INVALID_ARG;
+  API_TRY
+  dist_unique_id(out);
+  API_CATCH(kNoHandle)
+}
+
+spmv_status_t spmv_dist_init(void** comm, const uint8_t unique_id[128], int rank, int world, int device) {
+  if (!comm || !unique_id || world < 1 || rank < 0 || rank >= world) return SPMV_ERR_INVALID_ARG;
+  *comm = nullptr;
+  API_TRY
+  *comm = dist_init(unique_id, rank, world, device);
+  API_CATCH(kNoHandle)
+}
+
+spmv_status_t spmv_dist_destroy(void* comm) {
+  API_TRY
+  dist_destroy(comm);
+  API_CATCH(kNoHandle)
 }
 
 spmv_status_t spmv_format_info(spmv_handle_t h, spmv_format_t fmt, spmv_format_info_t* o) {
@@ -769,6 +807,7 @@ const char* spmv_status_string(spmv_status_t s) {
     case SPMV_ERR_UNSUPPORTED: return "SPMV_ERR_UNSUPPORTED";
     case SPMV_ERR_CUDA: return "SPMV_ERR_CUDA";
     case SPMV_ERR_NOT_CONVERTED: return "SPMV_ERR_NOT_CONVERTED";
+    case SPMV_ERR_NCCL: return "SPMV_ERR_NCCL";
   }
   return "SPMV_ERR_UNKNOWN";
 }

@@ -114,6 +114,16 @@ void run_hyb(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const sp
 // Σ y_i², Σ x_own_i·y_i over rows (power mode for formats without a fused epilogue).
 void run_norms(spmv_matrix* h, const Epilogue& e, const void* x, const void* y, int64_t n);
 
+// Power step / norm (api.cu) and the native loop + NCCL (dist.cu).
+void power_step_internal(spmv_matrix* h, const void* x, void* y, const double* sums_prev, double* sums_out,
+                         int64_t row_offset);
+void spmv_norm2_internal(spmv_matrix* h, const void* x, int64_t n, double* sums_out);
+void power_iterate(spmv_matrix* h, const void* x0, void* buf0, void* buf1, int64_t n_full, int64_t steps,
+                   double* sums, void* comm, int64_t chunk, void* chunk_buf, float* kernel_ms, int* final_buf);
+void* dist_init(const uint8_t id[128], int rank, int world, int device);
+void dist_unique_id(uint8_t out[128]);
+void dist_destroy(void* comm);
+
 // Make sure the power-step partial buffers hold >= nblocks entries.
 void ensure_pi_scratch(spmv_matrix* h, size_t nblocks);
 void* ensure_seg_scratch(spmv_matrix* h, size_t bytes);

@@ -135,6 +135,42 @@ class PowerIteration:
         return s[1:, 1] / np.sqrt(s[:-1, 0])
 
 
+class NativeComm:
+    """NCCL communicator of libspmv.so, bootstrapped through torch.distributed
+    (rank 0 creates the unique id, a broadcast shares it)."""
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import spmv_dist_init, spmv_dist_unique_id
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            uid = torch.frombuffer(bytearray(spmv_dist_unique_id()), dtype=torch.uint8).clone()
+        if dist.is_initialized() and world > 1:
+            t = uid.to(f"cuda:{device}") if dist.get_backend(group) == "nccl" else uid
+            dist.broadcast(t, 0, group=group)
+            uid = t.cpu()
+        self.comm = spmv_dist_init(bytes(uid.numpy().tobytes()), rank, world, device)
+        self.rank, self.world = rank, world
+
+    def close(self):
+        from . import spmv_dist_destroy
+        if self.comm is not None:
+            spmv_dist_destroy(self.comm)
+            self.comm = None
+
+
+def native_power_iteration(h, layout: Layout, rank: int, x0, bufs, steps: int, comm=None, time_kernels=False):
+    """E power steps in one C-ABI call (loop + NCCL exchange in C++).
+    Returns (z_E tensor view, sums, kernel_ms or None)."""
+    from . import spmv_power_iterate
+    c = comm.comm if comm is not None else None
+    fb, kms = spmv_power_iterate(h, x0, bufs["cur"], bufs["nxt"], steps, bufs["sums"], c, layout.chunk,
+                                 bufs["chunk"] if c is not None else None, time_kernels)
+    z = bufs["cur"] if fb == 0 else bufs["nxt"]
+    return z, bufs["sums"], kms
+
+
 def partition_rows(row_lengths, world):
     """nnz-balanced bounds via the C ABI (pure host integer logic)."""
     from . import spmv_dist_partition_lengths

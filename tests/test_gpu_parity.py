@@ -364,3 +364,52 @@ def test_tune_invariants():
         assert rep0.converted == 0 and rep0.format == P.FMT_CSR
     finally:
         P.spmv_destroy(h)
+
+
+# ------------------------------------------------------------------ native loop (+ NCCL at world 1)
+
+@pytest.mark.parametrize("use_comm", [False, True])
+def test_native_power_iterate_matches_stepwise(use_comm):
+    from paper_2302_05662_b200.dist import Layout, NativeComm, native_power_iteration
+    coo = si.stencil27(10, random_values=True)
+    h = create(coo)
+    comm = None
+    try:
+        P.spmv_convert(h, P.FMT_SELL)
+        n, E = coo.rows, 7
+        x0 = torch.from_numpy(vec(n, 21, "f64")).cuda()
+        layout = Layout.from_bounds(np.array([0, n]))
+        bufs = {"cur": torch.zeros(n, dtype=torch.float64, device="cuda"),
+                "nxt": torch.zeros(n, dtype=torch.float64, device="cuda"),
+                "chunk": torch.zeros(n, dtype=torch.float64, device="cuda"),
+                "sums": torch.zeros(E + 1, 2, dtype=torch.float64, device="cuda")}
+        if use_comm:
+            comm = NativeComm(0, 1, 0)
+        z, sums, kms = native_power_iteration(h, layout, 0, x0, bufs, E, comm, time_kernels=True)
+        torch.cuda.synchronize()
+        assert kms is not None and len(kms) == E and all(k > 0 for k in kms)
+        # step-by-step through spmv_power_step must give bitwise the same iterates
+        zp = x0.clone()
+        sp = torch.zeros(2, dtype=torch.float64, device="cuda")
+        P.spmv_norm2(h, zp, sp)
+        for k in range(E):
+            zn = torch.empty_like(zp)
+            sn = torch.zeros(2, dtype=torch.float64, device="cuda")
+            P.spmv_power_step(h, zp, zn, sp, sn)
+            assert torch.equal(sn, sums[k + 1])
+            zp, sp = zn, sn
+        assert torch.equal(zp, z)
+        # and the oracle's lambda (O11) on the same start vector
+        rp, R, C, V = oracle_csr(coo)
+        x = x0.cpu().numpy() / np.linalg.norm(x0.cpu().numpy())
+        lam = []
+        for k in range(E):
+            y, x, l, s = oracle.power_step(n, rp, C, V, x)
+            lam.append(l)
+        s_np = sums.cpu().numpy()
+        lam_gpu = s_np[1:, 1] / np.sqrt(s_np[:-1, 0])
+        assert np.allclose(lam_gpu, lam, rtol=1e-10, atol=0)
+    finally:
+        if comm is not None:
+            comm.close()
+        P.spmv_destroy(h)
