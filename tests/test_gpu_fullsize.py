@@ -1,0 +1,96 @@
+"""Full-size parity at BASELINE.json's configs (c1–c4), in the configuration
+bench.py times (selector + launch tuner decision): CSR and features bit-exact
+against the oracle over the whole matrix; y checked on sampled rows (random
+rows, first/last, the longest rows) whose expected values the oracle computes
+one by one; three native power steps checked the same way."""
+import numpy as np
+import pytest
+
+import oracle
+import spmv_inputs as si
+
+torch = pytest.importorskip("torch")
+P = pytest.importorskip("paper_2302_05662_b200")
+
+pytestmark = pytest.mark.gpu
+TAU = {"f64": 1e-12, "f32": 1e-5}
+
+
+def sub_csr(rp, col, val, rows_sel):
+    """CSR of the selected rows (oracle input); columns stay global."""
+    L = rp[rows_sel + 1] - rp[rows_sel]
+    srp = np.concatenate([[0], np.cumsum(L)]).astype(np.int64)
+    idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows_sel]) if len(rows_sel) else np.zeros(0, np.int64)
+    return srp, col[idx], val[idx]
+
+
+def sample_rows(rp, n, seed=5, k=3000):
+    rng = np.random.default_rng(seed)
+    L = np.diff(rp)
+    pick = set(rng.choice(n, size=min(k, n), replace=False).tolist())
+    pick |= {0, n - 1}
+    pick |= set(np.argsort(L)[-16:].tolist())
+    return np.array(sorted(pick), np.int64)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4"])
+def test_fullsize_selected_format(cfg):
+    coo = si.config_device(cfg)
+    dtype = si.CONFIGS[cfg]["dtype"]
+    dt = coo.val.dtype
+    R = coo.row.cpu().numpy()
+    Cc = coo.col.cpu().numpy()
+    V = coo.val.cpu().numpy().astype(np.float64)
+    n = coo.rows
+    h = P.spmv_create(coo.rows, coo.cols, coo.row, coo.col, coo.val)
+    try:
+        # a2: CSR row pointers bit-exact over the whole matrix
+        rp = oracle.csr(n, R)
+        info = P.spmv_format_info(h, P.FMT_CSR)
+        rpd = np.empty(n + 1, np.int64 if info["row_ptr_is64"] else np.int32)
+        P.spmv_copy_array(h, P.ARR_CSR_ROW_PTR, rpd)
+        assert (rpd.astype(np.int64) == rp).all()
+        # a3: features bit-exact
+        st, fo = oracle.features(n, coo.cols, rp, Cc)
+        fd = P.spmv_features(h)
+        for k, v in fo.items():
+            same = np.float64(fd[k]).tobytes() == np.float64(v).tobytes() if isinstance(v, float) else fd[k] == v
+            assert same, (k, fd[k], v)
+        # a6/a7: the configuration bench.py replays
+        rep = P.spmv_tune(h, P.TUNE_ALL, expected_iterations=100)
+        fmt = rep.format
+        # a5: y on sampled rows
+        x = si.vector_device(coo.cols, dtype=dt)
+        yin = si.vector_device(n, seed=si.Y_SEED, dtype=dt)
+        y = yin.clone()
+        P.spmv_run(h, 2.5, x, -0.5, y)
+        torch.cuda.synchronize()
+        rows_sel = sample_rows(rp, n)
+        srp, sc, sv = sub_csr(rp, Cc, V, rows_sel)
+        xh = x.cpu().numpy().astype(np.float64)
+        yinh = yin.cpu().numpy().astype(np.float64)[rows_sel]
+        y_ref, a_ref = oracle.spmv_csr(len(rows_sel), srp, sc, sv, xh, 2.5, -0.5, yinh)
+        yg = y.cpu().numpy().astype(np.float64)[rows_sel]
+        ok, worst, bad = oracle.parity_check(yg, y_ref, a_ref, 2.5, -0.5, yinh, TAU[dtype])
+        assert ok, (cfg, P.FORMAT_NAMES[fmt], worst, rows_sel[bad[:5]])
+        # a8: three native power steps, each checked against the oracle fed the GPU's own x_k
+        if coo.rows == coo.cols:
+            from paper_2302_05662_b200.dist import Layout, native_power_iteration
+            E = 3
+            layout = Layout.from_bounds(np.array([0, n]))
+            for steps in range(1, E + 1):
+                bufs = {"cur": torch.zeros(n, dtype=dt, device="cuda"), "nxt": torch.zeros(n, dtype=dt, device="cuda"),
+                        "chunk": torch.zeros(1, dtype=dt, device="cuda"),
+                        "sums": torch.zeros(steps + 1, 2, dtype=torch.float64, device="cuda")}
+                z, sums, _ = native_power_iteration(h, layout, 0, x, bufs, steps)
+                torch.cuda.synchronize()
+                zk = z.cpu().numpy().astype(np.float64)
+                if steps > 1:
+                    prev_sum = sums[steps - 1, 0].item()
+                    xk = zprev / np.sqrt(prev_sum)
+                    y_ref, a_ref = oracle.spmv_csr(len(rows_sel), srp, sc, sv, xk, 1.0, 0.0, None)
+                    ok, worst, bad = oracle.parity_check(zk[rows_sel], y_ref, a_ref, 1.0, 0.0, None, TAU[dtype])
+                    assert ok, (cfg, "power step", steps, worst)
+                zprev = zk
+    finally:
+        P.spmv_destroy(h)
