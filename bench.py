@@ -300,6 +300,7 @@ def run_ours(args):
     coo, n_global = gen_slab(args.config, bounds, rank, layout)
     nnz_local = coo.nnz
     del lengths
+    torch.cuda.empty_cache()
 
     # x0 (global, padded layout), generated on device
     x0g = si.vector_device(n_global, dtype=tdt, device=dev)

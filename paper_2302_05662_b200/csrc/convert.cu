@@ -173,12 +173,24 @@ int64_t read_i64(const int64_t* d, cudaStream_t s) {
   return v;
 }
 
+// Device memory a new layout may use: free memory plus what the library's
+// stream-ordered pool holds but does not use (it is reused before growing).
 void guard_bytes(double bytes, const char* what) {
   size_t fr = 0, tot = 0;
   CK(cudaMemGetInfo(&fr, &tot));
-  if (bytes > 0.9 * (double)fr)
+  double avail = (double)fr;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t reserved = 0, used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+      avail += (double)(reserved - used);
+  }
+  if (bytes > 0.95 * avail)
     fail(SPMV_ERR_INFEASIBLE, std::string(what) + ": padded layout needs " + std::to_string(bytes / 1e9) +
-                                  " GB, more than 90% of free device memory");
+                                  " GB, more than 95% of the device memory available (" +
+                                  std::to_string(avail / 1e9) + " GB)");
 }
 
 struct EventTimer {
