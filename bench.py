@@ -356,10 +356,17 @@ def run_ours(args):
         "sums": torch.zeros(E + 1, 2, dtype=torch.float64, device=dev)}
 
     def power(h, x_start):
-        z, sums, kms = native_power_iteration(h, layout, rank, x_start, bufs, E, comm,
-                                              time_kernels=state.get("time_kernels", False))
+        # N = 1: one event pair around the E back-to-back SpMV launches (no
+        # events between kernels); N > 1: per-kernel events (the loop also
+        # holds the NCCL collectives).
+        timing = state.get("time_kernels", False)
+        z, sums, kms, lms = native_power_iteration(h, layout, rank, x_start, bufs, E, comm,
+                                                   time_kernels=timing and world > 1,
+                                                   time_loop=timing and world == 1)
         if kms:
             state["kms"].extend(kms)
+        if lms is not None and timing:
+            state["kms"].extend([lms / E] * E)
         return z, sums
 
     phases = {} if os.environ.get("BENCH_PHASES") else None
@@ -529,6 +536,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": f"{P.FORMAT_NAMES[fmt]} SpMV (power-step epilogue)",
+                         "kernel_timing": ("CUDA events around the E back-to-back SpMV launches of each step / E "
+                                           "(includes launch gaps)") if world == 1 else "CUDA events per SpMV launch",
                          "alg_bytes_per_launch": int(alg_bytes), "kernel_avg_us": round(k_avg_ms * 1e3, 2),
                          "kernel_share_of_step": round(kernel_share, 4) if kernel_share else None,
                          "peak_source": peak_kind, "frac_of_8TBs": round(achieved / 8000.0, 4)},

@@ -230,11 +230,14 @@ spmv_status_t spmv_norm2(spmv_handle_t h, const void* x, int64_t n, double* sums
  * sums: device double[(steps+1)·2] (row k = [S_k, D_k]); lambda_k =
  * D_k / sqrt(S_{k-1}). buf0/buf1: device, n_full values (n_full = rows for a
  * single rank, world·chunk in the padded multi-GPU layout). kernel_ms: host
- * float[steps] (optional) receives each SpMV launch's CUDA-event time (the
- * call then synchronises). *final_buf (optional) = 0/1: which buffer holds z_E. */
+ * float[steps] (optional) receives each SpMV launch's CUDA-event time (events
+ * between launches: slightly perturbing). loop_ms: host float (optional)
+ * receives the CUDA-event time of the whole E-step loop (unperturbed). Either
+ * timing output makes the call synchronise. *final_buf (optional) = 0/1:
+ * which buffer holds z_E. */
 spmv_status_t spmv_power_iterate(spmv_handle_t h, const void* x0, void* buf0, void* buf1, int64_t n_full,
                                  int64_t steps, double* sums, void* comm, int64_t chunk, void* chunk_buf,
-                                 float* kernel_ms, int* final_buf);
+                                 float* kernel_ms, float* loop_ms, int* final_buf);
 
 /* ---------------------------------------------------------------- introspection */
 spmv_status_t spmv_format_info(spmv_handle_t h, spmv_format_t fmt, spmv_format_info_t* out);

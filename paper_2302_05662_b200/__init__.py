@@ -115,7 +115,7 @@ def lib():
         "spmv_launch_count": ([], ctypes.c_uint64),
         "spmv_trim_pool": ([i32], i32),
         "spmv_power_iterate": ([H, vp, vp, vp, i64, i64, vp, vp, i64, vp, ctypes.POINTER(ctypes.c_float),
-                                ctypes.POINTER(ctypes.c_int)], i32),
+                                ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int)], i32),
         "spmv_dist_unique_id": ([ctypes.c_char_p], i32),
         "spmv_dist_init": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, i32, i32], i32),
         "spmv_dist_destroy": ([vp], i32),
@@ -238,14 +238,16 @@ def spmv_power_step(h, x, y, sums_prev, sums_out, row_offset=0):
 
 
 def spmv_power_iterate(h, x0, buf0, buf1, steps, sums, comm=None, chunk=0, chunk_buf=None,
-                       time_kernels=False):
+                       time_kernels=False, time_loop=False):
     """Native E-step power iteration (see spmv.h). Returns (final_buf_index,
-    per-launch kernel ms list or None)."""
+    per-launch kernel ms list or None, loop ms or None)."""
     km = (ctypes.c_float * max(int(steps), 1))() if time_kernels else None
+    lm = ctypes.c_float(0.0)
     fb = ctypes.c_int(0)
     _check(lib().spmv_power_iterate(h, _ptr(x0), _ptr(buf0), _ptr(buf1), int(buf0.numel()), int(steps),
-                                    _ptr(sums), comm, int(chunk), _ptr(chunk_buf), km, ctypes.byref(fb)), h)
-    return fb.value, (list(km)[:int(steps)] if km is not None else None)
+                                    _ptr(sums), comm, int(chunk), _ptr(chunk_buf), km,
+                                    ctypes.byref(lm) if time_loop else None, ctypes.byref(fb)), h)
+    return fb.value, (list(km)[:int(steps)] if km is not None else None), (lm.value if time_loop else None)
 
 
 def spmv_dist_unique_id() -> bytes:

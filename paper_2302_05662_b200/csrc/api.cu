@@ -82,6 +82,15 @@ int64_t persistent_grid(const void* func, int block, int64_t needed_blocks) {
   return needed_blocks < cap ? needed_blocks : cap;
 }
 
+void set_max_dynamic_smem(const void* func, size_t bytes) {
+  static std::unordered_map<const void*, size_t> done;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = done.find(func);
+  if (it != done.end() && it->second >= bytes) return;
+  CK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done[func] = bytes;
+}
+
 void set_carveout(const void* func, int pct) {
   if (pct < 0) return;
   std::lock_guard<std::mutex> lk(g_mu);
@@ -687,13 +696,13 @@ spmv_status_t spmv_norm2(spmv_handle_t h, const void* x, int64_t n, double* sums
 
 spmv_status_t spmv_power_iterate(spmv_handle_t h, const void* x0, void* buf0, void* buf1, int64_t n_full,
                                  int64_t steps, double* sums, void* comm, int64_t chunk, void* chunk_buf,
-                                 float* kernel_ms, int* final_buf) {
+                                 float* kernel_ms, float* loop_ms, int* final_buf) {
   if (!h || !x0 || !buf0 || !buf1 || !sums || steps < 0 || n_full < h->rows || buf0 == buf1) return SPMV_ERR_INVALID_ARG;
   if (comm && (!chunk_buf || chunk < h->rows)) return SPMV_ERR_INVALID_ARG;
   if (!built(h, h->active)) return SPMV_ERR_NOT_CONVERTED;
   API_TRY
   DeviceGuard g(h->device);
-  power_iterate(h, x0, buf0, buf1, n_full, steps, sums, comm, chunk, chunk_buf, kernel_ms, final_buf);
+  power_iterate(h, x0, buf0, buf1, n_full, steps, sums, comm, chunk, chunk_buf, kernel_ms, loop_ms, final_buf);
   API_CATCH(h)
 }
 

@@ -70,7 +70,8 @@ struct Comm {
 
 // Power iteration loop (declared in handle.cuh).
 void power_iterate(spmv_matrix* h, const void* x0, void* buf0, void* buf1, int64_t n_full, int64_t steps,
-                   double* sums, void* comm_v, int64_t chunk, void* chunk_buf, float* kernel_ms, int* final_buf) {
+                   double* sums, void* comm_v, int64_t chunk, void* chunk_buf, float* kernel_ms, float* loop_ms,
+                   int* final_buf) {
   cudaStream_t s = h->stream;
   Comm* comm = static_cast<Comm*>(comm_v);
   const int vb = h->vbytes;
@@ -85,6 +86,12 @@ void power_iterate(spmv_matrix* h, const void* x0, void* buf0, void* buf1, int64
     ev.resize(2 * (size_t)steps);
     for (auto& e : ev) CK(cudaEventCreate(&e));
   }
+  cudaEvent_t l0 = nullptr, l1 = nullptr;
+  if (loop_ms) {
+    CK(cudaEventCreate(&l0));
+    CK(cudaEventCreate(&l1));
+    CK(cudaEventRecord(l0, s));
+  }
   void* cur = buf0;
   void* nxt = buf1;
   for (int64_t k = 0; k < steps; ++k) {
@@ -98,6 +105,13 @@ void power_iterate(spmv_matrix* h, const void* x0, void* buf0, void* buf1, int64
       nccl_check(nccl().AllGather(chunk_buf, nxt, (size_t)chunk, dtype, comm->c, s), "ncclAllGather");
     }
     std::swap(cur, nxt);
+  }
+  if (loop_ms) {
+    CK(cudaEventRecord(l1, s));
+    CK(cudaEventSynchronize(l1));
+    CK(cudaEventElapsedTime(loop_ms, l0, l1));
+    cudaEventDestroy(l0);
+    cudaEventDestroy(l1);
   }
   if (final_buf) *final_buf = (cur == buf0) ? 0 : 1;
   if (kernel_ms) {

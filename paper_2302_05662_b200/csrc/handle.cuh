@@ -119,7 +119,8 @@ void power_step_internal(spmv_matrix* h, const void* x, void* y, const double* s
                          int64_t row_offset);
 void spmv_norm2_internal(spmv_matrix* h, const void* x, int64_t n, double* sums_out);
 void power_iterate(spmv_matrix* h, const void* x0, void* buf0, void* buf1, int64_t n_full, int64_t steps,
-                   double* sums, void* comm, int64_t chunk, void* chunk_buf, float* kernel_ms, int* final_buf);
+                   double* sums, void* comm, int64_t chunk, void* chunk_buf, float* kernel_ms, float* loop_ms,
+                   int* final_buf);
 void* dist_init(const uint8_t id[128], int rank, int world, int device);
 void dist_unique_id(uint8_t out[128]);
 void dist_destroy(void* comm);
@@ -132,6 +133,8 @@ void* ensure_seg_scratch(spmv_matrix* h, size_t bytes);
 spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t& L);
 // Grid for a persistent (grid-stride) kernel: min(needed, SMs × resident blocks per SM).
 int64_t persistent_grid(const void* func, int block, int64_t needed_blocks);
+// Opt in to `bytes` of dynamic shared memory for func (cached).
+void set_max_dynamic_smem(const void* func, size_t bytes);
 // Carveout attribute (cached per function pointer).
 void set_carveout(const void* func, int pct);
 

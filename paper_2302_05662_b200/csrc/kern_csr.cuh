@@ -106,78 +106,124 @@ __device__ __forceinline__ void merge_search(const RP* rp, int64_t rows, int64_t
   yk = d - lo;
 }
 
+// Merge-path CSR (Merrill & Garland). A warp owns a chunk of 32·IPT items of
+// the merged (row ends, nnz indices) sequence; its start/end coordinates come
+// from the partition pre-pass. The warp stages the chunk's row ends and its
+// col/val segment in shared memory with coalesced loads, then each lane
+// consumes IPT items from shared memory. Rows crossing lanes are combined by
+// a warp segmented scan; rows crossing chunks go through chunk records and
+// k_seg_fixup (deterministic, no float atomics).
 template <int B, int R, class T, int IPT, class RP>
 __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_merge(const CsrParams p) {
+  constexpr int ITEMS = 32 * IPT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t chunk = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
+  if (chunk >= p.nchunks) return;  // whole warp exits together
+  unsigned char* base = smem_raw + (size_t)wib * ((size_t)(ITEMS + 1) * 4 + (size_t)ITEMS * (4 + sizeof(T)) + 16);
+  T* s_val = reinterpret_cast<T*>(base);                                   // ITEMS values (aligned first)
+  int32_t* s_col = reinterpret_cast<int32_t*>(base + (size_t)ITEMS * sizeof(T));
+  int32_t* s_end = s_col + ITEMS;                                           // ITEMS+1 row ends
   const RP* __restrict__ rp = static_cast<const RP*>(p.rp);
   const T* __restrict__ val = static_cast<const T*>(p.val);
   const T* __restrict__ x = static_cast<const T*>(p.x);
   T* __restrict__ y = static_cast<T*>(p.y);
-  const int lane = threadIdx.x & 31;
-  const int64_t chunk = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
-  const int64_t total = p.rows + p.nnz;
-  const int64_t d0 = chunk * 32 * IPT;
-  if (d0 >= total) return;  // whole warp exits together
   const double alpha = epi_alpha(p.e);
-  const int64_t d = d0 + (int64_t)lane * IPT;
-  int64_t xr, yk;
-  merge_search(rp, p.rows, p.nnz, d < total ? d : total, xr, yk);
-  // chunk start coordinate (lane 0's) and whether its first row began earlier
-  const int64_t x0 = __shfl_sync(0xffffffffu, xr, 0);
-  const int64_t y0 = __shfl_sync(0xffffffffu, yk, 0);
+  const int64_t x0 = p.coords[2 * chunk], y0 = p.coords[2 * chunk + 1];
+  const int64_t x1 = p.coords[2 * chunk + 2], y1 = p.coords[2 * chunk + 3];
+  const int nrow = (int)(x1 - x0), nnzc = (int)(y1 - y0);
+  // stage row ends (relative to y0, clamped) and the nnz segment
+  for (int i = lane; i <= nrow; i += 32) {
+    const int64_t r = x0 + i;
+    const int64_t e = r < p.rows ? (int64_t)rp[r + 1] - y0 : (int64_t)ITEMS + 1;
+    s_end[i] = (int32_t)(e > ITEMS + 1 ? ITEMS + 1 : e);
+  }
+  for (int j = lane; j < nnzc; j += 32) {
+    s_col[j] = ld_stream(p.col + y0 + j);
+    s_val[j] = ld_stream(val + y0 + j);
+  }
   const bool cont_in = x0 < p.rows && y0 > (int64_t)rp[x0];
-  const int64_t xs = xr;  // this lane's start row
+  __syncwarp();
+  // this lane's start on the chunk-local merge path (diagonal d)
+  const int d = lane * IPT;
+  int lo = d - nnzc > 0 ? d - nnzc : 0, hi = d < nrow ? d : nrow;
+  while (lo < hi) {
+    const int pivot = (lo + hi) >> 1;
+    if (s_end[pivot] <= d - pivot - 1) lo = pivot + 1;
+    else hi = pivot;
+  }
+  int xr = lo, yk = d - lo;
+  const int total = nrow + nnzc;
+  const int xs = xr;
   double acc = 0.0, first_part = 0.0;
-  int64_t first_row = -1;  // first row completed by this lane
-  int64_t row_end = xr < p.rows ? (int64_t)rp[xr + 1] : 0;
+  int first_row = -1;
+  int row_end = s_end[xr];
 #pragma unroll 4
   for (int i = 0; i < IPT; ++i) {
     if (d + i >= total) break;
     if (yk < row_end) {
-      acc = fma((double)ld_stream(val + yk), (double)ld_x(x + ld_stream(p.col + yk)), acc);
+      acc = fma((double)s_val[yk], (double)ld_x(x + s_col[yk]), acc);
       ++yk;
     } else {
       if (first_row < 0) {
         first_row = xr;
         first_part = acc;
       } else {
-        y[xr] = epi_value<T>(p.e, alpha, acc, y, xr);
+        const int64_t gr = x0 + xr;
+        y[gr] = epi_value<T>(p.e, alpha, acc, y, gr);
       }
       acc = 0.0;
       ++xr;
-      row_end = xr < p.rows ? (int64_t)rp[xr + 1] : 0;
+      row_end = s_end[xr];
     }
   }
   // lane carry-out: (row xr in progress, acc). Warp inclusive segmented scan.
   double s = acc;
-  const int64_t key = xr;
+  const int key = xr;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    double su = __shfl_up_sync(0xffffffffu, s, o);
-    int64_t ku = __shfl_up_sync(0xffffffffu, key, o);
+    const double su = __shfl_up_sync(0xffffffffu, s, o);
+    const int ku = __shfl_up_sync(0xffffffffu, key, o);
     if (lane >= o && ku == key) s += su;
   }
   const double s_prev = __shfl_up_sync(0xffffffffu, s, 1);
-  const int64_t k_prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const int k_prev = __shfl_up_sync(0xffffffffu, key, 1);
   const double carry_in = (lane > 0 && k_prev == xs) ? s_prev : 0.0;
   if (first_row >= 0) {
     const double tot = carry_in + first_part;
-    if (cont_in && first_row == x0) p.recs[chunk].head = tot;
-    else y[first_row] = epi_value<T>(p.e, alpha, tot, y, first_row);
+    const int64_t gr = x0 + first_row;
+    if (cont_in && first_row == 0) p.recs[chunk].head = tot;
+    else y[gr] = epi_value<T>(p.e, alpha, tot, y, gr);
   }
   if (lane == 31) {
     ChunkRec& rec = p.recs[chunk];
     rec.first_row = (int32_t)x0;
     rec.cont_in = cont_in;
-    const bool cont_out = xr < p.rows && yk > (int64_t)rp[xr];
-    rec.last_row = (int32_t)(xr < p.rows ? xr : p.rows - 1);
+    const int64_t gx = x0 + xr;  // == x1 for a full chunk
+    const bool cont_out = gx < p.rows && y0 + yk > (int64_t)rp[gx];
+    rec.last_row = (int32_t)(gx < p.rows ? gx : p.rows - 1);
     rec.cont_out = cont_out;
     if (cont_out) {
       rec.tail = s;
-      if (cont_in && xr == x0) rec.head = s;
+      if (cont_in && xr == 0) rec.head = s;
     }
   }
 }
 
+template <class RP>
+__global__ void k_merge_partition(const RP* __restrict__ rp, int64_t rows, int64_t nnz, int64_t items,
+                                  int64_t nchunks, int64_t* __restrict__ coords) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t total = rows + nnz;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= nchunks; c += stride) {
+    int64_t d = c * items;
+    if (d > total) d = total;
+    int64_t xx, yy;
+    merge_search(rp, rows, nnz, d, xx, yy);
+    coords[2 * c] = xx;
+    coords[2 * c + 1] = yy;
+  }
+}
 
 #define CSRV_ROW(B, L) {&k_csr_vector<B, 32, T, L, RP>, &k_csr_vector<B, 64, T, L, RP>, \
                         &k_csr_vector<B, 128, T, L, RP>, &k_csr_vector<B, 255, T, L, RP>}

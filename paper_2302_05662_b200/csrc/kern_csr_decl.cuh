@@ -16,6 +16,8 @@ struct CsrParams {
   void* y;
   Epilogue e;
   ChunkRec* recs;
+  const int64_t* coords;  // merge-path chunk start coordinates (x, y) pairs, nchunks+1
+  int64_t nchunks;
 };
 
 using CsrFn = void (*)(const CsrParams);
@@ -23,6 +25,14 @@ template <class T, class RP, int LANES>
 CsrFn csr_vector_fn(int bi, int ri);
 template <class T, class RP, int IPT>
 CsrFn csr_merge_fn(int bi, int ri);
+// Dynamic shared memory of a merge-path block of `block` threads.
+template <class T>
+constexpr size_t merge_smem_bytes(int block, int ipt) {
+  return (size_t)(block / 32) * ((size_t)(32 * ipt + 1) * 4 + (size_t)(32 * ipt) * (4 + sizeof(T)) + 16);
+}
+// Merge-path partition pre-pass: coords[2c], coords[2c+1] = start of chunk c.
+void merge_partition(const void* rp, bool rp64, int64_t rows, int64_t nnz, int64_t items_per_chunk,
+                     int64_t nchunks, int64_t* coords, cudaStream_t s);
 
 }  // namespace kern
 }  // namespace spmv

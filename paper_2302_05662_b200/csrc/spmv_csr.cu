@@ -50,15 +50,25 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     default: fail(SPMV_ERR_INVALID_ARG, "merge-path items per thread must be 4, 8 or 16");
   }
   set_carveout(fn, L.carveout_pct);
+  const size_t smem = kern::merge_smem_bytes<T>(L.block, ipt);
+  set_max_dynamic_smem(fn, smem);
   const int64_t total = h->rows + h->nnz;
-  const int64_t nchunks = (total + 32LL * ipt - 1) / (32LL * ipt);
+  const int64_t items = 32LL * ipt;
+  const int64_t nchunks = (total + items - 1) / items;
   if (nchunks <= 0) return;
-  p.recs = static_cast<ChunkRec*>(ensure_seg_scratch(h, (size_t)nchunks * sizeof(ChunkRec)));
+  // chunk records + partition coordinates share the grow-only scratch
+  const size_t rec_bytes = ((size_t)nchunks * sizeof(ChunkRec) + 255) / 256 * 256;
+  char* scratch = static_cast<char*>(ensure_seg_scratch(h, rec_bytes + (size_t)(nchunks + 1) * 2 * sizeof(int64_t)));
+  p.recs = reinterpret_cast<ChunkRec*>(scratch);
+  int64_t* coords = reinterpret_cast<int64_t*>(scratch + rec_bytes);
+  p.coords = coords;
+  p.nchunks = nchunks;
+  kern::merge_partition(h->row_ptr, h->rp64, h->rows, h->nnz, items, nchunks, coords, h->stream);
   // mode 1 (power step): alpha from device, beta = 0; the norms are computed
   // afterwards by run_norms because boundary rows finish in the fixup.
   const int64_t grid = (nchunks * 32 + L.block - 1) / L.block;
   void* args[] = {&p};
-  launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
+  launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, smem, h->stream);
   run_seg_fixup(h, p.recs, nchunks, e, y);
 }
 

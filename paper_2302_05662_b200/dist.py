@@ -160,14 +160,17 @@ class NativeComm:
             self.comm = None
 
 
-def native_power_iteration(h, layout: Layout, rank: int, x0, bufs, steps: int, comm=None, time_kernels=False):
+def native_power_iteration(h, layout: Layout, rank: int, x0, bufs, steps: int, comm=None, time_kernels=False,
+                           time_loop=False):
     """E power steps in one C-ABI call (loop + NCCL exchange in C++).
-    Returns (z_E tensor view, sums, kernel_ms or None)."""
+    Returns (z_E tensor view, sums, kernel_ms or None[, loop_ms])."""
     from . import spmv_power_iterate
     c = comm.comm if comm is not None else None
-    fb, kms = spmv_power_iterate(h, x0, bufs["cur"], bufs["nxt"], steps, bufs["sums"], c, layout.chunk,
-                                 bufs["chunk"] if c is not None else None, time_kernels)
+    fb, kms, lms = spmv_power_iterate(h, x0, bufs["cur"], bufs["nxt"], steps, bufs["sums"], c, layout.chunk,
+                                      bufs["chunk"] if c is not None else None, time_kernels, time_loop)
     z = bufs["cur"] if fb == 0 else bufs["nxt"]
+    if time_loop:
+        return z, bufs["sums"], kms, lms
     return z, bufs["sums"], kms
 
 

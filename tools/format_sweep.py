@@ -59,6 +59,7 @@ def main():
     ap.add_argument("--configs", default="c1,c2,c3,c4")
     ap.add_argument("--out", default="gpurun_out/format_sweep")
     ap.add_argument("--no-tune", action="store_true")
+    ap.add_argument("--formats", default="", help="comma list of variant names (default all)")
     args = ap.parse_args()
     results = []
     for cfg in args.configs.split(","):
@@ -72,6 +73,8 @@ def main():
         del coo
         torch.cuda.empty_cache()
         for name, fmt, params in VARIANTS:
+            if args.formats and name not in args.formats.split(","):
+                continue
             params = dict(params)
             if params.get("sell_sigma") == -1:
                 if feats["std"] <= 0.5 * feats["mean"]:
