@@ -122,6 +122,15 @@ void* ensure_seg_scratch(spmv_matrix* h, size_t bytes) {
   return h->seg_scratch;
 }
 
+void* ensure_fixup_scratch(spmv_matrix* h, size_t bytes) {
+  if (h->fix_scratch && h->fix_scratch_bytes >= bytes) return h->fix_scratch;
+  CK(cudaStreamSynchronize(h->stream));
+  dfree(h->fix_scratch, h->stream);
+  h->fix_scratch = dalloc(bytes, h->stream);
+  h->fix_scratch_bytes = bytes;
+  return h->fix_scratch;
+}
+
 static int csr_default_lanes(const spmv_matrix* h) {
   if (h->csr_T > 0) return h->csr_T;
   double mean = h->rows > 0 ? (double)h->nnz / (double)h->rows : 0.0;
@@ -457,6 +466,7 @@ static void destroy_handle(spmv_matrix* h) {
   cudaSetDevice(h->device);
   for (int f = 0; f < SPMV_NUM_FORMATS; ++f) free_format(h, f);
   dfree(h->seg_scratch, h->stream);
+  dfree(h->fix_scratch, h->stream);
   dfree(h->pi_partials, h->stream);
   dfree(h->pi_counter, h->stream);
   cudaStreamSynchronize(h->stream);

@@ -97,46 +97,46 @@ constexpr int kNumSMs = 148;
 // in L1 and mark evict-first in L2 (x stays resident instead).
 __device__ __forceinline__ int ld_stream(const int* p) {
   int r;
-  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
 }
 __device__ __forceinline__ int2 ld_stream(const int2* p) {
   int2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0,%1}, [%2];"
+  asm("ld.global.nc.L1::no_allocate.v2.b32 {%0,%1}, [%2];"
                : "=r"(r.x), "=r"(r.y) : "l"(p));
   return r;
 }
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+  asm("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
 __device__ __forceinline__ float ld_stream(const float* p) {
   float r;
-  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
   return r;
 }
 __device__ __forceinline__ double ld_stream(const double* p) {
   double r;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
   return r;
 }
 __device__ __forceinline__ float2 ld_stream(const float2* p) {
   float2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];"
+  asm("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];"
                : "=f"(r.x), "=f"(r.y) : "l"(p));
   return r;
 }
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
   return r;
 }
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
   double2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
                : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
@@ -145,12 +145,12 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
 // every row that touches the column).
 __device__ __forceinline__ double ld_x(const double* p) {
   double r;
-  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  asm("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
   return r;
 }
 __device__ __forceinline__ float ld_x(const float* p) {
   float r;
-  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  asm("ld.global.nc.f32 %0, [%1];" : "=f"(r) : "l"(p));
   return r;
 }
 

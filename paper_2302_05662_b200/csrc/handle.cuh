@@ -65,6 +65,8 @@ struct spmv_matrix {
   // power-step block partials.
   void* seg_scratch = nullptr;
   size_t seg_scratch_bytes = 0;
+  void* fix_scratch = nullptr;
+  size_t fix_scratch_bytes = 0;
   double* pi_partials = nullptr;
   unsigned* pi_counter = nullptr;
   size_t pi_partials_n = 0;
@@ -128,6 +130,7 @@ void dist_destroy(void* comm);
 // Make sure the power-step partial buffers hold >= nblocks entries.
 void ensure_pi_scratch(spmv_matrix* h, size_t nblocks);
 void* ensure_seg_scratch(spmv_matrix* h, size_t bytes);
+void* ensure_fixup_scratch(spmv_matrix* h, size_t bytes);
 
 // Resolve a launch variant to the defaults of its kernel.
 spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t& L);

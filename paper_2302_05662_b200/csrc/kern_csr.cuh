@@ -108,9 +108,10 @@ __device__ __forceinline__ void merge_search(const RP* rp, int64_t rows, int64_t
 
 // Merge-path CSR (Merrill & Garland). A warp owns a chunk of 32·IPT items of
 // the merged (row ends, nnz indices) sequence; its start/end coordinates come
-// from the partition pre-pass. The warp stages the chunk's row ends and its
-// col/val segment in shared memory with coalesced loads, then each lane
-// consumes IPT items from shared memory. Rows crossing lanes are combined by
+// from the partition pre-pass. The warp stages the chunk's row ends in shared
+// memory and computes the chunk's products a·x cooperatively (consecutive
+// lanes, coalesced col/val loads, independent x gathers), then each lane
+// walks IPT items of the merge path summing staged products. Rows crossing lanes are combined by
 // a warp segmented scan; rows crossing chunks go through chunk records and
 // k_seg_fixup (deterministic, no float atomics).
 template <int B, int R, class T, int IPT, class RP>
@@ -120,10 +121,9 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_merge(const
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t chunk = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
   if (chunk >= p.nchunks) return;  // whole warp exits together
-  unsigned char* base = smem_raw + (size_t)wib * ((size_t)(ITEMS + 1) * 4 + (size_t)ITEMS * (4 + sizeof(T)) + 16);
-  T* s_val = reinterpret_cast<T*>(base);                                   // ITEMS values (aligned first)
-  int32_t* s_col = reinterpret_cast<int32_t*>(base + (size_t)ITEMS * sizeof(T));
-  int32_t* s_end = s_col + ITEMS;                                           // ITEMS+1 row ends
+  unsigned char* base = smem_raw + (size_t)wib * merge_warp_smem(IPT);
+  double* s_prod = reinterpret_cast<double*>(base);                         // ITEMS products a·x (fp64)
+  int32_t* s_end = reinterpret_cast<int32_t*>(base + (size_t)ITEMS * 8);    // ITEMS+1 row ends
   const RP* __restrict__ rp = static_cast<const RP*>(p.rp);
   const T* __restrict__ val = static_cast<const T*>(p.val);
   const T* __restrict__ x = static_cast<const T*>(p.x);
@@ -132,15 +132,36 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_merge(const
   const int64_t x0 = p.coords[2 * chunk], y0 = p.coords[2 * chunk + 1];
   const int64_t x1 = p.coords[2 * chunk + 2], y1 = p.coords[2 * chunk + 3];
   const int nrow = (int)(x1 - x0), nnzc = (int)(y1 - y0);
-  // stage row ends (relative to y0, clamped) and the nnz segment
-  for (int i = lane; i <= nrow; i += 32) {
-    const int64_t r = x0 + i;
-    const int64_t e = r < p.rows ? (int64_t)rp[r + 1] - y0 : (int64_t)ITEMS + 1;
-    s_end[i] = (int32_t)(e > ITEMS + 1 ? ITEMS + 1 : e);
+  // stage row ends (relative to y0, clamped) and the chunk's products; the
+  // trip counts are bounded by IPT(+1), so both loops are fully unrolled and
+  // every lane has IPT column loads, then IPT x gathers, in flight together.
+#pragma unroll
+  for (int q = 0; q <= IPT; ++q) {
+    const int i = lane + 32 * q;
+    if (i <= nrow) {
+      const int64_t r = x0 + i;
+      const int64_t e = r < p.rows ? (int64_t)rp[r + 1] - y0 : (int64_t)ITEMS + 1;
+      s_end[i] = (int32_t)(e > ITEMS + 1 ? ITEMS + 1 : e);
+    }
   }
-  for (int j = lane; j < nnzc; j += 32) {
-    s_col[j] = ld_stream(p.col + y0 + j);
-    s_val[j] = ld_stream(val + y0 + j);
+  {
+    int c[IPT];
+    T v[IPT];
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      const int j = lane + 32 * q;
+      const bool ok = j < nnzc;
+      c[q] = ok ? ld_stream(p.col + y0 + j) : -1;
+      v[q] = ok ? ld_stream(val + y0 + j) : T(0);
+    }
+    T xv[IPT];
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) xv[q] = c[q] >= 0 ? ld_x(x + c[q]) : T(0);
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      const int j = lane + 32 * q;
+      if (j < nnzc) s_prod[j] = (double)v[q] * (double)xv[q];
+    }
   }
   const bool cont_in = x0 < p.rows && y0 > (int64_t)rp[x0];
   __syncwarp();
@@ -162,7 +183,7 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_merge(const
   for (int i = 0; i < IPT; ++i) {
     if (d + i >= total) break;
     if (yk < row_end) {
-      acc = fma((double)s_val[yk], (double)ld_x(x + s_col[yk]), acc);
+      acc += s_prod[yk];
       ++yk;
     } else {
       if (first_row < 0) {

@@ -26,9 +26,13 @@ CsrFn csr_vector_fn(int bi, int ri);
 template <class T, class RP, int IPT>
 CsrFn csr_merge_fn(int bi, int ri);
 // Dynamic shared memory of a merge-path block of `block` threads.
+// Per-warp slice: ITEMS fp64 products then ITEMS+1 int32 row ends, padded to 16 B.
+__host__ __device__ constexpr size_t merge_warp_smem(int ipt) {
+  return (((size_t)(32 * ipt) * 8 + (size_t)(32 * ipt + 1) * 4) + 15) / 16 * 16;
+}
 template <class T>
 constexpr size_t merge_smem_bytes(int block, int ipt) {
-  return (size_t)(block / 32) * ((size_t)(32 * ipt + 1) * 4 + (size_t)(32 * ipt) * (4 + sizeof(T)) + 16);
+  return (size_t)(block / 32) * merge_warp_smem(ipt);
 }
 // Merge-path partition pre-pass: coords[2c], coords[2c+1] = start of chunk c.
 void merge_partition(const void* rp, bool rp64, int64_t rows, int64_t nnz, int64_t items_per_chunk,

@@ -12,23 +12,68 @@
 
 namespace spmv {
 namespace {
-// Rows crossing chunk boundaries: the chunk where the row starts (cont_out
-// and not a single-row continuation chunk) walks forward adding heads.
+// Rows crossing chunk boundaries: the chunk where such a row starts (cont_out
+// and not a single-row continuation chunk) owns it.
+//  k_seg_fixup: thread per chunk; a row that ends in the next chunk (the usual
+//    case) is finished directly; longer runs are appended to a list.
+//  k_seg_fixup_long: one warp per listed run reads the following chunk records
+//    32 at a time, finds where the row ends (ballot) and sums the heads with a
+//    fixed-shape reduction — a 150K-entry row spanning hundreds of chunks costs
+//    a few warp steps. Both orders are fixed by the data: deterministic.
+__device__ __forceinline__ bool rec_mid(const ChunkRec& r) {
+  return r.cont_out && r.cont_in && r.first_row == r.last_row;
+}
+
 template <class T>
-__global__ void k_seg_fixup(const ChunkRec* __restrict__ recs, int64_t n, Epilogue e, T* __restrict__ y) {
+__global__ void k_seg_fixup(const ChunkRec* __restrict__ recs, int64_t n, Epilogue e, T* __restrict__ y,
+                            int64_t* __restrict__ longs, unsigned long long* __restrict__ nlong) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const double alpha = epi_alpha(e);
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride) {
     const ChunkRec rc = recs[c];
-    if (!rc.cont_out || (rc.cont_in && rc.first_row == rc.last_row)) continue;
-    const int r = rc.last_row;
-    double sum = rc.tail;
-    for (int64_t q = c + 1; q < n; ++q) {
-      const ChunkRec rq = recs[q];
-      sum += rq.head;
-      if (!(rq.cont_out && rq.cont_in && rq.first_row == rq.last_row)) break;
+    if (!rc.cont_out || rec_mid(rc) || c + 1 >= n) continue;
+    const ChunkRec rn = recs[c + 1];
+    if (rec_mid(rn)) {
+      longs[atomicAdd(nlong, 1ull)] = c;
+      continue;
     }
-    y[r] = epi_value<T>(e, alpha, sum, y, r);
+    const int r = rc.last_row;
+    y[r] = epi_value<T>(e, alpha, rc.tail + rn.head, y, r);
+  }
+}
+
+template <class T>
+__global__ void k_seg_fixup_long(const ChunkRec* __restrict__ recs, int64_t n, Epilogue e, T* __restrict__ y,
+                                 const int64_t* __restrict__ longs, const unsigned long long* __restrict__ nlong) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t count = (int64_t)*nlong;
+  const double alpha = epi_alpha(e);
+  for (int64_t w = warp0; w < count; w += nwarps) {
+    const int64_t c = longs[w];
+    const ChunkRec rc = recs[c];
+    double part = 0.0;
+    for (int64_t q0 = c + 1; q0 < n; q0 += 32) {
+      const int64_t q = q0 + lane;
+      const bool valid = q < n;
+      double hd = 0.0;
+      bool mid = false;
+      if (valid) {
+        const ChunkRec rq = recs[q];
+        hd = rq.head;
+        mid = rec_mid(rq);
+      }
+      const unsigned endm = __ballot_sync(0xffffffffu, valid && !mid);
+      const int last = endm ? __ffs(endm) - 1 : 31;
+      if (valid && lane <= last) part += hd;
+      if (endm || !__ballot_sync(0xffffffffu, valid)) break;
+    }
+    part = warp_sum(part);
+    if (lane == 0) {
+      const int r = rc.last_row;
+      y[r] = epi_value<T>(e, alpha, rc.tail + part, y, r);
+    }
   }
 }
 
@@ -96,9 +141,23 @@ void coo_launch(spmv_matrix* h, const int32_t* row, const int32_t* col, const vo
 
 void run_seg_fixup(spmv_matrix* h, const ChunkRec* recs, int64_t nchunks, const Epilogue& e, void* y) {
   if (nchunks <= 1) return;
+  // scratch for the long-run list lives after the records (same grow-only buffer)
+  const size_t rec_bytes = ((size_t)nchunks * sizeof(ChunkRec) + 255) / 256 * 256;
+  (void)rec_bytes;
+  int64_t* longs = static_cast<int64_t*>(ensure_fixup_scratch(h, (size_t)nchunks * sizeof(int64_t) + 256));
+  unsigned long long* nlong = reinterpret_cast<unsigned long long*>(longs + nchunks);
+  CK(cudaMemsetAsync(nlong, 0, sizeof(unsigned long long), h->stream));
   const unsigned g = grid_for(nchunks, 256);
-  if (h->dtype == SPMV_R64F) LAUNCH(k_seg_fixup<double>, g, 256, 0, h->stream, recs, nchunks, e, (double*)y);
-  else LAUNCH(k_seg_fixup<float>, g, 256, 0, h->stream, recs, nchunks, e, (float*)y);
+  const unsigned gl = (unsigned)(kNumSMs * 8);
+  if (h->dtype == SPMV_R64F) {
+    LAUNCH(k_seg_fixup<double>, g, 256, 0, h->stream, recs, nchunks, e, (double*)y, longs, nlong);
+    LAUNCH(k_seg_fixup_long<double>, gl, 256, 0, h->stream, recs, nchunks, e, (double*)y, (const int64_t*)longs,
+           (const unsigned long long*)nlong);
+  } else {
+    LAUNCH(k_seg_fixup<float>, g, 256, 0, h->stream, recs, nchunks, e, (float*)y, longs, nlong);
+    LAUNCH(k_seg_fixup_long<float>, gl, 256, 0, h->stream, recs, nchunks, e, (float*)y, (const int64_t*)longs,
+           (const unsigned long long*)nlong);
+  }
 }
 
 void run_rows_scale(spmv_matrix* h, const int32_t* rows_list, int64_t n, const Epilogue& e, void* y) {
