@@ -360,9 +360,10 @@ def run_ours(args):
         # events between kernels); N > 1: per-kernel events (the loop also
         # holds the NCCL collectives).
         timing = state.get("time_kernels", False)
-        z, sums, kms, lms = native_power_iteration(h, layout, rank, x_start, bufs, E, comm,
-                                                   time_kernels=timing and world > 1,
-                                                   time_loop=timing and world == 1)
+        res = native_power_iteration(h, layout, rank, x_start, bufs, E, comm,
+                                     time_kernels=timing and world > 1, time_loop=timing and world == 1)
+        z, sums, kms = res[:3]
+        lms = res[3] if len(res) > 3 else None
         if kms:
             state["kms"].extend(kms)
         if lms is not None and timing:

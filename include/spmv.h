@@ -170,7 +170,11 @@ spmv_status_t spmv_create(spmv_handle_t* out, int64_t rows, int64_t cols, int64_
                           spmv_dtype_t dtype, spmv_mem_t where, int device, void* cuda_stream);
 
 /* Build (or re-activate, if cached) `fmt` on the device and make it the
- * active format (§8(a) row a4). p = NULL uses defaults. Synchronous.
+ * active format (§8(a) row a4). p = NULL uses defaults. Stream-ordered: the
+ * build is enqueued on the handle's stream (later calls on the handle see
+ * it); it synchronises only when a host decision needs a device-computed size
+ * (HYB tail, COO empty rows, strongly skewed SELL). Its device time is
+ * reported by spmv_overheads.
  * INFEASIBLE if ELL/SELL/HYB padding would not fit the device-memory guard
  * (the handle is unchanged); UNSUPPORTED for SELL C outside {32,64,128,256}. */
 spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format_params_t* p);

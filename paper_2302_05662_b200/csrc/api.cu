@@ -357,8 +357,9 @@ static void tune_launch(spmv_matrix* h, int fmt, TuneScratch& ts, spmv_tune_repo
   }
 }
 
-static double sell_padding(const spmv_matrix* h) {
-  return h->sell_slots > 0 ? 1.0 - (double)h->nnz / (double)h->sell_slots : 0.0;
+static double sell_padding(spmv_matrix* h) {
+  const int64_t sl = sell_slots(h);
+  return sl > 0 ? 1.0 - (double)h->nnz / (double)sl : 0.0;
 }
 
 // Run-time mode analog: features -> candidates -> measure -> gate.
@@ -412,7 +413,7 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
       return;
     }
     double t = time_variant(h, fmt, resolve_launch(h, fmt, h->launch[fmt]), ts.x, ts.y);
-    cands.push_back({fmt, 0, t, h->c_latency[fmt], why});
+    cands.push_back({fmt, 0, t, format_latency(h, fmt), why});
   };
   if (f.ell_ratio >= 0.9) try_build(SPMV_FMT_ELL, "ell_ratio>=0.9");
   if (f.ell_ratio >= 0.5 || !skewed) try_build(SPMV_FMT_SELL, "sell padding<=10%");
@@ -468,8 +469,10 @@ static void destroy_handle(spmv_matrix* h) {
   dfree(h->seg_scratch, h->stream);
   dfree(h->fix_scratch, h->stream);
   dfree(h->pi_partials, h->stream);
-  dfree(h->pi_counter, h->stream);
-  cudaStreamSynchronize(h->stream);
+  dfree(h->pi_counter, h->stream);  // stream-ordered frees: no host synchronisation
+  for (auto& evs : h->lat_ev)
+    for (auto& ev : evs)
+      if (ev) cudaEventDestroy(ev);
   delete h;
 }
 
@@ -598,8 +601,7 @@ spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format
       break;
     }
   }
-  h->active = fmt;
-  CK(cudaStreamSynchronize(h->stream));
+  h->active = fmt;  // builds are stream-ordered: no synchronisation here
   API_CATCH(h)
 }
 
@@ -745,7 +747,13 @@ spmv_status_t spmv_format_info(spmv_handle_t h, spmv_format_t fmt, spmv_format_i
   switch (fmt) {
     case SPMV_FMT_ELL: o->K = h->ell_K; o->n_pad = h->ell_npad; o->slots = h->ell_K * h->ell_npad; break;
     case SPMV_FMT_SELL:
-      o->C = h->sell_C; o->sigma = h->sell_sigma; o->n_slices = h->sell_ns; o->slots = h->sell_slots;
+      o->C = h->sell_C; o->sigma = h->sell_sigma; o->n_slices = h->sell_ns;
+      try {
+        o->slots = h->sell_built ? sell_slots(h) : 0;
+      } catch (const SpmvError& e) {
+        h->last_error = e.msg;
+        return e.status;
+      }
       break;
     case SPMV_FMT_HYB:
       o->K = h->hyb_K; o->n_pad = h->hyb_npad; o->slots = h->hyb_K * h->hyb_npad; o->tail_nnz = h->hyb_tail;
@@ -773,8 +781,8 @@ spmv_status_t spmv_copy_array(spmv_handle_t h, spmv_array_t which, void* dst, in
     case SPMV_ARR_ELL_VAL: need = h->ell_built; src = h->ell_val; bytes = h->ell_K * h->ell_npad * vb; break;
     case SPMV_ARR_SELL_PERM: need = h->sell_built; src = h->sell_perm; bytes = h->rows * 4; break;
     case SPMV_ARR_SELL_SLICE_PTR: need = h->sell_built; src = h->sell_sp; bytes = (h->sell_ns + 1) * 8; break;
-    case SPMV_ARR_SELL_COL: need = h->sell_built; src = h->sell_col; bytes = h->sell_slots * 4; break;
-    case SPMV_ARR_SELL_VAL: need = h->sell_built; src = h->sell_val; bytes = h->sell_slots * vb; break;
+    case SPMV_ARR_SELL_COL: need = h->sell_built; src = h->sell_col; bytes = (h->sell_built ? sell_slots(h) : 0) * 4; break;
+    case SPMV_ARR_SELL_VAL: need = h->sell_built; src = h->sell_val; bytes = (h->sell_built ? sell_slots(h) : 0) * vb; break;
     case SPMV_ARR_HYB_ELL_COL: need = h->hyb_built; src = h->hyb_ecol; bytes = h->hyb_K * h->hyb_npad * 4; break;
     case SPMV_ARR_HYB_ELL_VAL: need = h->hyb_built; src = h->hyb_eval; bytes = h->hyb_K * h->hyb_npad * vb; break;
     case SPMV_ARR_HYB_TAIL_ROW: need = h->hyb_built; src = h->hyb_trow; bytes = h->hyb_tail * 4; break;
@@ -848,9 +856,10 @@ size_t spmv_decision_log(spmv_handle_t h, char* buf, size_t len) {
 spmv_status_t spmv_overheads(spmv_handle_t h, double* f_latency_s, double* c_latency_s) {
   if (!h) return SPMV_ERR_INVALID_ARG;
   if (f_latency_s) *f_latency_s = h->f_latency;
+  API_TRY
   if (c_latency_s)
-    for (int i = 0; i < SPMV_NUM_FORMATS; ++i) c_latency_s[i] = h->c_latency[i];
-  return SPMV_OK;
+    for (int i = 0; i < SPMV_NUM_FORMATS; ++i) c_latency_s[i] = format_latency(h, i);
+  API_CATCH(h)
 }
 
 uint64_t spmv_launch_count(void) { return g_launches.load(); }

@@ -173,59 +173,52 @@ int64_t read_i64(const int64_t* d, cudaStream_t s) {
   return v;
 }
 
-// Device memory a new layout may use: free memory plus what the library's
-// stream-ordered pool holds but does not use (it is reused before growing).
+// Device memory a new layout may use: what the library's stream-ordered pool
+// holds unused (reused before it grows) plus, only if that is not enough, the
+// device's free memory (cudaMemGetInfo is comparatively slow).
 void guard_bytes(double bytes, const char* what) {
-  size_t fr = 0, tot = 0;
-  CK(cudaMemGetInfo(&fr, &tot));
-  double avail = (double)fr;
+  double avail = 0.0;
   int dev = 0;
   cudaMemPool_t pool;
   if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t reserved = 0, used = 0;
     if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
-      avail += (double)(reserved - used);
+      avail = (double)(reserved - used);
   }
+  if (bytes <= avail) return;
+  size_t fr = 0, tot = 0;
+  CK(cudaMemGetInfo(&fr, &tot));
+  avail += (double)fr;
   if (bytes > 0.95 * avail)
     fail(SPMV_ERR_INFEASIBLE, std::string(what) + ": padded layout needs " + std::to_string(bytes / 1e9) +
                                   " GB, more than 95% of the device memory available (" +
                                   std::to_string(avail / 1e9) + " GB)");
 }
 
-struct EventTimer {
-  cudaEvent_t a, b;
-  cudaStream_t s;
-  explicit EventTimer(cudaStream_t st) : s(st) {
-    CK(cudaEventCreate(&a));
-    CK(cudaEventCreate(&b));
-    CK(cudaEventRecord(a, s));
-  }
-  double stop() {
-    CK(cudaEventRecord(b, s));
-    CK(cudaEventSynchronize(b));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, a, b));
-    return ms * 1e-3;
-  }
-  ~EventTimer() {
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-  }
-};
+void lat_begin(spmv_matrix* h, int fmt) {
+  for (int i = 0; i < 2; ++i)
+    if (!h->lat_ev[fmt][i]) CK(cudaEventCreate(&h->lat_ev[fmt][i]));
+  CK(cudaEventRecord(h->lat_ev[fmt][0], h->stream));
+}
+
+void lat_end(spmv_matrix* h, int fmt) {
+  CK(cudaEventRecord(h->lat_ev[fmt][1], h->stream));
+  h->lat_pending[fmt] = true;
+}
 
 template <class RP, class V>
 void ell_typed(spmv_matrix* h) {
   cudaStream_t s = h->stream;
   const int64_t K = h->feat.max_len, n_pad = (h->rows + 127) / 128 * 128;
   guard_bytes((double)K * n_pad * (4.0 + sizeof(V)), "ELL");
-  EventTimer tm(s);
+  lat_begin(h, SPMV_FMT_ELL);
   Scratch sc(s);
   int32_t* colE = sc.get<int32_t>(K * n_pad);
   V* valE = sc.get<V>(K * n_pad);
   LAUNCH((k_ell_fill<RP, V>), grid_for(n_pad, 256), 256, 0, s, static_cast<const RP*>(h->row_ptr), h->col,
          static_cast<const V*>(h->val), h->rows, K, n_pad, colE, valE);
-  h->c_latency[SPMV_FMT_ELL] = tm.stop();
+  lat_end(h, SPMV_FMT_ELL);
   sc.keep(colE);
   sc.keep(valE);
   h->ell_K = K;
@@ -239,7 +232,7 @@ template <class RP, class V>
 void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma) {
   cudaStream_t s = h->stream;
   const int64_t rows = h->rows, ns = (rows + C - 1) / C;
-  EventTimer tm(s);
+  lat_begin(h, SPMV_FMT_SELL);
   Scratch sc(s);
   const RP* rp = static_cast<const RP*>(h->row_ptr);
   int32_t* perm = nullptr;
@@ -259,19 +252,24 @@ void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma) {
   int64_t* sp = sc.get<int64_t>(ns + 1);
   LAUNCH(k_sell_widths<RP>, grid_for(ns, 256), 256, 0, s, rp, (const int32_t*)perm, rows, C, ns, cw);
   exclusive_scan_i64(cw, sp, ns, s);
-  const int64_t slots = read_i64(sp + ns, s);
+  // Near-regular matrices: allocate the upper bound ns·C·max_len (no host
+  // round trip); the exact slot count stays on the device until asked for.
+  const int64_t ub = ns * C * h->feat.max_len;
+  const bool use_ub = (double)ub <= 1.25 * (double)h->nnz + (double)(64 << 20) / (4.0 + sizeof(V));
+  const int64_t slots = use_ub ? ub : read_i64(sp + ns, s);
   guard_bytes((double)slots * (4.0 + sizeof(V)), "SELL");
   int32_t* colS = sc.get<int32_t>(slots);
   V* valS = sc.get<V>(slots);
   LAUNCH((k_sell_fill<RP, V>), grid_for(ns * C, 256), 256, 0, s, rp, h->col, static_cast<const V*>(h->val),
          (const int32_t*)perm, rows, C, ns, (const int64_t*)sp, colS, valS);
-  h->c_latency[SPMV_FMT_SELL] = tm.stop();
+  lat_end(h, SPMV_FMT_SELL);
   for (void* p : {(void*)perm, (void*)sp, (void*)colS, (void*)valS})
     if (p) sc.keep(p);
   h->sell_C = C;
   h->sell_sigma = sigma;
   h->sell_ns = ns;
   h->sell_slots = slots;
+  h->sell_slots_pending = use_ub;
   h->sell_perm = perm;
   h->sell_sp = sp;
   h->sell_col = colS;
@@ -284,7 +282,7 @@ void hyb_typed(spmv_matrix* h, int64_t K) {
   cudaStream_t s = h->stream;
   const int64_t rows = h->rows, n_pad = (rows + 127) / 128 * 128;
   guard_bytes((double)K * n_pad * (4.0 + sizeof(V)), "HYB");
-  EventTimer tm(s);
+  lat_begin(h, SPMV_FMT_HYB);
   Scratch sc(s);
   const RP* rp = static_cast<const RP*>(h->row_ptr);
   int32_t* colE = sc.get<int32_t>(K * n_pad);
@@ -302,7 +300,7 @@ void hyb_typed(spmv_matrix* h, int64_t K) {
   if (h->nnz > 0 && tail > 0)
     LAUNCH((k_expand<RP, V>), (unsigned)((h->nnz + kExpandTile - 1) / kExpandTile), kExpandThreads, 0, s, rp,
            h->col, static_cast<const V*>(h->val), rows, h->nnz, 1, K, (const int64_t*)toff, trow, tcol, tval);
-  h->c_latency[SPMV_FMT_HYB] = tm.stop();
+  lat_end(h, SPMV_FMT_HYB);
   for (void* p : {(void*)colE, (void*)valE, (void*)trow, (void*)tcol, (void*)tval}) sc.keep(p);
   h->hyb_K = K;
   h->hyb_npad = n_pad;
@@ -319,7 +317,7 @@ template <class RP, class V>
 void coo_typed(spmv_matrix* h) {
   cudaStream_t s = h->stream;
   const int64_t rows = h->rows;
-  EventTimer tm(s);
+  lat_begin(h, SPMV_FMT_COO);
   Scratch sc(s);
   const RP* rp = static_cast<const RP*>(h->row_ptr);
   int32_t* crow = sc.get<int32_t>(h->nnz);
@@ -335,7 +333,7 @@ void coo_typed(spmv_matrix* h) {
   int32_t* empty = sc.get<int32_t>(n_empty);
   if (n_empty > 0)
     LAUNCH(k_compact_empty<RP>, grid_for(rows, 256), 256, 0, s, rp, (const int64_t*)off, rows, empty);
-  h->c_latency[SPMV_FMT_COO] = tm.stop();
+  lat_end(h, SPMV_FMT_COO);
   sc.keep(crow);
   sc.keep(empty);
   h->coo_row = crow;
@@ -411,6 +409,7 @@ void free_format(spmv_matrix* h, int fmt) {
     case SPMV_FMT_SELL:
       F(h->sell_perm); F(h->sell_sp); F(h->sell_col); F(h->sell_val);
       h->sell_built = false;
+      h->sell_slots_pending = false;
       break;
     case SPMV_FMT_HYB:
       F(h->hyb_ecol); F(h->hyb_eval); F(h->hyb_trow); F(h->hyb_tcol); F(h->hyb_tval);
@@ -422,14 +421,36 @@ void free_format(spmv_matrix* h, int fmt) {
   }
 }
 
-int64_t format_stored_bytes(const spmv_matrix* h, int fmt) {
+double format_latency(spmv_matrix* h, int fmt) {
+  if (h->lat_pending[fmt]) {
+    CK(cudaEventSynchronize(h->lat_ev[fmt][1]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->lat_ev[fmt][0], h->lat_ev[fmt][1]));
+    h->c_latency[fmt] = ms * 1e-3;
+    h->lat_pending[fmt] = false;
+  }
+  return h->c_latency[fmt];
+}
+
+int64_t sell_slots(spmv_matrix* h) {
+  if (h->sell_built && h->sell_slots_pending) {
+    int64_t v = 0;
+    CK(cudaMemcpyAsync(&v, h->sell_sp + h->sell_ns, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->sell_slots = v;
+    h->sell_slots_pending = false;
+  }
+  return h->sell_slots;
+}
+
+int64_t format_stored_bytes(spmv_matrix* h, int fmt) {
   const int64_t vb = h->vbytes, rpb = h->rp64 ? 8 : 4;
   switch (fmt) {
     case SPMV_FMT_CSR: return (h->rows + 1) * rpb + h->nnz * (4 + vb);
     case SPMV_FMT_COO: return h->nnz * (8 + vb) + h->coo_n_empty * 4;
     case SPMV_FMT_ELL: return h->ell_K * h->ell_npad * (4 + vb);
     case SPMV_FMT_SELL:
-      return h->sell_slots * (4 + vb) + (h->sell_ns + 1) * 8 + (h->sell_perm ? h->rows * 4 : 0);
+      return sell_slots(h) * (4 + vb) + (h->sell_ns + 1) * 8 + (h->sell_perm ? h->rows * 4 : 0);
     case SPMV_FMT_HYB: return h->hyb_K * h->hyb_npad * (4 + vb) + h->hyb_tail * (8 + vb);
   }
   return 0;

@@ -60,6 +60,10 @@ struct spmv_matrix {
 
   double f_latency = 0.0;
   double c_latency[SPMV_NUM_FORMATS] = {0, 0, 0, 0, 0};
+  // conversion timings are recorded as CUDA events and resolved lazily (no sync in convert)
+  cudaEvent_t lat_ev[SPMV_NUM_FORMATS][2] = {};
+  bool lat_pending[SPMV_NUM_FORMATS] = {false, false, false, false, false};
+  bool sell_slots_pending = false;  // sell_slots still on the device (sell_sp[ns])
 
   // Scratch (grow-only) for segmented-reduction chunk records and for the
   // power-step block partials.
@@ -90,7 +94,11 @@ void build_ell(spmv_matrix* h);
 void build_sell(spmv_matrix* h, int64_t C, int64_t sigma);
 void build_hyb(spmv_matrix* h, int64_t K);
 void free_format(spmv_matrix* h, int fmt);
-int64_t format_stored_bytes(const spmv_matrix* h, int fmt);
+int64_t format_stored_bytes(spmv_matrix* h, int fmt);
+// Conversion latency of fmt in seconds (waits for its stop event if needed).
+double format_latency(spmv_matrix* h, int fmt);
+// SELL stored slot count (reads it back from the device if still pending).
+int64_t sell_slots(spmv_matrix* h);
 
 // Epilogue parameters shared by every SpMV kernel.
 struct Epilogue {

@@ -30,6 +30,11 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
   const T* __restrict__ val = static_cast<const T*>(p.val);
   const T* __restrict__ x = static_cast<const T*>(p.x);
   T* __restrict__ y = static_cast<T*>(p.y);
+  // Programmatic dependent launch (power loop): let the next step's grid get
+  // resident while this one drains, and wait for the previous step's writes
+  // (x, sums_prev) before reading them. No-ops without the launch attribute.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const double alpha = epi_alpha(p.e);
   double yy = 0.0, xy = 0.0;
   // persistent: each warp walks slices warp0, warp0 + nwarps, ... so the

@@ -25,6 +25,24 @@ void launch_sliced(spmv_matrix* h, kern::SlicedParams& p, int C, const spmv_laun
     p.e.counter = h->pi_counter;
   }
   void* args[] = {&p};
+  if (p.e.mode == 1) {
+    // power step: programmatic dependent launch (see k_sliced)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(L.block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e != cudaSuccess) cudaGetLastError();
+    cuda_check(e, "cudaLaunchKernelExC");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return;
+  }
   launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
 }
 
