@@ -5,6 +5,8 @@
 // saved in a third array called Row Index") — fused into ONE pass
 // over the triplets when the input is already sorted (28 B/nnz for fp64).
 // Unsorted input is radix-sorted by (row, col) first.
+#include <cstdlib>
+
 #include "handle.cuh"
 #include "primitives.cuh"
 
@@ -237,7 +239,12 @@ void ingest_typed(spmv_matrix* h, const int32_t* row_idx, const int32_t* col_idx
 
 void ingest(spmv_matrix* h, const int32_t* row_idx, const int32_t* col_idx, const void* vals,
             spmv_mem_t where) {
-  h->rp64 = h->nnz > (int64_t)INT32_MAX;
+  // int64 row pointers iff nnz >= 2^31; SPMV_FORCE_RP64=1 forces them (testing the int64 paths)
+  static const bool force64 = [] {
+    const char* e = getenv("SPMV_FORCE_RP64");
+    return e && e[0] == '1';
+  }();
+  h->rp64 = force64 || h->nnz > (int64_t)INT32_MAX;
   if (h->dtype == SPMV_R64F) {
     if (h->rp64)
       ingest_typed<int64_t, double>(h, row_idx, col_idx, static_cast<const double*>(vals), where);
