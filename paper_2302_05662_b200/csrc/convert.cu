@@ -56,20 +56,30 @@ __global__ void k_sell_keys(const RP* __restrict__ rp, int64_t rows, int64_t sig
 template <class RP>
 __global__ void k_sell_widths(const RP* __restrict__ rp, const int32_t* __restrict__ perm, int64_t rows,
                               int64_t C, int64_t ns, int64_t* __restrict__ cw) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += stride) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = w0; s < ns; s += nw) {  // warp per slice, lanes over its rows
     int64_t w = 0;
-    for (int64_t j = 0; j < C; ++j) {
-      int64_t q = s * C + j;
-      if (q >= rows) break;
-      int64_t i = perm ? perm[q] : q;
-      int64_t L = rp[i + 1] - rp[i];
-      w = L > w ? L : w;
+    for (int64_t j = lane; j < C; j += 32) {
+      const int64_t q = s * C + j;
+      if (q < rows) {
+        const int64_t i = perm ? perm[q] : q;
+        const int64_t L = rp[i + 1] - rp[i];
+        w = L > w ? L : w;
+      }
     }
-    cw[s] = C * w;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t v = __shfl_xor_sync(0xffffffffu, w, o);
+      w = v > w ? v : w;
+    }
+    if (lane == 0) cw[s] = C * w;
   }
 }
 
+// Thread per (slice, lane): writes of one step k are coalesced across the
+// lanes of a slice; each thread walks its own row's entries in order.
 template <class RP, class V>
 __global__ void k_sell_fill(const RP* __restrict__ rp, const int32_t* __restrict__ col,
                             const V* __restrict__ val, const int32_t* __restrict__ perm, int64_t rows,
@@ -78,16 +88,16 @@ __global__ void k_sell_fill(const RP* __restrict__ rp, const int32_t* __restrict
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t total = ns * C;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
-    int64_t s = t / C, j = t - s * C;
-    int64_t base = sp[s], w = (sp[s + 1] - base) / C;
+    const int64_t s = t / C, j = t - s * C;
+    const int64_t base = sp[s], w = (sp[s + 1] - base) / C;
     int64_t a = 0, L = 0;
     if (t < rows) {
-      int64_t i = perm ? perm[t] : t;
+      const int64_t i = perm ? perm[t] : t;
       a = rp[i];
       L = rp[i + 1] - a;
     }
     for (int64_t k = 0; k < w; ++k) {
-      int64_t pos = base + k * C + j;
+      const int64_t pos = base + k * C + j;
       if (k < L) {
         colS[pos] = col[a + k];
         valS[pos] = val[a + k];
@@ -250,7 +260,8 @@ void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma) {
   }
   int64_t* cw = sc.get<int64_t>(ns);
   int64_t* sp = sc.get<int64_t>(ns + 1);
-  LAUNCH(k_sell_widths<RP>, grid_for(ns, 256), 256, 0, s, rp, (const int32_t*)perm, rows, C, ns, cw);
+  LAUNCH(k_sell_widths<RP>, grid_for(ns * 32, 256, (int64_t)kNumSMs * 16), 256, 0, s, rp, (const int32_t*)perm,
+         rows, C, ns, cw);
   exclusive_scan_i64(cw, sp, ns, s);
   // Near-regular matrices: allocate the upper bound ns·C·max_len (no host
   // round trip); the exact slot count stays on the device until asked for.

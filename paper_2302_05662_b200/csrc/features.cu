@@ -113,20 +113,38 @@ __global__ void __launch_bounds__(1024) k_select(const unsigned* __restrict__ hi
                                                  const long long* __restrict__ big,
                                                  const unsigned long long* __restrict__ nbig_p,
                                                  const long long* __restrict__ targets,
+                                                 const StatPartial* __restrict__ part, int nparts,
                                                  long long* __restrict__ out) {
   __shared__ long long s_chunk[kChunks + 1];
   __shared__ long long s_scan[1024];
   __shared__ unsigned long long s_best[32];
+  __shared__ long long s_max[32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const long long nbig = (long long)*nbig_p;
-  // chunk sums: 16 threads per chunk, 64 bins each
+  // largest row length (from the row-stats partials) bounds the bins to scan
   {
-    int c = t >> 4, part = t & 15;
-    long long s = 0;
-    for (int b = 0; b < 64; ++b) s += hist[c * kChunk + part * 64 + b];
+    long long m = 0;
+    for (int i = t; i < nparts; i += blockDim.x) m = part[i].max_len > m ? part[i].max_len : m;
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (part == 0) s_chunk[c + 1] = s;
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long v = __shfl_xor_sync(0xffffffffu, m, o);
+      m = v > m ? v : m;
+    }
+    if (lane == 0) s_max[warp] = m;
+  }
+  __syncthreads();
+  long long maxlen = 0;
+  for (int w = 0; w < 32; ++w) maxlen = s_max[w] > maxlen ? s_max[w] : maxlen;
+  const int maxbin = (int)(maxlen < kBins - 1 ? maxlen : kBins - 1);
+  const int nchunk = maxbin / kChunk + 1;
+  // chunk sums over the used chunks: a warp per chunk, coalesced loads
+  for (int c = warp; c < kChunks; c += 32) {
+    long long sum = 0;
+    if (c < nchunk)
+      for (int b = lane; b < kChunk; b += 32) sum += hist[c * kChunk + b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) s_chunk[c + 1] = sum;
   }
   __syncthreads();
   if (t == 0) {
@@ -172,7 +190,7 @@ __global__ void __launch_bounds__(1024) k_select(const unsigned* __restrict__ hi
   }
   // mode: max count, smallest length on ties. Pack (count, ~bin) into u64.
   unsigned long long best = 0;
-  for (int b = t; b < kBins; b += blockDim.x) {
+  for (int b = t; b <= maxbin; b += blockDim.x) {
     unsigned long long key = ((unsigned long long)hist[b] << 32) | (unsigned long long)(0xFFFFFFFFu - (unsigned)b);
     if (hist[b] && key > best) best = key;
   }
@@ -231,7 +249,7 @@ void features_typed(spmv_matrix* h) {
   LAUNCH(k_row_stats<RP>, grid, kStatThreads, 0, s, static_cast<const RP*>(h->row_ptr), h->col, n, part,
          hist, big, nbig);
   LAUNCH(k_select, 1, 1024, 0, s, (const unsigned*)hist, (const long long*)big,
-         (const unsigned long long*)nbig, (const long long*)d_targets, d_out);
+         (const unsigned long long*)nbig, (const long long*)d_targets, (const StatPartial*)part, (int)grid, d_out);
   std::vector<StatPartial> hp(grid);
   long long res[4];
   CK(cudaMemcpyAsync(hp.data(), part, grid * sizeof(StatPartial), cudaMemcpyDeviceToHost, s));
