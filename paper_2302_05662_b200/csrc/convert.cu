@@ -222,10 +222,10 @@ void ell_typed(spmv_matrix* h) {
   cudaStream_t s = h->stream;
   const int64_t K = h->feat.max_len, n_pad = (h->rows + 127) / 128 * 128;
   guard_bytes((double)K * n_pad * (4.0 + sizeof(V)), "ELL");
-  lat_begin(h, SPMV_FMT_ELL);
   Scratch sc(s);
   int32_t* colE = sc.get<int32_t>(K * n_pad);
   V* valE = sc.get<V>(K * n_pad);
+  lat_begin(h, SPMV_FMT_ELL);  // c_latency = device time of the conversion kernels (allocation excluded)
   LAUNCH((k_ell_fill<RP, V>), grid_for(n_pad, 256), 256, 0, s, static_cast<const RP*>(h->row_ptr), h->col,
          static_cast<const V*>(h->val), h->rows, K, n_pad, colE, valE);
   lat_end(h, SPMV_FMT_ELL);
@@ -242,35 +242,48 @@ template <class RP, class V>
 void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma) {
   cudaStream_t s = h->stream;
   const int64_t rows = h->rows, ns = (rows + C - 1) / C;
-  lat_begin(h, SPMV_FMT_SELL);
   Scratch sc(s);
   const RP* rp = static_cast<const RP*>(h->row_ptr);
+  // Near-regular matrices: allocate the upper bound ns·C·max_len up front (no
+  // host round trip); the exact slot count stays on the device until asked for.
+  const int64_t ub = ns * C * h->feat.max_len;
+  const bool use_ub = (double)ub <= 1.25 * (double)h->nnz + (double)(64 << 20) / (4.0 + sizeof(V));
   int32_t* perm = nullptr;
+  uint64_t *keys = nullptr, *keys_s = nullptr;
+  uint32_t* p32 = nullptr;
   if (sigma > 1 && rows > 0) {
+    keys = sc.get<uint64_t>(rows);
+    keys_s = sc.get<uint64_t>(rows);
+    p32 = sc.get<uint32_t>(rows);
+    perm = sc.get<int32_t>(rows);
+  }
+  int64_t* cw = sc.get<int64_t>(ns);
+  int64_t* sp = sc.get<int64_t>(ns + 1);
+  int32_t* colS = nullptr;
+  V* valS = nullptr;
+  if (use_ub) {
+    guard_bytes((double)ub * (4.0 + sizeof(V)), "SELL");
+    colS = sc.get<int32_t>(ub);
+    valS = sc.get<V>(ub);
+  }
+  lat_begin(h, SPMV_FMT_SELL);  // c_latency = device time of the conversion kernels
+  if (perm) {
     const int64_t maxlen = h->feat.max_len;
     int lenbits = bits_for((uint64_t)maxlen);
     int winbits = bits_for((uint64_t)((rows - 1) / sigma));
-    uint64_t* keys = sc.get<uint64_t>(rows);
-    uint64_t* keys_s = sc.get<uint64_t>(rows);
-    uint32_t* p32 = sc.get<uint32_t>(rows);
-    perm = sc.get<int32_t>(rows);
     LAUNCH(k_sell_keys<RP>, grid_for(rows, 256), 256, 0, s, rp, rows, sigma, lenbits, maxlen, keys);
     radix_sort_pairs(keys, nullptr, keys_s, p32, rows, lenbits + winbits, s);
     LAUNCH(k_u32_to_i32, grid_for(rows, 256), 256, 0, s, (const uint32_t*)p32, perm, rows);
   }
-  int64_t* cw = sc.get<int64_t>(ns);
-  int64_t* sp = sc.get<int64_t>(ns + 1);
   LAUNCH(k_sell_widths<RP>, grid_for(ns * 32, 256, (int64_t)kNumSMs * 16), 256, 0, s, rp, (const int32_t*)perm,
          rows, C, ns, cw);
   exclusive_scan_i64(cw, sp, ns, s);
-  // Near-regular matrices: allocate the upper bound ns·C·max_len (no host
-  // round trip); the exact slot count stays on the device until asked for.
-  const int64_t ub = ns * C * h->feat.max_len;
-  const bool use_ub = (double)ub <= 1.25 * (double)h->nnz + (double)(64 << 20) / (4.0 + sizeof(V));
   const int64_t slots = use_ub ? ub : read_i64(sp + ns, s);
-  guard_bytes((double)slots * (4.0 + sizeof(V)), "SELL");
-  int32_t* colS = sc.get<int32_t>(slots);
-  V* valS = sc.get<V>(slots);
+  if (!use_ub) {
+    guard_bytes((double)slots * (4.0 + sizeof(V)), "SELL");
+    colS = sc.get<int32_t>(slots);
+    valS = sc.get<V>(slots);
+  }
   LAUNCH((k_sell_fill<RP, V>), grid_for(ns * C, 256), 256, 0, s, rp, h->col, static_cast<const V*>(h->val),
          (const int32_t*)perm, rows, C, ns, (const int64_t*)sp, colS, valS);
   lat_end(h, SPMV_FMT_SELL);
@@ -293,15 +306,15 @@ void hyb_typed(spmv_matrix* h, int64_t K) {
   cudaStream_t s = h->stream;
   const int64_t rows = h->rows, n_pad = (rows + 127) / 128 * 128;
   guard_bytes((double)K * n_pad * (4.0 + sizeof(V)), "HYB");
-  lat_begin(h, SPMV_FMT_HYB);
   Scratch sc(s);
   const RP* rp = static_cast<const RP*>(h->row_ptr);
   int32_t* colE = sc.get<int32_t>(K * n_pad);
   V* valE = sc.get<V>(K * n_pad);
-  LAUNCH((k_ell_fill<RP, V>), grid_for(n_pad, 256), 256, 0, s, rp, h->col, static_cast<const V*>(h->val),
-         rows, K, n_pad, colE, valE);
   int64_t* cnt = sc.get<int64_t>(rows);
   int64_t* toff = sc.get<int64_t>(rows + 1);
+  lat_begin(h, SPMV_FMT_HYB);  // kernels + the tail-size read-back
+  LAUNCH((k_ell_fill<RP, V>), grid_for(n_pad, 256), 256, 0, s, rp, h->col, static_cast<const V*>(h->val),
+         rows, K, n_pad, colE, valE);
   LAUNCH(k_row_counts<RP>, grid_for(rows, 256), 256, 0, s, rp, rows, 1, K, cnt);
   exclusive_scan_i64(cnt, toff, rows, s);
   const int64_t tail = read_i64(toff + rows, s);
@@ -328,16 +341,16 @@ template <class RP, class V>
 void coo_typed(spmv_matrix* h) {
   cudaStream_t s = h->stream;
   const int64_t rows = h->rows;
-  lat_begin(h, SPMV_FMT_COO);
   Scratch sc(s);
   const RP* rp = static_cast<const RP*>(h->row_ptr);
   int32_t* crow = sc.get<int32_t>(h->nnz);
+  int64_t* flag = sc.get<int64_t>(rows);
+  int64_t* off = sc.get<int64_t>(rows + 1);
+  lat_begin(h, SPMV_FMT_COO);  // kernels + the empty-row count read-back
   if (h->nnz > 0)
     LAUNCH((k_expand<RP, V>), (unsigned)((h->nnz + kExpandTile - 1) / kExpandTile), kExpandThreads, 0, s, rp,
            h->col, static_cast<const V*>(h->val), rows, h->nnz, 0, (int64_t)0, (const int64_t*)nullptr, crow,
            (int32_t*)nullptr, (V*)nullptr);
-  int64_t* flag = sc.get<int64_t>(rows);
-  int64_t* off = sc.get<int64_t>(rows + 1);
   LAUNCH(k_row_counts<RP>, grid_for(rows, 256), 256, 0, s, rp, rows, 0, (int64_t)0, flag);
   exclusive_scan_i64(flag, off, rows, s);
   const int64_t n_empty = read_i64(off + rows, s);
