@@ -12,7 +12,7 @@ hi = [i for i, r in enumerate(rows) if "Source" in r and "Address" in r][0]
 h = rows[hi]
 si = h.index("Warp Stall Sampling (All Samples)")
 stall_cols = [i for i, n in enumerate(h) if n.startswith("stall_") and "Not Issued" not in n]
-data = [r for r in rows[hi + 1:] if len(r) == len(h)]
+data = [r for r in rows[hi + 1:] if len(r) == len(h) and r[si].isdigit()]
 tot = sum(int(r[si]) for r in data)
 print("total samples", tot)
 for r in sorted(data, key=lambda r: -int(r[si]))[:top]:
