@@ -413,3 +413,21 @@ def test_native_power_iterate_matches_stepwise(use_comm):
         if comm is not None:
             comm.close()
         P.spmv_destroy(h)
+
+
+def test_tune_skewed_considers_skew_formats():
+    """Run-time mode on a power-law matrix: the selector must measure the
+    skew-oriented candidates (merge-path CSR, HYB, COO) and its choice must
+    still produce oracle-correct y (fp32 data, fp64 accumulation)."""
+    coo = si.rmat(15, dtype=np.float32)
+    h = create(coo, "f32")
+    try:
+        rep = P.spmv_tune(h, P.TUNE_ALL, expected_iterations=10 ** 6)
+        sel = [r for r in P.spmv_decision_log(h) if r["kind"] == "format_select"][0]
+        measured = {(c["format"], c.get("alg")) for c in sel["candidates"] if "t_s" in c}
+        assert ("CSR", "merge") in measured and ("HYB", None) in measured and ("COO", None) in measured
+        best = min(c["t_s"] for c in sel["candidates"] if "t_s" in c)
+        assert sel["gate"]["t_best_s"] == best
+        check_y(h, coo, "f32", rep.format, 2.5, -0.5)
+    finally:
+        P.spmv_destroy(h)
