@@ -46,7 +46,8 @@ typedef enum {
   SPMV_ERR_UNSUPPORTED = 6,        /* rows/cols > 2^31-1, SELL C not in {32,64,128,256}, ... */
   SPMV_ERR_CUDA = 7,               /* CUDA runtime error (sticky device faults surface here) */
   SPMV_ERR_NOT_CONVERTED = 8,      /* requested format has not been built on this handle */
-  SPMV_ERR_NCCL = 9                /* NCCL missing or a collective failed */
+  SPMV_ERR_NCCL = 9,               /* NCCL missing or a collective failed */
+  SPMV_ERR_NVML = 10               /* NVML missing (energy/power objectives) */
 } spmv_status_t;
 
 typedef enum { SPMV_R32F = 0, SPMV_R64F = 1 } spmv_dtype_t;
@@ -106,6 +107,18 @@ typedef struct {
 #define SPMV_TUNE_LAUNCH 1u /* compile-time-mode analog: sweep launch variants of the active format */
 #define SPMV_TUNE_FORMAT 2u /* run-time-mode analog: select a format from features, measure, gate */
 #define SPMV_TUNE_ALL 3u
+/* Optimisation objective (the paper's four), OR-ed into the
+ * flags. Non-latency objectives measure each candidate's energy with NVML
+ * over >= 0.4 s of back-to-back SpMVs (SPMV_ERR_NVML if NVML is missing):
+ *  LATENCY    min seconds per SpMV (default)
+ *  ENERGY     min joules per SpMV
+ *  POWER      min average watts while running
+ *  EFFICIENCY max MFLOPS/W (= MFLOP per joule) */
+#define SPMV_TUNE_OBJ_LATENCY (0u << 4)
+#define SPMV_TUNE_OBJ_ENERGY (1u << 4)
+#define SPMV_TUNE_OBJ_POWER (2u << 4)
+#define SPMV_TUNE_OBJ_EFFICIENCY (3u << 4)
+#define SPMV_TUNE_OBJ_MASK (3u << 4)
 
 typedef struct {
   int32_t format;                /* chosen spmv_format_t (active after the call) */
@@ -119,6 +132,11 @@ typedef struct {
   int32_t converted;             /* 1 iff the gate accepted the conversion */
   int32_t n_candidates;          /* formats measured */
   int32_t n_variants;            /* launch variants measured */
+  int32_t objective;             /* 0 latency, 1 energy, 2 power, 3 efficiency */
+  int32_t reserved;
+  double energy_j;               /* chosen: joules per SpMV (NaN if not measured) */
+  double power_w;                /* chosen: average watts while running (NaN if not measured) */
+  double mflops_per_w;           /* chosen: MFLOPS/W (NaN if not measured) */
 } spmv_tune_report_t;
 
 /* Format introspection (sizes of what spmv_copy_array can export). */
@@ -206,8 +224,11 @@ spmv_status_t spmv_get_launch(spmv_handle_t h, spmv_format_t fmt, spmv_launch_t*
  * LAUNCH: time every launch variant of the active format, keep the fastest.
  * FORMAT: features -> candidate formats -> convert + measure each -> gate:
  *   switch away from CSR iff expected_iterations·(t_csr − t_best) >
- *   f_latency + c_latency(best) (strict >). Uses scratch x/y (never
- *   the caller's). Synchronous. Decisions appended to the JSON log. */
+ *   f_latency + c_latency(best) (strict >). With an energy /
+ *   efficiency objective the gate compares energy (conversion energy =
+ *   CSR's average power × (f + c)); with the power objective the format with
+ *   the lower average power wins. Uses scratch x/y (never the caller's).
+ *   Synchronous. Decisions appended to the JSON log. */
 spmv_status_t spmv_tune(spmv_handle_t h, uint32_t flags, int64_t expected_iterations,
                         spmv_tune_report_t* out);
 

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libspmv.so")
 
 # ---------------------------------------------------------------- enums (spmv.h)
 OK, ERR_INVALID_ARG, ERR_INDEX_OUT_OF_RANGE, ERR_DUPLICATE, ERR_INFEASIBLE, ERR_OUT_OF_MEMORY, \
-    ERR_UNSUPPORTED, ERR_CUDA, ERR_NOT_CONVERTED, ERR_NCCL = range(10)
+    ERR_UNSUPPORTED, ERR_CUDA, ERR_NOT_CONVERTED, ERR_NCCL, ERR_NVML = range(11)
 R32F, R64F = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
 FMT_COO, FMT_CSR, FMT_ELL, FMT_HYB, FMT_SELL = 0, 1, 2, 3, 4
@@ -29,6 +29,7 @@ FORMATS = {"COO": FMT_COO, "CSR": FMT_CSR, "ELL": FMT_ELL, "HYB": FMT_HYB, "SELL
 FORMAT_NAMES = {v: k for k, v in FORMATS.items()}
 CSR_AUTO, CSR_SCALAR, CSR_VECTOR, CSR_MERGE = 0, 1, 2, 3
 TUNE_LAUNCH, TUNE_FORMAT, TUNE_ALL = 1, 2, 3
+OBJECTIVES = {"latency": 0, "energy": 1, "power": 2, "efficiency": 3}   # OR-ed into flags as value << 4
 (ARR_CSR_ROW_PTR, ARR_CSR_COL, ARR_CSR_VAL, ARR_COO_ROW, ARR_ELL_COL, ARR_ELL_VAL, ARR_SELL_PERM,
  ARR_SELL_SLICE_PTR, ARR_SELL_COL, ARR_SELL_VAL, ARR_HYB_ELL_COL, ARR_HYB_ELL_VAL, ARR_HYB_TAIL_ROW,
  ARR_HYB_TAIL_COL, ARR_HYB_TAIL_VAL, ARR_COO_EMPTY_ROWS) = range(16)
@@ -68,7 +69,9 @@ class TuneReport(ctypes.Structure):
                 ("t_csr_s", ctypes.c_double), ("t_best_s", ctypes.c_double),
                 ("f_latency_s", ctypes.c_double), ("c_latency_s", ctypes.c_double),
                 ("expected_iterations", ctypes.c_int64), ("converted", ctypes.c_int32),
-                ("n_candidates", ctypes.c_int32), ("n_variants", ctypes.c_int32)]
+                ("n_candidates", ctypes.c_int32), ("n_variants", ctypes.c_int32),
+                ("objective", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("energy_j", ctypes.c_double), ("power_w", ctypes.c_double), ("mflops_per_w", ctypes.c_double)]
 
 
 class FormatInfo(ctypes.Structure):
@@ -227,9 +230,11 @@ def spmv_get_launch(h, fmt):
     return L.as_tuple()
 
 
-def spmv_tune(h, flags=TUNE_ALL, expected_iterations=100):
+def spmv_tune(h, flags=TUNE_ALL, expected_iterations=100, objective="latency"):
+    """objective: latency | energy | power | efficiency (the paper's four)."""
     r = TuneReport()
-    _check(lib().spmv_tune(h, flags, int(expected_iterations), ctypes.byref(r)), h)
+    fl = int(flags) | (OBJECTIVES[objective] << 4)
+    _check(lib().spmv_tune(h, fl, int(expected_iterations), ctypes.byref(r)), h)
     return r
 
 

@@ -283,6 +283,39 @@ struct TuneScratch {
   }
 };
 
+// Objective-aware measurement.
+struct Objective {
+  int obj = 0;  // 0 latency, 1 energy, 2 power, 3 efficiency
+  static const char* name(int o) {
+    static const char* n[] = {"latency", "energy", "power", "efficiency"};
+    return (o >= 0 && o < 4) ? n[o] : "?";
+  }
+};
+
+struct Measured {
+  double t = 0;                           // seconds per SpMV (latency sweep)
+  double ej = std::nan(""), w = std::nan(""), eff = std::nan("");  // J per SpMV, W, MFLOPS/W
+};
+
+static void measure_objective(spmv_matrix* h, int fmt, const spmv_launch_t& L, const void* x, void* y,
+                              Measured& m) {
+  Epilogue e;
+  EnergySample s = measure_energy(h, [&] { dispatch(h, fmt, e, x, y, L); }, 0.4);
+  m.ej = s.reps > 0 ? s.joules / (double)s.reps : std::nan("");
+  m.w = s.watts;
+  m.eff = s.joules > 0 ? 2.0 * (double)h->nnz * (double)s.reps / 1e6 / s.joules : std::nan("");
+}
+
+// Smaller is better for every objective (efficiency is negated).
+static double objective_value(int obj, const Measured& m) {
+  switch (obj) {
+    case 1: return m.ej;
+    case 2: return m.w;
+    case 3: return -m.eff;
+    default: return m.t;
+  }
+}
+
 static const char* fmt_name(int f) {
   static const char* n[] = {"COO", "CSR", "ELL", "HYB", "SELL"};
   return (f >= 0 && f < 5) ? n[f] : "?";
@@ -316,15 +349,22 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
 
 // Compile-time mode analog: sweep block × maxreg × carveout × knob
 // for the active format; keep the argmin of the median time.
-static void tune_launch(spmv_matrix* h, int fmt, TuneScratch& ts, spmv_tune_report_t* rep) {
+// Compile-time mode analog: sweep block × maxreg × carveout × knob
+// for the active format; keep the argmin of the median time. With a
+// non-latency objective the 6 fastest variants are re-measured with NVML and
+// the objective decides among them.
+static void tune_launch(spmv_matrix* h, int fmt, TuneScratch& ts, spmv_tune_report_t* rep, int obj) {
   static const int blocks[] = {64, 128, 256, 512, 1024};
   static const int regs[] = {32, 64, 128, 255};
   static const int carve[] = {0, 25, 50, 100};
   spmv_launch_t best = resolve_launch(h, fmt, h->launch[fmt]);
   double tbest = time_variant(h, fmt, best, ts.x, ts.y);
+  std::vector<std::pair<double, spmv_launch_t>> all{{tbest, best}};
   int n = 1;
   std::ostringstream os;
-  os << "{\"kind\":\"launch_sweep\",\"format\":\"" << fmt_name(fmt) << "\",\"variants\":[";
+  os.precision(9);
+  os << "{\"kind\":\"launch_sweep\",\"format\":\"" << fmt_name(fmt) << "\",\"objective\":\""
+     << Objective::name(obj) << "\",\"variants\":[";
   bool first = true;
   for (int knob : knob_set(h, fmt))
     for (int b : blocks)
@@ -339,6 +379,7 @@ static void tune_launch(spmv_matrix* h, int fmt, TuneScratch& ts, spmv_tune_repo
             continue;
           }
           ++n;
+          all.push_back({t, L});
           os << (first ? "" : ",") << "[" << b << "," << r << "," << c << "," << knob << "," << t << "]";
           first = false;
           if (t < tbest) {
@@ -347,13 +388,42 @@ static void tune_launch(spmv_matrix* h, int fmt, TuneScratch& ts, spmv_tune_repo
           }
         }
   os << "],\"best\":[" << best.block << "," << best.maxreg << "," << best.carveout_pct << "," << best.knob
-     << "],\"t_best_s\":" << tbest << "}";
+     << "],\"t_best_s\":" << tbest;
+  Measured chosen;
+  chosen.t = tbest;
+  if (obj != 0) {
+    std::sort(all.begin(), all.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    const size_t top = std::min<size_t>(6, all.size());
+    double vbest = 0;
+    os << ",\"objective_top\":[";
+    for (size_t i = 0; i < top; ++i) {
+      Measured m;
+      m.t = all[i].first;
+      measure_objective(h, fmt, all[i].second, ts.x, ts.y, m);
+      const double v = objective_value(obj, m);
+      const spmv_launch_t& L = all[i].second;
+      os << (i ? "," : "") << "{\"launch\":[" << L.block << "," << L.maxreg << "," << L.carveout_pct << ","
+         << L.knob << "],\"t_s\":" << m.t << ",\"j_per_spmv\":" << m.ej << ",\"w\":" << m.w
+         << ",\"mflops_per_w\":" << m.eff << "}";
+      if (i == 0 || v < vbest) {
+        vbest = v;
+        best = L;
+        chosen = m;
+      }
+    }
+    os << "],\"objective_best\":[" << best.block << "," << best.maxreg << "," << best.carveout_pct << ","
+       << best.knob << "]";
+  }
+  os << "}";
   log_append(h, os.str());
   h->launch[fmt] = best;
   if (rep) {
     rep->launch = best;
-    rep->t_best_s = tbest;
+    rep->t_best_s = chosen.t;
     rep->n_variants += n;
+    rep->energy_j = chosen.ej;
+    rep->power_w = chosen.w;
+    rep->mflops_per_w = chosen.eff;
   }
 }
 
@@ -363,7 +433,7 @@ static double sell_padding(spmv_matrix* h) {
 }
 
 // Run-time mode analog: features -> candidates -> measure -> gate.
-static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tune_report_t* rep) {
+static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tune_report_t* rep, int obj) {
   if (!h->have_features) compute_features(h);
   const spmv_features_t& f = h->feat;
   const int orig_alg = h->csr_alg;
@@ -378,6 +448,7 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
     int alg;
     double t, c;
     std::string why;
+    Measured m;
   };
   std::vector<Cand> cands;
   // CSR (paper default): CSR-vector with T from the mean.
@@ -421,22 +492,49 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
     try_build(SPMV_FMT_HYB, "skewed rows");
     try_build(SPMV_FMT_COO, "skewed rows");
   }
+  for (Cand& c : cands) {
+    c.m.t = c.t;
+    if (obj != 0) {  // energy / power / efficiency: NVML window per candidate
+      if (c.fmt == SPMV_FMT_CSR) h->csr_alg = c.alg;
+      measure_objective(h, c.fmt, resolve_launch(h, c.fmt, c.fmt == SPMV_FMT_CSR ? spmv_launch_t{0, 0, -1, 0}
+                                                                              : h->launch[c.fmt]),
+                        ts.x, ts.y, c.m);
+      h->csr_alg = orig_alg;
+    }
+  }
   size_t bi = 0;
   for (size_t i = 0; i < cands.size(); ++i) {
     const Cand& c = cands[i];
     os << "{\"format\":\"" << fmt_name(c.fmt) << "\"" << (c.alg == SPMV_CSR_MERGE ? ",\"alg\":\"merge\"" : "")
-       << ",\"t_s\":" << c.t << ",\"c_latency_s\":" << c.c << ",\"why\":\"" << c.why << "\"}"
-       << (i + 1 < cands.size() ? "," : "");
-    if (c.t < cands[bi].t) bi = i;
+       << ",\"t_s\":" << c.t << ",\"c_latency_s\":" << c.c << ",\"why\":\"" << c.why << "\"";
+    if (obj != 0)
+      os << ",\"j_per_spmv\":" << c.m.ej << ",\"w\":" << c.m.w << ",\"mflops_per_w\":" << c.m.eff;
+    os << "}" << (i + 1 < cands.size() ? "," : "");
+    if (objective_value(obj, c.m) < objective_value(obj, cands[bi].m)) bi = i;
   }
   const Cand& best = cands[bi];
-  const double gain = (double)iters * (t_csr - best.t);
-  const double overhead = h->f_latency + best.c;
-  const bool convert = gain > overhead;  // strict
+  const Cand& csr = cands[0];
+  double gain, overhead;
+  bool convert;
+  if (obj == 0) {  // time (strict >)
+    gain = (double)iters * (t_csr - best.t);
+    overhead = h->f_latency + best.c;
+    convert = gain > overhead;
+  } else if (obj == 2) {  // average power: no amortisation, the lower draw wins
+    gain = csr.m.w - best.m.w;
+    overhead = 0.0;
+    convert = gain > overhead;
+  } else {  // energy / efficiency: joules, conversion energy at CSR's average power
+    gain = (double)iters * (csr.m.ej - best.m.ej);
+    overhead = csr.m.w * (h->f_latency + best.c);
+    convert = gain > overhead;
+  }
   const int chosen = convert ? best.fmt : SPMV_FMT_CSR;
   const int chosen_alg = convert ? best.alg : SPMV_CSR_VECTOR;
-  os << "],\"gate\":{\"expected_iterations\":" << iters << ",\"t_csr_s\":" << t_csr << ",\"t_best_s\":" << best.t
-     << ",\"gain_s\":" << gain << ",\"f_latency_s\":" << h->f_latency << ",\"c_latency_s\":" << best.c
+  os << "],\"objective\":\"" << Objective::name(obj) << "\",\"gate\":{\"expected_iterations\":" << iters
+     << ",\"t_csr_s\":" << t_csr << ",\"t_best_s\":" << best.t << ",\"gain_s\":" << gain
+     << ",\"gain\":" << gain << ",\"overhead\":" << overhead
+     << ",\"f_latency_s\":" << h->f_latency << ",\"c_latency_s\":" << best.c
      << ",\"convert\":" << (convert ? "true" : "false") << "},\"chosen\":\"" << fmt_name(chosen)
      << (chosen == SPMV_FMT_CSR && chosen_alg == SPMV_CSR_MERGE ? "-merge" : "") << "\"}";
   log_append(h, os.str());
@@ -454,6 +552,10 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
     rep->expected_iterations = iters;
     rep->converted = convert ? 1 : 0;
     rep->n_candidates = (int32_t)cands.size();
+    const Measured& cm = convert ? best.m : csr.m;
+    rep->energy_j = cm.ej;
+    rep->power_w = cm.w;
+    rep->mflops_per_w = cm.eff;
     rep->params.csr_alg = h->csr_alg;
     rep->params.csr_T = h->csr_T;
     rep->params.sell_C = (int32_t)h->sell_C;
@@ -671,16 +773,22 @@ spmv_status_t spmv_get_launch(spmv_handle_t h, spmv_format_t fmt, spmv_launch_t*
 }
 
 spmv_status_t spmv_tune(spmv_handle_t h, uint32_t flags, int64_t expected_iterations, spmv_tune_report_t* out) {
-  if (!h || (flags & ~SPMV_TUNE_ALL) || flags == 0 || expected_iterations < 0) return SPMV_ERR_INVALID_ARG;
+  const uint32_t what = flags & SPMV_TUNE_ALL;
+  const int obj = (int)((flags & SPMV_TUNE_OBJ_MASK) >> 4);
+  if (!h || (flags & ~(SPMV_TUNE_ALL | SPMV_TUNE_OBJ_MASK)) || what == 0 || expected_iterations < 0)
+    return SPMV_ERR_INVALID_ARG;
   if (h->rows == 0 || h->nnz == 0) return SPMV_ERR_INVALID_ARG;
   API_TRY
   DeviceGuard g(h->device);
+  if (obj != 0 && !nvml_available()) fail(SPMV_ERR_NVML, "energy/power objectives need libnvidia-ml");
   spmv_tune_report_t rep{};
   rep.format = h->active;
   rep.expected_iterations = expected_iterations;
+  rep.objective = obj;
+  rep.energy_j = rep.power_w = rep.mflops_per_w = std::nan("");
   TuneScratch ts(h);
-  if (flags & SPMV_TUNE_FORMAT) tune_format(h, expected_iterations, ts, &rep);
-  if (flags & SPMV_TUNE_LAUNCH) tune_launch(h, h->active, ts, &rep);
+  if (what & SPMV_TUNE_FORMAT) tune_format(h, expected_iterations, ts, &rep, obj);
+  if (what & SPMV_TUNE_LAUNCH) tune_launch(h, h->active, ts, &rep, obj);
   rep.format = h->active;
   rep.launch = resolve_launch(h, h->active, h->launch[h->active]);
   CK(cudaStreamSynchronize(h->stream));
@@ -835,6 +943,7 @@ const char* spmv_status_string(spmv_status_t s) {
     case SPMV_ERR_CUDA: return "SPMV_ERR_CUDA";
     case SPMV_ERR_NOT_CONVERTED: return "SPMV_ERR_NOT_CONVERTED";
     case SPMV_ERR_NCCL: return "SPMV_ERR_NCCL";
+    case SPMV_ERR_NVML: return "SPMV_ERR_NVML";
   }
   return "SPMV_ERR_UNKNOWN";
 }

@@ -1,6 +1,7 @@
 // handle.cuh — the spmv_matrix handle and the internal entry points shared
 // by the translation units of libspmv.so.
 #pragma once
+#include <functional>
 #include <string>
 
 #include "common.cuh"
@@ -134,6 +135,14 @@ void power_iterate(spmv_matrix* h, const void* x0, void* buf0, void* buf1, int64
 void* dist_init(const uint8_t id[128], int rank, int world, int device);
 void dist_unique_id(uint8_t out[128]);
 void dist_destroy(void* comm);
+
+// energy.cu: NVML energy over a window of back-to-back launches.
+struct EnergySample {
+  double seconds = 0, joules = 0, watts = 0;
+  int64_t reps = 0;
+};
+EnergySample measure_energy(spmv_matrix* h, const std::function<void()>& launch, double min_seconds);
+bool nvml_available();
 
 // Make sure the power-step partial buffers hold >= nblocks entries.
 void ensure_pi_scratch(spmv_matrix* h, size_t nblocks);

@@ -431,3 +431,40 @@ def test_tune_skewed_considers_skew_formats():
         check_y(h, coo, "f32", rep.format, 2.5, -0.5)
     finally:
         P.spmv_destroy(h)
+
+
+@pytest.mark.parametrize("objective", ["energy", "power", "efficiency"])
+def test_tune_objectives(objective):
+    """The paper's four objectives: the selector measures
+    each candidate with NVML and picks the best for the objective; the gate
+    compares the objective's own units; the chosen format stays correct."""
+    coo = si.stencil27(48, random_values=True)
+    h = create(coo)
+    try:
+        try:
+            rep = P.spmv_tune(h, P.TUNE_ALL, expected_iterations=10 ** 5, objective=objective)
+        except P.SpmvError as e:
+            if e.status == P.ERR_NVML:
+                pytest.skip("NVML not available")
+            raise
+        log = P.spmv_decision_log(h)
+        sel = [r for r in log if r["kind"] == "format_select"][-1]
+        assert sel["objective"] == objective and rep.objective == P.OBJECTIVES[objective]
+        cands = [c for c in sel["candidates"] if "t_s" in c]
+        key = {"energy": lambda c: c["j_per_spmv"], "power": lambda c: c["w"],
+               "efficiency": lambda c: -c["mflops_per_w"]}[objective]
+        for c in cands:
+            assert c["j_per_spmv"] > 0 and c["w"] > 0 and c["mflops_per_w"] > 0
+            # MFLOPS/W is MFLOP per joule (P:891)
+            assert abs(c["mflops_per_w"] - 2 * coo.nnz / 1e6 / c["j_per_spmv"]) <= 1e-6 * c["mflops_per_w"]
+        best = min(cands, key=key)
+        g = sel["gate"]
+        assert g["convert"] == (g["gain"] > g["overhead"])
+        chosen = sel["chosen"].split("-")[0]
+        assert chosen == (best["format"] if g["convert"] else "CSR")
+        sweep = [r for r in log if r["kind"] == "launch_sweep"][-1]
+        assert sweep["objective"] == objective and len(sweep["objective_top"]) >= 1
+        assert np.isfinite(rep.energy_j) and np.isfinite(rep.power_w) and np.isfinite(rep.mflops_per_w)
+        check_y(h, coo, "f64", rep.format, 1.0, 0.0)
+    finally:
+        P.spmv_destroy(h)
