@@ -54,15 +54,17 @@ typedef enum { SPMV_R32F = 0, SPMV_R64F = 1 } spmv_dtype_t;
 typedef enum { SPMV_MEM_HOST = 0, SPMV_MEM_DEVICE = 1 } spmv_mem_t;
 
 /* Storage formats: COO, CSR, ELL, HYB (ELL + COO
- * tail; not in the paper, north star), SELL-C-sigma (P:165 generalised). */
+ * tail; not in the paper, north star), SELL-C-sigma (P:165 generalised),
+ * BELL (ELL over dense b×b blocks, Fig. 2(d) b = 2). */
 typedef enum {
   SPMV_FMT_COO = 0,
   SPMV_FMT_CSR = 1,
   SPMV_FMT_ELL = 2,
   SPMV_FMT_HYB = 3,
-  SPMV_FMT_SELL = 4
+  SPMV_FMT_SELL = 4,
+  SPMV_FMT_BELL = 5
 } spmv_format_t;
-#define SPMV_NUM_FORMATS 5
+#define SPMV_NUM_FORMATS 6
 
 /* CSR kernel algorithms: scalar (thread per row), vector (T lanes per row,
  * the "coordination among threads within a warp" of P:159), merge-path. */
@@ -80,6 +82,8 @@ typedef struct {
   int32_t sell_C;     /* SELL slice height in {32,64,128,256}; 0 = 32·(16 B / sizeof(value)) */
   int32_t sell_sigma; /* sorting window: 1 (no sort) or a multiple of sell_C; 0 = 1 */
   int64_t hyb_K;      /* HYB ELL width; -1 = automatic (CUSP/Bell–Garland rule, R12) */
+  int32_t bell_b;     /* BELL square block dimension in {2,3,4}; 0 = 2 (the paper's 2×2) */
+  int32_t reserved;
 } spmv_format_params_t;
 
 /* Table 2 features + the north star's max and bandwidth.
@@ -151,6 +155,7 @@ typedef struct {
   int64_t tail_nnz;      /* HYB COO tail */
   int64_t n_empty_rows;  /* COO: rows without entries */
   int64_t stored_bytes;  /* bytes of the format's arrays (padding included) */
+  int64_t block;         /* BELL block dimension b (K = blocks per block row, n_pad = padded block rows) */
 } spmv_format_info_t;
 
 typedef enum {
@@ -169,7 +174,9 @@ typedef enum {
   SPMV_ARR_HYB_TAIL_ROW = 12, /* int32 [tail_nnz], (row, col) order */
   SPMV_ARR_HYB_TAIL_COL = 13,
   SPMV_ARR_HYB_TAIL_VAL = 14,
-  SPMV_ARR_COO_EMPTY_ROWS = 15 /* int32 [n_empty_rows], ascending */
+  SPMV_ARR_COO_EMPTY_ROWS = 15, /* int32 [n_empty_rows], ascending */
+  SPMV_ARR_BELL_COL = 16,     /* int32 [K·n_pad]: block column of slot (I, k) at k·n_pad + I, pad −1 */
+  SPMV_ARR_BELL_VAL = 17      /* value [K·b·b·n_pad]: entry (r, c) of slot (I, k) at (k·b·b + r·b + c)·n_pad + I */
 } spmv_array_t;
 
 /* ---------------------------------------------------------------- core API */
@@ -279,7 +286,7 @@ const char* spmv_last_error(spmv_handle_t h);
 size_t spmv_decision_log(spmv_handle_t h, char* buf, size_t len);
 /* Conversion timings measured on the device by the last spmv_create /
  * spmv_convert / spmv_features calls, seconds (c_latency per format, f_latency). */
-spmv_status_t spmv_overheads(spmv_handle_t h, double* f_latency_s, double* c_latency_s /*[5]*/);
+spmv_status_t spmv_overheads(spmv_handle_t h, double* f_latency_s, double* c_latency_s /*[SPMV_NUM_FORMATS]*/);
 
 /* Number of CUDA kernels this library has launched in this process. */
 uint64_t spmv_launch_count(void);

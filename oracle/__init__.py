@@ -78,6 +78,9 @@ def lib():
         L.oracle_hyb_tail_nnz.argtypes = [i64, vp, i64]
         L.oracle_hyb_tail_nnz.restype = i64
         L.oracle_hyb_tail.argtypes = [i64, vp, vp, vp, i64, vp, vp, vp]
+        L.oracle_bell_kb.argtypes = [i64, vp, vp, i64, i64]
+        L.oracle_bell_kb.restype = i64
+        L.oracle_bell.argtypes = [i64, vp, vp, vp, i64, i64, i64, i64, vp, vp]
         L.oracle_spmv_csr.argtypes = [i64, vp, vp, vp, vp, d, d, vp, vp, vp]
         L.oracle_dense_spmv.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp]
         L.oracle_power_step.argtypes = [i64, vp, vp, vp, vp, vp, vp,
@@ -176,6 +179,19 @@ def hyb(rows, row_ptr, col, val, K=None):
     tr, tc, tv = np.empty(t, np.int32), np.empty(t, np.int32), np.empty(t, np.float64)
     lib().oracle_hyb_tail(rows, _p(rp), _p(col), _p(val), K, _p(tr), _p(tc), _p(tv))
     return K, n_pad, colE, valE, tr, tc, tv
+
+
+def bell(rows, row_ptr, col, val, bh=2, bw=2):
+    """O13: (Kb, nbr_pad, bcol[Kb·nbr_pad], bval[Kb·bh·bw·nbr_pad]) — value plane
+    e = r·bw + c of slot k at (k·bh·bw + e)·nbr_pad + I."""
+    rp, col, val = _c(row_ptr, np.int64), _c(col, np.int32), _c(val, np.float64)
+    kb = lib().oracle_bell_kb(rows, _p(rp), _p(col), bh, bw)
+    nbr = (rows + bh - 1) // bh
+    nbr_pad = (nbr + 127) // 128 * 128
+    bcol = np.empty(kb * nbr_pad, np.int32)
+    bval = np.empty(kb * bh * bw * nbr_pad, np.float64)
+    lib().oracle_bell(rows, _p(rp), _p(col), _p(val), bh, bw, kb, nbr_pad, _p(bcol), _p(bval))
+    return kb, nbr_pad, bcol, bval
 
 
 # --------------------------------------------------------------------------- O8–O12

@@ -6,7 +6,7 @@
  * this file shares no code, header, table or constant generator with it.
  *
  * Plain, slow, obviously-correct C in fp64, written from the paper's
- * definitions as read in SURVEY.md §8(c) (items O1–O12) and DESIGN.md
+ * definitions as read in SURVEY.md §8(c) (items O1–O12, plus O13 BELL) and DESIGN.md
  * "Readings". Citations: P:n = /root/reference/PAPER.md line n,
  * S:n = /root/reference/SPEC.md line n (interfaces/test ideas only).
  *
@@ -332,6 +332,68 @@ EXPORT void oracle_hyb_tail(int64_t rows, const int64_t* row_ptr, const int32_t*
       tv[t] = val[k];
       ++t;
     }
+}
+
+/* ---------------------------------------------------------------------------
+ * O13 BELL — "a block of non-zero elements is considered as an element of the
+ * ELL format ... 1) Data matrix, which is used to store blocks of non-zero
+ * elements, and 2) Column Index matrix, which is used to store the block
+ * indices" (Fig. 2(d) uses 2 × 2 blocks). Reading R11b:
+ * block row I covers rows [I·bh, I·bh+bh), block column J covers columns
+ * [J·bw, J·bw+bw); a block is stored iff it holds at least one entry; block
+ * row I lists its blocks by increasing J; Kb = max blocks per block row;
+ * column-major padding to nbr_pad = ceil(n_brows/128)·128 block rows:
+ * bcol[k·nbr_pad + I] = J or −1, and value plane e = r·bw + c of slot k at
+ * bval[(k·bh·bw + e)·nbr_pad + I] = A(I·bh + r, J·bw + c) or +0.0.
+ * Pins: SPEC S:143-144 examples, reconstruct-dense, block-count brute force.
+ * ------------------------------------------------------------------------- */
+EXPORT int64_t oracle_bell_kb(int64_t rows, const int64_t* row_ptr, const int32_t* col, int64_t bh,
+                              int64_t bw) {
+  int64_t nbr = (rows + bh - 1) / bh, kb = 0;
+  for (int64_t I = 0; I < nbr; ++I) {
+    int64_t count = 0, last = -1;
+    /* blocks of block row I in increasing J: repeatedly take the smallest J > last */
+    for (;;) {
+      int64_t best = -1;
+      for (int64_t i = I * bh; i < (I + 1) * bh && i < rows; ++i)
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+          int64_t J = col[k] / bw;
+          if (J > last && (best < 0 || J < best)) best = J;
+        }
+      if (best < 0) break;
+      last = best;
+      ++count;
+    }
+    if (count > kb) kb = count;
+  }
+  return kb;
+}
+
+EXPORT void oracle_bell(int64_t rows, const int64_t* row_ptr, const int32_t* col, const double* val,
+                        int64_t bh, int64_t bw, int64_t kb, int64_t nbr_pad, int32_t* bcol, double* bval) {
+  int64_t nbr = (rows + bh - 1) / bh, be = bh * bw;
+  for (int64_t q = 0; q < kb * nbr_pad; ++q) bcol[q] = -1;
+  for (int64_t q = 0; q < kb * be * nbr_pad; ++q) bval[q] = 0.0;
+  for (int64_t I = 0; I < nbr; ++I) {
+    int64_t last = -1;
+    for (int64_t slot = 0; slot < kb; ++slot) {
+      int64_t best = -1;
+      for (int64_t i = I * bh; i < (I + 1) * bh && i < rows; ++i)
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+          int64_t J = col[k] / bw;
+          if (J > last && (best < 0 || J < best)) best = J;
+        }
+      if (best < 0) break;
+      last = best;
+      bcol[slot * nbr_pad + I] = (int32_t)best;
+      for (int64_t i = I * bh; i < (I + 1) * bh && i < rows; ++i)
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
+          if (col[k] / bw == best) {
+            int64_t e = (i - I * bh) * bw + (col[k] - best * bw);
+            bval[(slot * be + e) * nbr_pad + I] = val[k];
+          }
+    }
+  }
 }
 
 /* ---------------------------------------------------------------------------

@@ -24,15 +24,15 @@ OK, ERR_INVALID_ARG, ERR_INDEX_OUT_OF_RANGE, ERR_DUPLICATE, ERR_INFEASIBLE, ERR_
     ERR_UNSUPPORTED, ERR_CUDA, ERR_NOT_CONVERTED, ERR_NCCL, ERR_NVML = range(11)
 R32F, R64F = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
-FMT_COO, FMT_CSR, FMT_ELL, FMT_HYB, FMT_SELL = 0, 1, 2, 3, 4
-FORMATS = {"COO": FMT_COO, "CSR": FMT_CSR, "ELL": FMT_ELL, "HYB": FMT_HYB, "SELL": FMT_SELL}
+FMT_COO, FMT_CSR, FMT_ELL, FMT_HYB, FMT_SELL, FMT_BELL = 0, 1, 2, 3, 4, 5
+FORMATS = {"COO": FMT_COO, "CSR": FMT_CSR, "ELL": FMT_ELL, "HYB": FMT_HYB, "SELL": FMT_SELL, "BELL": FMT_BELL}
 FORMAT_NAMES = {v: k for k, v in FORMATS.items()}
 CSR_AUTO, CSR_SCALAR, CSR_VECTOR, CSR_MERGE = 0, 1, 2, 3
 TUNE_LAUNCH, TUNE_FORMAT, TUNE_ALL = 1, 2, 3
 OBJECTIVES = {"latency": 0, "energy": 1, "power": 2, "efficiency": 3}   # OR-ed into flags as value << 4
 (ARR_CSR_ROW_PTR, ARR_CSR_COL, ARR_CSR_VAL, ARR_COO_ROW, ARR_ELL_COL, ARR_ELL_VAL, ARR_SELL_PERM,
  ARR_SELL_SLICE_PTR, ARR_SELL_COL, ARR_SELL_VAL, ARR_HYB_ELL_COL, ARR_HYB_ELL_VAL, ARR_HYB_TAIL_ROW,
- ARR_HYB_TAIL_COL, ARR_HYB_TAIL_VAL, ARR_COO_EMPTY_ROWS) = range(16)
+ ARR_HYB_TAIL_COL, ARR_HYB_TAIL_VAL, ARR_COO_EMPTY_ROWS, ARR_BELL_COL, ARR_BELL_VAL) = range(18)
 
 
 class SpmvError(RuntimeError):
@@ -43,7 +43,8 @@ class SpmvError(RuntimeError):
 
 class FormatParams(ctypes.Structure):
     _fields_ = [("csr_alg", ctypes.c_int32), ("csr_T", ctypes.c_int32), ("sell_C", ctypes.c_int32),
-                ("sell_sigma", ctypes.c_int32), ("hyb_K", ctypes.c_int64)]
+                ("sell_sigma", ctypes.c_int32), ("hyb_K", ctypes.c_int64), ("bell_b", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class Features(ctypes.Structure):
@@ -77,7 +78,7 @@ class TuneReport(ctypes.Structure):
 class FormatInfo(ctypes.Structure):
     _fields_ = [("present", ctypes.c_int32), ("row_ptr_is64", ctypes.c_int32)] + \
                [(n, ctypes.c_int64) for n in ("K", "n_pad", "C", "sigma", "n_slices", "slots", "tail_nnz",
-                                              "n_empty_rows", "stored_bytes")]
+                                              "n_empty_rows", "stored_bytes", "block")]
 
 
 _lib = None
@@ -191,8 +192,8 @@ def spmv_create(rows, cols, row_idx, col_idx, vals, device: int = 0, stream=None
     return h
 
 
-def spmv_convert(h, fmt, csr_alg=0, csr_T=0, sell_C=0, sell_sigma=0, hyb_K=-1):
-    p = FormatParams(csr_alg, csr_T, sell_C, sell_sigma, hyb_K)
+def spmv_convert(h, fmt, csr_alg=0, csr_T=0, sell_C=0, sell_sigma=0, hyb_K=-1, bell_b=0):
+    p = FormatParams(csr_alg, csr_T, sell_C, sell_sigma, hyb_K, bell_b, 0)
     _check(lib().spmv_convert(h, fmt, ctypes.byref(p)), h)
 
 
@@ -306,9 +307,9 @@ def spmv_decision_log(h) -> list:
 
 def spmv_overheads(h):
     f = ctypes.c_double()
-    c = (ctypes.c_double * 5)()
+    c = (ctypes.c_double * 6)()
     _check(lib().spmv_overheads(h, ctypes.byref(f), c), h)
-    return f.value, {FORMAT_NAMES[i]: c[i] for i in range(5)}
+    return f.value, {FORMAT_NAMES[i]: c[i] for i in range(6)}
 
 
 def spmv_dist_partition(row_ptr, world):

@@ -154,6 +154,7 @@ spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t&
       case SPMV_FMT_SELL: r.knob = (int)h->sell_C; break;
       case SPMV_FMT_COO: r.knob = 4; break;
       case SPMV_FMT_HYB: r.knob = 4; break;
+      case SPMV_FMT_BELL: r.knob = (int)h->bell_b; break;
     }
   }
   return r;
@@ -166,6 +167,7 @@ static bool built(const spmv_matrix* h, int fmt) {
     case SPMV_FMT_ELL: return h->ell_built;
     case SPMV_FMT_SELL: return h->sell_built;
     case SPMV_FMT_HYB: return h->hyb_built;
+    case SPMV_FMT_BELL: return h->bell_built;
   }
   return false;
 }
@@ -183,12 +185,14 @@ static void dispatch(spmv_matrix* h, int fmt, const Epilogue& e, const void* x, 
     case SPMV_FMT_SELL: run_sell(h, e, x, y, L); break;
     case SPMV_FMT_COO: run_coo(h, e, x, y, L); break;
     case SPMV_FMT_HYB: run_hyb(h, e, x, y, L); break;
+    case SPMV_FMT_BELL: run_bell(h, e, x, y, L); break;
     default: fail(SPMV_ERR_INVALID_ARG, "bad format");
   }
 }
 
 static bool fused_norms(const spmv_matrix* h, int fmt) {
-  return fmt == SPMV_FMT_ELL || fmt == SPMV_FMT_SELL || (fmt == SPMV_FMT_CSR && h->csr_alg != SPMV_CSR_MERGE);
+  return fmt == SPMV_FMT_ELL || fmt == SPMV_FMT_SELL || fmt == SPMV_FMT_BELL ||
+         (fmt == SPMV_FMT_CSR && h->csr_alg != SPMV_CSR_MERGE);
 }
 
 void power_step_internal(spmv_matrix* h, const void* x, void* y, const double* sums_prev, double* sums_out,
@@ -317,8 +321,8 @@ static double objective_value(int obj, const Measured& m) {
 }
 
 static const char* fmt_name(int f) {
-  static const char* n[] = {"COO", "CSR", "ELL", "HYB", "SELL"};
-  return (f >= 0 && f < 5) ? n[f] : "?";
+  static const char* n[] = {"COO", "CSR", "ELL", "HYB", "SELL", "BELL"};
+  return (f >= 0 && f < 6) ? n[f] : "?";
 }
 
 static void log_append(spmv_matrix* h, const std::string& rec) {
@@ -343,6 +347,7 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
     case SPMV_FMT_SELL: return {(int)h->sell_C};
     case SPMV_FMT_COO: return {2, 4, 8};
     case SPMV_FMT_HYB: return {2, 4, 8};
+    case SPMV_FMT_BELL: return {(int)h->bell_b};
   }
   return {0};
 }
@@ -462,11 +467,13 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
     cands.push_back({SPMV_FMT_CSR, SPMV_CSR_MERGE, t, 0.0, "std/mean>1 or max>32*mean"});
   }
   h->csr_alg = orig_alg;
+  int64_t bell_b_try = 2;
   auto try_build = [&](int fmt, const char* why) {
     bool was = built(h, fmt);
     try {
       if (!was) {
         switch (fmt) {
+          case SPMV_FMT_BELL: build_bell(h, bell_b_try); break;
           case SPMV_FMT_ELL: build_ell(h); break;
           case SPMV_FMT_SELL: build_sell(h, h->dtype == SPMV_R64F ? 64 : 128, 1); break;
           case SPMV_FMT_HYB: build_hyb(h, -1); break;
@@ -483,11 +490,33 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
       if (!was) free_format(h, fmt);
       return;
     }
+    if (fmt == SPMV_FMT_BELL) {
+      const double slots = (double)h->bell_kb * (double)h->bell_nbr * (double)(h->bell_b * h->bell_b);
+      const double pad = slots > 0 ? 1.0 - (double)h->nnz / slots : 1.0;
+      if (pad > 0.10) {
+        os << "{\"format\":\"BELL\",\"b\":" << h->bell_b << ",\"rejected\":\"block padding " << pad
+           << " > 0.10\"},";
+        if (!was) free_format(h, fmt);
+        return;
+      }
+    }
     double t = time_variant(h, fmt, resolve_launch(h, fmt, h->launch[fmt]), ts.x, ts.y);
     cands.push_back({fmt, 0, t, format_latency(h, fmt), why});
   };
   if (f.ell_ratio >= 0.9) try_build(SPMV_FMT_ELL, "ell_ratio>=0.9");
-  if (f.ell_ratio >= 0.5 || !skewed) try_build(SPMV_FMT_SELL, "sell padding<=10%");
+  // BELL: only block-structured matrices keep block padding <= 10%
+  if (!skewed && f.mean >= 4.0) {
+    if (built(h, SPMV_FMT_BELL)) {
+      bell_b_try = h->bell_b;
+      try_build(SPMV_FMT_BELL, "block padding<=10% (pre-built)");
+    } else {
+      for (int64_t b : {int64_t(3), int64_t(2)}) {
+        bell_b_try = b;
+        try_build(SPMV_FMT_BELL, b == 2 ? "2x2 block padding<=10%" : "3x3 block padding<=10%");
+        if (built(h, SPMV_FMT_BELL)) break;  // accepted (rejections free the build)
+      }
+    }
+  }
   if (skewed) {
     try_build(SPMV_FMT_HYB, "skewed rows");
     try_build(SPMV_FMT_COO, "skewed rows");
@@ -561,6 +590,7 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
     rep->params.sell_C = (int32_t)h->sell_C;
     rep->params.sell_sigma = (int32_t)h->sell_sigma;
     rep->params.hyb_K = h->hyb_K;
+    rep->params.bell_b = (int32_t)h->bell_b;
   }
 }
 
@@ -688,6 +718,15 @@ spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format
       if (!h->sell_built || h->sell_C != C || h->sell_sigma != sigma) {
         if (h->sell_built) free_format(h, SPMV_FMT_SELL);
         build_sell(h, C, sigma);
+      }
+      break;
+    }
+    case SPMV_FMT_BELL: {
+      const int64_t b = q.bell_b ? q.bell_b : 2;
+      if (b < 2 || b > 4) fail(SPMV_ERR_UNSUPPORTED, "BELL block dimension must be 2, 3 or 4");
+      if (!h->bell_built || h->bell_b != b) {
+        if (h->bell_built) free_format(h, SPMV_FMT_BELL);
+        build_bell(h, b);
       }
       break;
     }
@@ -867,6 +906,10 @@ spmv_status_t spmv_format_info(spmv_handle_t h, spmv_format_t fmt, spmv_format_i
       o->K = h->hyb_K; o->n_pad = h->hyb_npad; o->slots = h->hyb_K * h->hyb_npad; o->tail_nnz = h->hyb_tail;
       break;
     case SPMV_FMT_COO: o->n_empty_rows = h->coo_n_empty; break;
+    case SPMV_FMT_BELL:
+      o->K = h->bell_kb; o->n_pad = h->bell_nbr_pad; o->block = h->bell_b;
+      o->slots = h->bell_kb * h->bell_nbr * h->bell_b * h->bell_b;
+      break;
     default: break;
   }
   o->stored_bytes = o->present ? format_stored_bytes(h, fmt) : 0;
@@ -896,6 +939,12 @@ spmv_status_t spmv_copy_array(spmv_handle_t h, spmv_array_t which, void* dst, in
     case SPMV_ARR_HYB_TAIL_ROW: need = h->hyb_built; src = h->hyb_trow; bytes = h->hyb_tail * 4; break;
     case SPMV_ARR_HYB_TAIL_COL: need = h->hyb_built; src = h->hyb_tcol; bytes = h->hyb_tail * 4; break;
     case SPMV_ARR_HYB_TAIL_VAL: need = h->hyb_built; src = h->hyb_tval; bytes = h->hyb_tail * vb; break;
+    case SPMV_ARR_BELL_COL: need = h->bell_built; src = h->bell_col; bytes = h->bell_kb * h->bell_nbr_pad * 4; break;
+    case SPMV_ARR_BELL_VAL:
+      need = h->bell_built;
+      src = h->bell_val;
+      bytes = h->bell_kb * h->bell_b * h->bell_b * h->bell_nbr_pad * vb;
+      break;
     default: return SPMV_ERR_INVALID_ARG;
   }
   if (!need) return SPMV_ERR_NOT_CONVERTED;

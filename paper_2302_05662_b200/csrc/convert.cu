@@ -176,6 +176,75 @@ __global__ void k_compact_empty(const RP* __restrict__ rp, const int64_t* __rest
     if (rp[i + 1] == rp[i]) out[off[i]] = (int32_t)i;
 }
 
+// ---------------------------------------------------------------- BELL
+// Block row I merges the column lists of its b rows (each sorted) and walks
+// the distinct block columns J = col / b in increasing order.
+template <class RP>
+__device__ __forceinline__ int64_t bell_next_block(const RP* rp, const int32_t* col, int64_t r0, int nr, int64_t b,
+                                                   const int64_t* pos, int64_t last) {
+  int64_t best = -1;
+  for (int r = 0; r < nr; ++r) {
+    const int64_t k = pos[r];
+    if (k < (int64_t)rp[r0 + r + 1]) {
+      const int64_t J = col[k] / b;
+      if (J > last && (best < 0 || J < best)) best = J;
+    }
+  }
+  return best;
+}
+
+template <class RP>
+__global__ void k_bell_count(const RP* __restrict__ rp, const int32_t* __restrict__ col, int64_t rows, int64_t b,
+                             int64_t nbr, unsigned long long* __restrict__ kb_max) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long local = 0;
+  for (int64_t I = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; I < nbr; I += stride) {
+    const int64_t r0 = I * b;
+    const int nr = (int)(rows - r0 < b ? rows - r0 : b);
+    int64_t pos[4];
+    for (int r = 0; r < nr; ++r) pos[r] = rp[r0 + r];
+    int64_t last = -1, count = 0;
+    for (;;) {
+      const int64_t J = bell_next_block(rp, col, r0, nr, b, pos, last);
+      if (J < 0) break;
+      for (int r = 0; r < nr; ++r)
+        while (pos[r] < (int64_t)rp[r0 + r + 1] && col[pos[r]] / b == J) ++pos[r];
+      last = J;
+      ++count;
+    }
+    local = (unsigned long long)count > local ? (unsigned long long)count : local;
+  }
+  if (local) atomicMax(kb_max, local);
+}
+
+template <class RP, class V>
+__global__ void k_bell_fill(const RP* __restrict__ rp, const int32_t* __restrict__ col, const V* __restrict__ val,
+                            int64_t rows, int64_t b, int64_t nbr_pad, int64_t kb, int32_t* __restrict__ bcol,
+                            V* __restrict__ bval) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t be = b * b;
+  for (int64_t I = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; I < nbr_pad; I += stride) {
+    const int64_t r0 = I * b;
+    const int nr = r0 < rows ? (int)(rows - r0 < b ? rows - r0 : b) : 0;
+    int64_t pos[4];
+    for (int r = 0; r < nr; ++r) pos[r] = rp[r0 + r];
+    int64_t last = -1;
+    for (int64_t s = 0; s < kb; ++s) {
+      const int64_t J = nr > 0 ? bell_next_block(rp, col, r0, nr, b, pos, last) : -1;
+      bcol[s * nbr_pad + I] = (int32_t)J;
+      for (int64_t e = 0; e < be; ++e) bval[(s * be + e) * nbr_pad + I] = V(0);
+      if (J < 0) continue;
+      for (int r = 0; r < nr; ++r)
+        while (pos[r] < (int64_t)rp[r0 + r + 1] && col[pos[r]] / b == J) {
+          const int64_t c = col[pos[r]] - J * b;
+          bval[(s * be + r * b + c) * nbr_pad + I] = val[pos[r]];
+          ++pos[r];
+        }
+      last = J;
+    }
+  }
+}
+
 int64_t read_i64(const int64_t* d, cudaStream_t s) {
   int64_t v = 0;
   CK(cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, s));
@@ -366,6 +435,38 @@ void coo_typed(spmv_matrix* h) {
   h->coo_built = true;
 }
 
+template <class RP, class V>
+void bell_typed(spmv_matrix* h, int64_t b) {
+  cudaStream_t s = h->stream;
+  const int64_t rows = h->rows, nbr = (rows + b - 1) / b, nbr_pad = (nbr + 127) / 128 * 128;
+  const RP* rp = static_cast<const RP*>(h->row_ptr);
+  Scratch sc(s);
+  unsigned long long* d_kb = sc.get<unsigned long long>(1);
+  lat_begin(h, SPMV_FMT_BELL);  // kernels + the block-width read-back
+  CK(cudaMemsetAsync(d_kb, 0, sizeof(unsigned long long), s));
+  if (nbr > 0) LAUNCH(k_bell_count<RP>, grid_for(nbr, 256), 256, 0, s, rp, h->col, rows, b, nbr, d_kb);
+  unsigned long long kbu = 0;
+  CK(cudaMemcpyAsync(&kbu, d_kb, sizeof(kbu), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t kb = (int64_t)kbu;
+  guard_bytes((double)kb * nbr_pad * (4.0 + b * b * sizeof(V)), "BELL");
+  int32_t* bcol = sc.get<int32_t>(kb * nbr_pad);
+  V* bval = sc.get<V>(kb * b * b * nbr_pad);
+  if (kb > 0)
+    LAUNCH((k_bell_fill<RP, V>), grid_for(nbr_pad, 256), 256, 0, s, rp, h->col, static_cast<const V*>(h->val), rows,
+           b, nbr_pad, kb, bcol, bval);
+  lat_end(h, SPMV_FMT_BELL);
+  sc.keep(bcol);
+  sc.keep(bval);
+  h->bell_b = b;
+  h->bell_kb = kb;
+  h->bell_nbr = nbr;
+  h->bell_nbr_pad = nbr_pad;
+  h->bell_col = bcol;
+  h->bell_val = bval;
+  h->bell_built = true;
+}
+
 template <class F>
 void dispatch(spmv_matrix* h, F&& f) {
   if (h->dtype == SPMV_R64F) {
@@ -407,6 +508,14 @@ void build_hyb(spmv_matrix* h, int64_t K) {
   });
 }
 
+void build_bell(spmv_matrix* h, int64_t b) {
+  dispatch(h, [&](auto rpt, auto vt) {
+    using RP = std::remove_pointer_t<decltype(rpt)>;
+    using V = std::remove_pointer_t<decltype(vt)>;
+    bell_typed<RP, V>(h, b);
+  });
+}
+
 void build_coo(spmv_matrix* h) {
   dispatch(h, [&](auto rpt, auto vt) {
     using RP = std::remove_pointer_t<decltype(rpt)>;
@@ -442,6 +551,10 @@ void free_format(spmv_matrix* h, int fmt) {
     case SPMV_FMT_CSR:
       F(h->row_ptr); F(h->col); F(h->val);
       break;
+    case SPMV_FMT_BELL:
+      F(h->bell_col); F(h->bell_val);
+      h->bell_built = false;
+      break;
   }
 }
 
@@ -476,6 +589,7 @@ int64_t format_stored_bytes(spmv_matrix* h, int fmt) {
     case SPMV_FMT_SELL:
       return sell_slots(h) * (4 + vb) + (h->sell_ns + 1) * 8 + (h->sell_perm ? h->rows * 4 : 0);
     case SPMV_FMT_HYB: return h->hyb_K * h->hyb_npad * (4 + vb) + h->hyb_tail * (8 + vb);
+    case SPMV_FMT_BELL: return h->bell_kb * h->bell_nbr_pad * (4 + h->bell_b * h->bell_b * vb);
   }
   return 0;
 }

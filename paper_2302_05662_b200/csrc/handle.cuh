@@ -48,6 +48,12 @@ struct spmv_matrix {
   int32_t* hyb_tcol = nullptr;
   void* hyb_tval = nullptr;
 
+  // BELL: ELL over dense b×b blocks (value planes, column-major over block rows).
+  bool bell_built = false;
+  int64_t bell_b = 2, bell_kb = 0, bell_nbr = 0, bell_nbr_pad = 0;
+  int32_t* bell_col = nullptr;
+  void* bell_val = nullptr;
+
   // CSR kernel choice.
   int csr_alg = SPMV_CSR_AUTO;
   int csr_T = 0;
@@ -60,10 +66,10 @@ struct spmv_matrix {
   int64_t hyb_auto_K = -1;  // from the feature histogram
 
   double f_latency = 0.0;
-  double c_latency[SPMV_NUM_FORMATS] = {0, 0, 0, 0, 0};
+  double c_latency[SPMV_NUM_FORMATS] = {0, 0, 0, 0, 0, 0};
   // conversion timings are recorded as CUDA events and resolved lazily (no sync in convert)
   cudaEvent_t lat_ev[SPMV_NUM_FORMATS][2] = {};
-  bool lat_pending[SPMV_NUM_FORMATS] = {false, false, false, false, false};
+  bool lat_pending[SPMV_NUM_FORMATS] = {false, false, false, false, false, false};
   bool sell_slots_pending = false;  // sell_slots still on the device (sell_sp[ns])
 
   // Scratch (grow-only) for segmented-reduction chunk records and for the
@@ -94,6 +100,7 @@ void build_coo(spmv_matrix* h);
 void build_ell(spmv_matrix* h);
 void build_sell(spmv_matrix* h, int64_t C, int64_t sigma);
 void build_hyb(spmv_matrix* h, int64_t K);
+void build_bell(spmv_matrix* h, int64_t b);
 void free_format(spmv_matrix* h, int fmt);
 int64_t format_stored_bytes(spmv_matrix* h, int fmt);
 // Conversion latency of fmt in seconds (waits for its stop event if needed).
@@ -122,6 +129,7 @@ void run_scale(spmv_matrix* h, void* y, double beta);
 void run_sell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
 void run_coo(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
 void run_hyb(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
+void run_bell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
 // Σ y_i², Σ x_own_i·y_i over rows (power mode for formats without a fused epilogue).
 void run_norms(spmv_matrix* h, const Epilogue& e, const void* x, const void* y, int64_t n);
 

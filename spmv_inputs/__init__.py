@@ -30,7 +30,7 @@ MATRIX_SEED = 0x2302056620230211
 X_SEED = 0x5EEDC0FFEE000001
 Y_SEED = 0x5EEDC0FFEE000002
 
-LAP2D, STENCIL27 = 0, 1
+LAP2D, STENCIL27, BLOCK27 = 0, 1, 100
 # Graph500 RMAT quadrant probabilities.
 RMAT_ABC = (0.57, 0.19, 0.19)
 
@@ -114,9 +114,17 @@ def rmat_thresholds(a=RMAT_ABC[0], b=RMAT_ABC[1], c=RMAT_ABC[2]):
 
 # ----------------------------------------------------------------------------- host
 
+def _stencil_n(kind, N):
+    if kind == LAP2D:
+        return N * N
+    if kind > BLOCK27:
+        return (kind - BLOCK27) * N ** 3
+    return N ** 3
+
+
 def stencil(kind: int, N: int, r0: int = 0, r1: int | None = None, random_values: bool = False,
             seed: int = MATRIX_SEED, row_base: int | None = None, dtype=np.float64) -> COO:
-    n = N * N if kind == LAP2D else N ** 3
+    n = _stencil_n(kind, N)
     r1 = n if r1 is None else r1
     row_base = r0 if row_base is None else row_base
     L = lib()
@@ -126,6 +134,11 @@ def stencil(kind: int, N: int, r0: int = 0, r1: int | None = None, random_values
     val = np.empty(nnz, np.float64)
     L.gen_stencil(kind, N, r0, r1, row_base, int(random_values), seed, _ptr(row), _ptr(col), _ptr(val))
     return COO(r1 - r0 if row_base == r0 else n, n, row, col, val.astype(dtype, copy=False))
+
+
+def block27(N: int, B: int, **kw) -> COO:
+    """27-point stencil with B unknowns per point and dense B×B blocks."""
+    return stencil(BLOCK27 + B, N, **kw)
 
 
 def lap2d(N: int, **kw) -> COO:
@@ -220,7 +233,7 @@ def stencil_device(kind: int, N: int, r0: int = 0, r1: int | None = None,
                    row_base: int | None = None, dtype=None, device="cuda") -> COO:
     import torch
     dtype = dtype or torch.float64
-    n = N * N if kind == LAP2D else N ** 3
+    n = _stencil_n(kind, N)
     r1 = n if r1 is None else r1
     row_base = r0 if row_base is None else row_base
     L = lib()
@@ -285,6 +298,9 @@ CONFIGS = {
     "c3": dict(desc="RMAT scale 23 edgefactor 16 fp32", kind="rmat", scale=23, ef=16, dtype="f32"),
     "c4": dict(desc="uniform random n=2^22, 32/row fp64", kind="uniform", n=1 << 22, k=32, dtype="f64"),
     "c5": dict(desc="3D 27-point stencil 512^3 fp64", kind="stencil27", N=512, dtype="f64"),
+    # extra workloads (not BASELINE configs): block-structured matrices for BELL
+    "b2": dict(desc="27-point stencil 100^3 x 2 dof (2x2 blocks) fp64", kind="block27", N=100, B=2, dtype="f64"),
+    "b3": dict(desc="27-point stencil 80^3 x 3 dof (3x3 blocks) fp64", kind="block27", N=80, B=3, dtype="f64"),
 }
 
 
@@ -298,6 +314,9 @@ def config_device(name: str, random_values: bool = True, device="cuda", r0: int 
         return stencil_device(LAP2D, cfg["N"], r0, r1, random_values=random_values, dtype=dt, device=device)
     if cfg["kind"] == "stencil27":
         return stencil_device(STENCIL27, cfg["N"], r0, r1, random_values=random_values, dtype=dt, device=device)
+    if cfg["kind"] == "block27":
+        return stencil_device(BLOCK27 + cfg["B"], cfg["N"], r0, r1, random_values=random_values, dtype=dt,
+                              device=device)
     if cfg["kind"] == "rmat":
         return rmat_device(cfg["scale"], cfg["ef"], dtype=dt, device=device)
     if cfg["kind"] == "uniform":
@@ -312,6 +331,8 @@ def config_host(name: str, random_values: bool = True, **override) -> COO:
         return lap2d(cfg["N"], random_values=random_values, dtype=dt)
     if cfg["kind"] == "stencil27":
         return stencil27(cfg["N"], random_values=random_values, dtype=dt)
+    if cfg["kind"] == "block27":
+        return block27(cfg["N"], cfg["B"], random_values=random_values, dtype=dt)
     if cfg["kind"] == "rmat":
         return rmat(cfg["scale"], cfg["ef"], dtype=dt)
     if cfg["kind"] == "uniform":

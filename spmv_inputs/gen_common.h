@@ -39,11 +39,19 @@ GEN_HD double gen_value(uint64_t h) {
 
 /* Stencil kinds. 5-point 2-D Laplacian on an N×N grid (row r = y·N + x) and
  * the 27-point 3-D stencil on an N³ grid (row r = (z·N + y)·N + x, HPCG
- * convention). Neighbours are emitted in increasing column order. */
-enum { GEN_LAP2D = 0, GEN_STENCIL27 = 1 };
+ * convention). Neighbours are emitted in increasing column order.
+ * GEN_BLOCK27 + B (B = 2..4): the 27-point stencil with B unknowns per grid
+ * point and dense B×B couplings (row r = p·B + a, columns q·B + b for every
+ * neighbour q of p and b < B) — a block-structured matrix (BELL's case). */
+enum { GEN_LAP2D = 0, GEN_STENCIL27 = 1, GEN_BLOCK27 = 100 };
+#define GEN_MAX_ROW 108
 
 /* Number of entries in row r of the stencil. */
 GEN_HD int gen_stencil_row_len(int kind, int64_t N, int64_t r) {
+  if (kind > GEN_BLOCK27) {
+    const int B = kind - GEN_BLOCK27;
+    return B * gen_stencil_row_len(GEN_STENCIL27, N, r / B);
+  }
   if (kind == GEN_LAP2D) {
     int64_t y = r / N, x = r % N;
     return 1 + (y > 0) + (y < N - 1) + (x > 0) + (x < N - 1);
@@ -62,6 +70,31 @@ GEN_HD int gen_stencil_row_len(int kind, int64_t N, int64_t r) {
 GEN_HD int gen_stencil_row(int kind, int64_t N, int64_t r, int random_vals, uint64_t seed,
                            int32_t* cols, double* vals) {
   int n = 0;
+  if (kind > GEN_BLOCK27) {  /* no recursion: device stacks are small */
+    const int B = kind - GEN_BLOCK27;
+    const int64_t pt = r / B;
+    const int64_t x = pt % N, y = (pt / N) % N, z = pt / (N * N);
+    for (int dz = -1; dz <= 1; ++dz) {
+      const int64_t zz = z + dz;
+      if (zz < 0 || zz >= N) continue;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int64_t yy = y + dy;
+        if (yy < 0 || yy >= N) continue;
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int64_t xx = x + dx;
+          if (xx < 0 || xx >= N) continue;
+          const int64_t q = (zz * N + yy) * N + xx;
+          for (int b = 0; b < B; ++b) {
+            const int64_t c = q * B + b;
+            cols[n] = (int32_t)c;
+            vals[n] = random_vals ? gen_value(gen_hash3(seed, (uint64_t)r, (uint64_t)c)) : (c == r ? 26.0 * B : -1.0);
+            ++n;
+          }
+        }
+      }
+    }
+    return n;
+  }
   if (kind == GEN_LAP2D) {
     int64_t y = r / N, x = r % N;
     int64_t cand[5];

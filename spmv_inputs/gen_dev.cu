@@ -26,8 +26,8 @@ __global__ void k_stencil_fill(int kind, int64_t N, int64_t r0, int64_t r1, int6
                                void* val, int random_vals, uint64_t seed) {
   int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= r1) return;
-  int32_t c[27];
-  double v[27];
+  int32_t c[GEN_MAX_ROW];
+  double v[GEN_MAX_ROW];
   int n = gen_stencil_row(kind, N, r, random_vals, seed, c, v);
   int64_t off = offsets[r - r0];
   for (int t = 0; t < n; ++t) {

@@ -192,6 +192,14 @@ def test_layouts_bit_exact(name, dtype):
             assert (fetch(h, P.ARR_HYB_TAIL_ROW, tr.shape[0], np.int32) == tr).all()
             assert (fetch(h, P.ARR_HYB_TAIL_COL, tr.shape[0], np.int32) == tc).all()
             assert (fetch(h, P.ARR_HYB_TAIL_VAL, tr.shape[0], npv).astype(np.float64) == tv).all()
+        # BELL (b = 2, 3, 4)
+        for b in (2, 3, 4):
+            P.spmv_convert(h, P.FMT_BELL, bell_b=b)
+            kb, nbr_pad, bcol, bval = oracle.bell(coo.rows, rp, C, V, b, b)
+            info = P.spmv_format_info(h, P.FMT_BELL)
+            assert (info["K"], info["n_pad"], info["block"]) == (kb, nbr_pad, b)
+            assert (fetch(h, P.ARR_BELL_COL, kb * nbr_pad, np.int32) == bcol).all()
+            assert (fetch(h, P.ARR_BELL_VAL, kb * b * b * nbr_pad, npv).astype(np.float64) == bval).all()
         # COO
         P.spmv_convert(h, P.FMT_COO)
         assert (fetch(h, P.ARR_COO_ROW, coo.nnz, np.int32) == R).all()
@@ -213,7 +221,10 @@ FMTS = [("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)),
         ("SELL-sigma", P.FMT_SELL, dict(sell_C=32, sell_sigma=256)),
         ("HYB", P.FMT_HYB, {}),
         ("HYB-K2", P.FMT_HYB, dict(hyb_K=2)),
-        ("COO", P.FMT_COO, {})]
+        ("COO", P.FMT_COO, {}),
+        ("BELL-2", P.FMT_BELL, dict(bell_b=2)),
+        ("BELL-3", P.FMT_BELL, dict(bell_b=3)),
+        ("BELL-4", P.FMT_BELL, dict(bell_b=4))]
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -238,7 +249,8 @@ def test_spmv_parity(name, dtype, fname, fmt, params):
     ("ELL", P.FMT_ELL, {}, [32, 64, 128]),
     ("SELL", P.FMT_SELL, {}, [0]),
     ("COO", P.FMT_COO, {}, [2, 4, 8]),
-    ("HYB", P.FMT_HYB, {}, [2, 4, 8])])
+    ("HYB", P.FMT_HYB, {}, [2, 4, 8]),
+    ("BELL", P.FMT_BELL, {"bell_b": 3}, [0])])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_launch_variants_parity(fname, fmt, params, knobs, dtype):
     coo = CASES["ragged_empty"]
@@ -412,6 +424,28 @@ def test_native_power_iterate_matches_stepwise(use_comm):
     finally:
         if comm is not None:
             comm.close()
+        P.spmv_destroy(h)
+
+
+@pytest.mark.parametrize("B", [2, 3])
+def test_bell_block_matrix_parity_and_selection(B):
+    """BELL's best-suited matrix (k-dof 27-point stencil): bit-exact layout,
+    SpMV parity, power steps, and the selector measures BELL as a candidate."""
+    coo = si.block27(24, B, random_values=True)   # large enough that boundary (Kb) padding < 10%
+    h = create(coo)
+    try:
+        ref = oracle_csr(coo)
+        P.spmv_convert(h, P.FMT_BELL, bell_b=B)
+        info = P.spmv_format_info(h, P.FMT_BELL)
+        bcol = fetch(h, P.ARR_BELL_COL, info["K"] * info["n_pad"], np.int32)
+        assert (bcol >= 0).sum() * B * B == coo.nnz   # dense blocks: no padding inside stored blocks
+        for a, b in AB:
+            check_y(h, coo, "f64", P.FMT_BELL, a, b, ref)
+        rep = P.spmv_tune(h, P.TUNE_FORMAT, expected_iterations=10 ** 6)
+        sel = [r for r in P.spmv_decision_log(h) if r["kind"] == "format_select"][-1]
+        assert any(c["format"] == "BELL" and "t_s" in c for c in sel["candidates"]), sel["candidates"]
+        check_y(h, coo, "f64", rep.format, 2.5, -0.5, ref)
+    finally:
         P.spmv_destroy(h)
 
 

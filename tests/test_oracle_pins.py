@@ -467,3 +467,64 @@ def test_partition_invariants():
         per = np.diff(rp[b])
         assert per.sum() == nnz
         assert (np.abs(per - nnz / P) <= np.diff(rp).max() + 1).all()
+
+
+# ------------------------------------------------------------------ O13 BELL
+
+def reconstruct_bell(kb, nbr_pad, bcol, bval, b, rows, cols):
+    D = [[0.0] * cols for _ in range(rows)]
+    for k in range(kb):
+        for I in range(nbr_pad):
+            J = bcol[k * nbr_pad + I]
+            for r in range(b):
+                for c in range(b):
+                    v = bval[(k * b * b + r * b + c) * nbr_pad + I]
+                    if J < 0:
+                        assert v == 0.0
+                        continue
+                    i, j = I * b + r, J * b + c
+                    if i < rows and j < cols:
+                        D[i][j] += v
+                    else:
+                        assert v == 0.0
+    return D
+
+
+def test_bell_spec_examples():
+    # 4x4 with nonzeros confined to the top-left 2x2 -> 1 stored block
+    rp = np.array([0, 2, 4, 4, 4]); C = np.array([0, 1, 0, 1]); V = np.array([1.0, 2, 3, 4])
+    kb, nbr_pad, bcol, bval = oracle.bell(4, rp, C, V, 2, 2)
+    assert kb == 1 and (bcol >= 0).sum() == 1 and bcol[0] == 0
+    # 4x4 dense -> 4 stored blocks, each fully dense
+    rpd = np.array([0, 4, 8, 12, 16]); Cd = np.tile(np.arange(4), 4); Vd = np.arange(1.0, 17.0)
+    kb, nbr_pad, bcol, bval = oracle.bell(4, rpd, Cd, Vd, 2, 2)
+    assert kb == 2 and (bcol >= 0).sum() == 4
+    assert reconstruct_bell(kb, nbr_pad, bcol, bval, 2, 4, 4) == [[float(4 * i + j + 1) for j in range(4)]
+                                                                  for i in range(4)]
+
+
+@pytest.mark.parametrize("b", [2, 3, 4])
+@pytest.mark.parametrize("seed", range(4))
+def test_bell_bruteforce_and_reconstruct(b, seed):
+    rng = np.random.default_rng(seed)
+    rows, cols = int(rng.integers(1, 40)), int(rng.integers(1, 40))   # ragged edges
+    coo = si.random_coo(rows, cols, int(rng.integers(0, rows * cols // 2 + 1)), seed)
+    rp, C, V = build(coo)
+    kb, nbr_pad, bcol, bval = oracle.bell(rows, rp, C, V, b, b)
+    blocks = {}
+    for i, j in zip(coo.row.tolist(), coo.col.tolist()):
+        blocks.setdefault(i // b, set()).add(j // b)
+    assert kb == max((len(v) for v in blocks.values()), default=0)
+    for I in range((rows + b - 1) // b):
+        got = [int(bcol[k * nbr_pad + I]) for k in range(kb) if bcol[k * nbr_pad + I] >= 0]
+        assert got == sorted(blocks.get(I, set()))                        # increasing block columns
+    assert reconstruct_bell(kb, nbr_pad, bcol, bval, b, rows, cols) == dense_of(rows, cols, coo.row, coo.col, coo.val)
+
+
+def test_block27_generator_block_structure():
+    # every stored 3x3 block of the 3-dof 27-point stencil is dense -> zero block padding
+    coo = si.block27(5, 3)
+    rp, C, V = build(coo)
+    kb, nbr_pad, bcol, bval = oracle.bell(coo.rows, rp, C, V, 3, 3)
+    nblocks = int((bcol >= 0).sum())
+    assert nblocks * 9 == coo.nnz and kb == 27

@@ -29,7 +29,9 @@ VARIANTS = [("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)),
             ("SELL", P.FMT_SELL, {}),
             ("SELL-sigma", P.FMT_SELL, dict(sell_sigma=-1)),
             ("HYB", P.FMT_HYB, {}),
-            ("COO", P.FMT_COO, {})]
+            ("COO", P.FMT_COO, {}),
+            ("BELL-2", P.FMT_BELL, dict(bell_b=2)),
+            ("BELL-3", P.FMT_BELL, dict(bell_b=3))]
 
 
 def time_kernel(h, fmt, x, y, reps=None):
@@ -75,6 +77,8 @@ def main():
         for name, fmt, params in VARIANTS:
             if args.formats and name not in args.formats.split(","):
                 continue
+            if name.startswith("BELL") and (feats["std"] > feats["mean"] or feats["mean"] < 4):
+                continue  # block formats only make sense on block-structured matrices
             params = dict(params)
             if params.get("sell_sigma") == -1:
                 if feats["std"] <= 0.5 * feats["mean"]:
@@ -103,7 +107,8 @@ def main():
                         "frac_8TBs": round(alg / t / 1e9 / 8000, 4), "useful_GBps": round(csr_min / t / 1e9, 1),
                         "GFLOPs": round(2 * feats["nnz"] / t / 1e9, 1),
                         "c_latency_ms": round(c_lat[P.FORMAT_NAMES[fmt]] * 1e3, 3),
-                        "padding": round(1 - feats["nnz"] / info["slots"], 4) if info["slots"] else None})
+                        "padding": (round(1 - feats["nnz"] / info["slots"], 4)
+                                    if info["slots"] and fmt in (P.FMT_ELL, P.FMT_SELL, P.FMT_BELL) else None)})
             results.append(rec)
             print(json.dumps(rec), flush=True)
             if fmt not in (P.FMT_CSR,):
