@@ -67,12 +67,17 @@ typedef enum {
 #define SPMV_NUM_FORMATS 6
 
 /* CSR kernel algorithms: scalar (thread per row), vector (T lanes per row,
- * the "coordination among threads within a warp" of P:159), merge-path. */
+ * the "coordination among threads within a warp" of P:159), merge-path, and
+ * stream (a block stages the CSR segment of its rows in shared memory with
+ * coalesced loads, then a thread per row gathers x — consecutive rows gather
+ * together, as in ELL, without ELL's padding; blocks whose segment does not
+ * fit fall back to warp-per-row). */
 typedef enum {
   SPMV_CSR_AUTO = 0,
   SPMV_CSR_SCALAR = 1,
   SPMV_CSR_VECTOR = 2,
-  SPMV_CSR_MERGE = 3
+  SPMV_CSR_MERGE = 3,
+  SPMV_CSR_STREAM = 4
 } spmv_csr_alg_t;
 
 /* Format parameters (NULL = defaults). */

@@ -27,7 +27,7 @@ MEM_HOST, MEM_DEVICE = 0, 1
 FMT_COO, FMT_CSR, FMT_ELL, FMT_HYB, FMT_SELL, FMT_BELL = 0, 1, 2, 3, 4, 5
 FORMATS = {"COO": FMT_COO, "CSR": FMT_CSR, "ELL": FMT_ELL, "HYB": FMT_HYB, "SELL": FMT_SELL, "BELL": FMT_BELL}
 FORMAT_NAMES = {v: k for k, v in FORMATS.items()}
-CSR_AUTO, CSR_SCALAR, CSR_VECTOR, CSR_MERGE = 0, 1, 2, 3
+CSR_AUTO, CSR_SCALAR, CSR_VECTOR, CSR_MERGE, CSR_STREAM = 0, 1, 2, 3, 4
 TUNE_LAUNCH, TUNE_FORMAT, TUNE_ALL = 1, 2, 3
 OBJECTIVES = {"latency": 0, "energy": 1, "power": 2, "efficiency": 3}   # OR-ed into flags as value << 4
 (ARR_CSR_ROW_PTR, ARR_CSR_COL, ARR_CSR_VAL, ARR_COO_ROW, ARR_ELL_COL, ARR_ELL_VAL, ARR_SELL_PERM,

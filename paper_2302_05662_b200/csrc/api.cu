@@ -58,7 +58,7 @@ void dfree(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
 }
 
-int64_t persistent_grid(const void* func, int block, int64_t needed_blocks) {
+int64_t persistent_grid(const void* func, int block, int64_t needed_blocks, size_t dyn_smem) {
   static std::unordered_map<uint64_t, int> occ;
   static int sms = 0;
   int per_sm;
@@ -69,11 +69,11 @@ int64_t persistent_grid(const void* func, int block, int64_t needed_blocks) {
       CK(cudaGetDevice(&dev));
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    const uint64_t key = (uint64_t)(uintptr_t)func ^ ((uint64_t)block << 48);
+    const uint64_t key = (uint64_t)(uintptr_t)func ^ ((uint64_t)block << 48) ^ ((uint64_t)dyn_smem << 20);
     auto it = occ.find(key);
     if (it == occ.end()) {
       int nb = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, func, block, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, func, block, dyn_smem));
       it = occ.emplace(key, std::max(nb, 1)).first;
     }
     per_sm = it->second;
@@ -147,6 +147,7 @@ spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t&
     switch (fmt) {
       case SPMV_FMT_CSR:
         if (h->csr_alg == SPMV_CSR_MERGE) r.knob = 8;
+        else if (h->csr_alg == SPMV_CSR_STREAM) r.knob = 32;
         else if (h->csr_alg == SPMV_CSR_SCALAR) r.knob = 1;
         else r.knob = csr_default_lanes(h);
         break;
@@ -192,7 +193,7 @@ static void dispatch(spmv_matrix* h, int fmt, const Epilogue& e, const void* x, 
 
 static bool fused_norms(const spmv_matrix* h, int fmt) {
   return fmt == SPMV_FMT_ELL || fmt == SPMV_FMT_SELL || fmt == SPMV_FMT_BELL ||
-         (fmt == SPMV_FMT_CSR && h->csr_alg != SPMV_CSR_MERGE);
+         (fmt == SPMV_FMT_CSR && h->csr_alg != SPMV_CSR_MERGE);  // vector, scalar and stream fuse the norms
 }
 
 void power_step_internal(spmv_matrix* h, const void* x, void* y, const double* sums_prev, double* sums_out,
@@ -335,6 +336,7 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
   switch (fmt) {
     case SPMV_FMT_CSR:
       if (h->csr_alg == SPMV_CSR_MERGE) return {4, 8, 16};
+      if (h->csr_alg == SPMV_CSR_STREAM) return {16, 32, 64};
       {
         int t = csr_default_lanes(h);
         std::vector<int> v{t};
@@ -363,7 +365,14 @@ static void tune_launch(spmv_matrix* h, int fmt, TuneScratch& ts, spmv_tune_repo
   static const int regs[] = {32, 64, 128, 255};
   static const int carve[] = {0, 25, 50, 100};
   spmv_launch_t best = resolve_launch(h, fmt, h->launch[fmt]);
-  double tbest = time_variant(h, fmt, best, ts.x, ts.y);
+  double tbest;
+  try {
+    tbest = time_variant(h, fmt, best, ts.x, ts.y);
+  } catch (const SpmvError&) {  // the current variant is invalid for this kernel: start from defaults
+    cudaGetLastError();
+    best = resolve_launch(h, fmt, spmv_launch_t{0, 0, -1, 0});
+    tbest = time_variant(h, fmt, best, ts.x, ts.y);
+  }
   std::vector<std::pair<double, spmv_launch_t>> all{{tbest, best}};
   int n = 1;
   std::ostringstream os;
@@ -697,9 +706,10 @@ spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format
   if (p) q = *p;
   switch (fmt) {
     case SPMV_FMT_CSR:
-      if (q.csr_alg < 0 || q.csr_alg > SPMV_CSR_MERGE) fail(SPMV_ERR_INVALID_ARG, "bad csr_alg");
+      if (q.csr_alg < 0 || q.csr_alg > SPMV_CSR_STREAM) fail(SPMV_ERR_INVALID_ARG, "bad csr_alg");
       if (q.csr_T != 0 && (q.csr_T < 1 || q.csr_T > 32 || (q.csr_T & (q.csr_T - 1))))
         fail(SPMV_ERR_INVALID_ARG, "csr_T must be a power of two in [1, 32]");
+      if (h->csr_alg != q.csr_alg) h->launch[SPMV_FMT_CSR] = spmv_launch_t{0, 0, -1, 0};  // other kernel
       h->csr_alg = q.csr_alg;
       h->csr_T = q.csr_T;
       h->launch[SPMV_FMT_CSR].knob = 0;

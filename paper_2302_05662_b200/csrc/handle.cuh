@@ -160,7 +160,7 @@ void* ensure_fixup_scratch(spmv_matrix* h, size_t bytes);
 // Resolve a launch variant to the defaults of its kernel.
 spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t& L);
 // Grid for a persistent (grid-stride) kernel: min(needed, SMs × resident blocks per SM).
-int64_t persistent_grid(const void* func, int block, int64_t needed_blocks);
+int64_t persistent_grid(const void* func, int block, int64_t needed_blocks, size_t dyn_smem = 0);
 // Opt in to `bytes` of dynamic shared memory for func (cached).
 void set_max_dynamic_smem(const void* func, size_t bytes);
 // Carveout attribute (cached per function pointer).

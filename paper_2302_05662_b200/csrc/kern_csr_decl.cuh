@@ -25,6 +25,13 @@ template <class T, class RP, int LANES>
 CsrFn csr_vector_fn(int bi, int ri);
 template <class T, class RP, int IPT>
 CsrFn csr_merge_fn(int bi, int ri);
+template <class T, class RP, int EPT>
+CsrFn csr_stream_fn(int bi, int ri);
+// Dynamic shared memory of a CSR-stream block: B rows × EPT entries of (col, value).
+template <class T>
+constexpr size_t stream_smem_bytes(int block, int ept) {
+  return (size_t)block * (size_t)ept * (4 + sizeof(T));
+}
 // Dynamic shared memory of a merge-path block of `block` threads.
 // Per-warp slice: ITEMS fp64 products then ITEMS+1 int32 row ends, padded to 16 B.
 __host__ __device__ constexpr size_t merge_warp_smem(int ipt) {

@@ -15,6 +15,30 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
   p.e = e;
   const int bi = block_index(L.block), ri = reg_index(L.maxreg);
   const bool merge = h->csr_alg == SPMV_CSR_MERGE;
+  if (h->csr_alg == SPMV_CSR_STREAM) {
+    const int ept = L.knob;
+    const void* fn;
+    switch (ept) {
+      case 16: fn = (const void*)kern::csr_stream_fn<T, RP, 16>(bi, ri); break;
+      case 32: fn = (const void*)kern::csr_stream_fn<T, RP, 32>(bi, ri); break;
+      case 64: fn = (const void*)kern::csr_stream_fn<T, RP, 64>(bi, ri); break;
+      default: fail(SPMV_ERR_INVALID_ARG, "CSR-stream entries per row slot must be 16, 32 or 64");
+    }
+    const size_t smem = kern::stream_smem_bytes<T>(L.block, ept);
+    if (smem > 227 * 1024) fail(SPMV_ERR_UNSUPPORTED, "CSR-stream block × entries exceeds shared memory");
+    set_carveout(fn, L.carveout_pct);
+    set_max_dynamic_smem(fn, smem);
+    const int64_t grid = persistent_grid(fn, L.block, (h->rows + L.block - 1) / L.block, smem);
+    if (grid <= 0) return;
+    if (e.mode == 1) {
+      ensure_pi_scratch(h, (size_t)grid);
+      p.e.partials = h->pi_partials;
+      p.e.counter = h->pi_counter;
+    }
+    void* args[] = {&p};
+    launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, smem, h->stream);
+    return;
+  }
   if (!merge) {
     const int lanes = L.knob;
     const void* fn;

@@ -25,6 +25,7 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
 
 VARIANTS = [("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)),
             ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE)),
+            ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM)),
             ("ELL", P.FMT_ELL, {}),
             ("SELL", P.FMT_SELL, {}),
             ("SELL-sigma", P.FMT_SELL, dict(sell_sigma=-1)),

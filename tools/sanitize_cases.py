@@ -17,7 +17,8 @@ from gpu_cases import corpus  # noqa: E402
 
 FMTS = [(P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)), (P.FMT_CSR, dict(csr_alg=P.CSR_SCALAR)),
         (P.FMT_CSR, dict(csr_alg=P.CSR_MERGE)), (P.FMT_ELL, {}), (P.FMT_SELL, {}),
-        (P.FMT_SELL, dict(sell_C=32, sell_sigma=64)), (P.FMT_HYB, {}), (P.FMT_COO, {})]
+        (P.FMT_SELL, dict(sell_C=32, sell_sigma=64)), (P.FMT_HYB, {}), (P.FMT_COO, {}),
+        (P.FMT_CSR, dict(csr_alg=P.CSR_STREAM)), (P.FMT_BELL, dict(bell_b=2)), (P.FMT_BELL, dict(bell_b=3))]
 
 
 def main():
