@@ -57,16 +57,11 @@ __global__ void k_seg_fixup_long(const ChunkRec* __restrict__ recs, int64_t n, E
     for (int64_t q0 = c + 1; q0 < n; q0 += 32) {
       const int64_t q = q0 + lane;
       const bool valid = q < n;
-      double hd = 0.0;
       bool mid = false;
-      if (valid) {
-        const ChunkRec rq = recs[q];
-        hd = rq.head;
-        mid = rec_mid(rq);
-      }
+      if (valid) mid = rec_mid(recs[q]);  // flags are always written; head only when cont_in
       const unsigned endm = __ballot_sync(0xffffffffu, valid && !mid);
       const int last = endm ? __ffs(endm) - 1 : 31;
-      if (valid && lane <= last) part += hd;
+      if (valid && lane <= last) part += recs[q].head;
       if (endm || !__ballot_sync(0xffffffffu, valid)) break;
     }
     part = warp_sum(part);
