@@ -377,22 +377,39 @@ def run_ours(args):
             torch.cuda.synchronize()
             phases.setdefault(name, []).append(time.perf_counter())
 
-    def one_step(coo_in, host=False):
+    ev_names = ["create", "features", "convert", "power", "destroy"]
+
+    def ev_mark(i):
+        # CUDA events at phase boundaries on the stream (no synchronisation)
+        if state.get("phase_events") is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            state["phase_events"][-1].append(e)
+
+    def one_step(coo_in, want_info=False):
+        if state.get("phase_events") is not None:
+            state["phase_events"].append([])
         mark("0_start")
+        ev_mark(0)
         h = P.spmv_create(coo_in.rows, coo_in.cols, coo_in.row, coo_in.col, coo_in.val)
         state["h"] = h
         mark("1_create")
+        ev_mark(1)
         P.spmv_features(h)
         mark("2_features")
+        ev_mark(2)
         P.spmv_convert(h, fmt, **params)
         P.spmv_set_launch(h, fmt, *launch)
-        info = P.spmv_format_info(h, fmt)
+        info = P.spmv_format_info(h, fmt) if want_info else None  # (reads sizes back: not in the timed loop)
         mark("3_convert")
+        ev_mark(3)
         power(h, x0)
         mark("4_power")
+        ev_mark(4)
         P.spmv_destroy(h)
         state["h"] = None
         mark("5_destroy")
+        ev_mark(5)
         return info
 
     def barrier():
@@ -401,14 +418,18 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        info = one_step(coo)
+    info = None
+    for w in range(args.warmup):
+        info = one_step(coo, want_info=(w == args.warmup - 1)) or info
+    if info is None:
+        info = one_step(coo, want_info=True)
     barrier()
 
     clocks = ClockSampler(local) if not os.environ.get("BENCH_NO_CLOCKS") else None
     energy = Energy(local)
     state["time_kernels"] = not os.environ.get("BENCH_NO_KEVENTS")
     state["kms"] = []
+    state["phase_events"] = []
     l0 = P.launch_count()
     e_j0 = energy.read_j()
     t_start = torch.cuda.Event(enable_timing=True)
@@ -417,7 +438,7 @@ def run_ours(args):
     state["host_t0"] = time.perf_counter()
     t_start.record(stream)
     for _ in range(args.steps):
-        info = one_step(coo)
+        one_step(coo)
     t_end.record(stream)
     barrier()
     e_j1 = energy.read_j()
@@ -436,6 +457,13 @@ def run_ours(args):
                       "median_ms": round(statistics.median(d) * 1e3, 3)}
         print("PHASES", json.dumps(rep), file=sys.stderr, flush=True)
     kernel_ms = list(state["kms"])
+    phase_ms = {}
+    pe = state.pop("phase_events", None) or []
+    state["phase_events"] = None
+    for i, name in enumerate(ev_names):
+        vals = [st[i].elapsed_time(st[i + 1]) for st in pe if len(st) > i + 1]
+        if vals:
+            phase_ms[name] = round(statistics.median(vals), 4)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
@@ -543,6 +571,7 @@ def run_ours(args):
                          "kernel_share_of_step": round(kernel_share, 4) if kernel_share else None,
                          "peak_source": peak_kind, "frac_of_8TBs": round(achieved / 8000.0, 4)},
             "hbm_gbs": round(achieved, 1),
+            "step_phases_ms": phase_ms,
             "mflops_per_w": round(mflops_w, 1) if mflops_w else None,
             "cpu_baseline": cpu,
             "e2e": e2e,
