@@ -262,8 +262,9 @@ spmv_status_t spmv_norm2(spmv_handle_t h, const void* x, int64_t n, double* sums
 /* The whole E-step power iteration on the handle's stream (no host round
  * trips): buf0 <- x0 (n_full values, may alias buf0), S_0 = Σ over ranks of
  * ||own rows of buf0||², then per step k: one spmv_power_step into the next
- * buffer (comm = NULL) or into chunk_buf followed by ncclAllReduce(sums[k+1])
- * and ncclAllGather(chunk_buf -> next buffer, chunk values per rank).
+ * buffer — at this rank's chunk (rank·chunk) when comm != NULL, followed by
+ * the all-reduce of sums[k+1] and an in-place all-gather of the chunks
+ * (chunk values per rank). chunk_buf is unused (may be NULL).
  * sums: device double[(steps+1)·2] (row k = [S_k, D_k]); lambda_k =
  * D_k / sqrt(S_{k-1}). buf0/buf1: device, n_full values (n_full = rows for a
  * single rank, world·chunk in the padded multi-GPU layout). kernel_ms: host
@@ -275,6 +276,67 @@ spmv_status_t spmv_norm2(spmv_handle_t h, const void* x, int64_t n, double* sums
 spmv_status_t spmv_power_iterate(spmv_handle_t h, const void* x0, void* buf0, void* buf1, int64_t n_full,
                                  int64_t steps, double* sums, void* comm, int64_t chunk, void* chunk_buf,
                                  float* kernel_ms, float* loop_ms, int* final_buf);
+
+/* ---------------------------------------------------------------- distributed plan
+ * Interior/halo overlap and halo exchange (SURVEY.md §8(e) (i)–(iv), §8(f) f4).
+ * spmv_dist_plan_create splits the rank's slab h (rows = local rows, columns
+ * in the padded layout: rank r owns positions [r·chunk, r·chunk + rows_r))
+ * into three row blocks, each a new handle converted to h's active format,
+ * parameters and launch variant:
+ *   part 0 interior [h0, h1): every column inside the own chunk;
+ *   part 1 lo halo  [0, h0):  h0 = 1 + the last row with a column below it;
+ *   part 2 hi halo  [h1, n):  h1 = the first row with a column above it.
+ * Exact for any matrix (a general graph may have an empty interior). h may
+ * be destroyed after the call (the plan owns copies). comm = NULL: one rank,
+ * a single interior part, no exchange (chunk ignored).
+ * flags: SPMV_PLAN_OVERLAP — the interior SpMV of step k waits only for the
+ *   all-reduce of step k−1 and overlaps the exchange of z_{k−1} on a second
+ *   stream; the halo SpMVs wait for the exchange. Without it every kernel of
+ *   the step waits for the exchange.
+ * SPMV_PLAN_HALO — exchange only the remote entries the halo rows reference
+ *   (NCCL send/recv, lists built here with the communicator) instead of the
+ *   all-gather of whole chunks; kept only if every rank then receives less
+ *   than half of what the all-gather moves (collective decision).
+ * Collective: every rank of comm must call it. Synchronous. */
+#define SPMV_PLAN_OVERLAP 1u
+#define SPMV_PLAN_HALO 2u
+typedef struct spmv_dist_plan* spmv_dist_plan_t;
+typedef struct {
+  int32_t rank, world, overlap, halo;   /* halo: 1 = list exchange in use, 0 = all-gather */
+  int64_t rows, chunk, h0, h1;
+  int64_t part_rows[3], part_nnz[3];
+  int64_t recv_elems, send_elems;       /* per step, per rank */
+  int64_t recv_bytes_per_step;
+  int32_t direct_recv, direct_send;     /* halo segments move without pack/unpack kernels */
+} spmv_dist_plan_info_t;
+spmv_status_t spmv_dist_plan_create(spmv_dist_plan_t* out, spmv_handle_t h, void* comm, int64_t chunk,
+                                    uint32_t flags);
+spmv_status_t spmv_dist_plan_info(spmv_dist_plan_t plan, spmv_dist_plan_info_t* out);
+/* Borrowed handle of part p (0..2) or NULL when that block is empty; it may
+ * be re-converted or re-tuned (the plan uses its active format). */
+spmv_status_t spmv_dist_plan_part(spmv_dist_plan_t plan, int part, spmv_handle_t* out);
+/* E power steps with the plan's schedule (same mathematics and sums layout
+ * as spmv_power_iterate; buf0/buf1 hold world·chunk values; in halo mode only
+ * the own chunk and the received halo entries of the final buffer are
+ * current). loop_ms (optional): CUDA-event time of the loop on the compute
+ * stream; interior_ms (optional, host float[steps]): each step's interior
+ * kernel time. Collective. */
+spmv_status_t spmv_dist_plan_iterate(spmv_dist_plan_t plan, const void* x0, void* buf0, void* buf1,
+                                     int64_t steps, double* sums, float* loop_ms, float* interior_ms,
+                                     int* final_buf);
+spmv_status_t spmv_dist_plan_destroy(spmv_dist_plan_t plan); /* NULL is a no-op */
+
+/* W communicators of ONE process (rank r on devices[r]; devices may repeat):
+ * collectives are stream-ordered device copies plus a host barrier, so W host
+ * threads — one per rank, each calling the collective entry points with its
+ * own communicator — run exactly the multi-rank schedule of the NCCL path.
+ * comms: host void*[world], each released with spmv_dist_destroy. A rank that
+ * fails releases the others from the barrier (they return SPMV_ERR_NCCL). */
+spmv_status_t spmv_dist_local_group(int world, const int* devices, void** comms);
+
+/* Rows [row_begin, row_end) of h's CSR as a new handle (same columns, dtype,
+ * device and stream; active format CSR). Copies the slice. */
+spmv_status_t spmv_create_row_slice(spmv_handle_t* out, spmv_handle_t h, int64_t row_begin, int64_t row_end);
 
 /* ---------------------------------------------------------------- introspection */
 spmv_status_t spmv_format_info(spmv_handle_t h, spmv_format_t fmt, spmv_format_info_t* out);

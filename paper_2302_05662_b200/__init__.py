@@ -81,6 +81,23 @@ class FormatInfo(ctypes.Structure):
                                               "n_empty_rows", "stored_bytes", "block")]
 
 
+class PlanInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("rank", "world", "overlap", "halo")] + \
+               [(n, ctypes.c_int64) for n in ("rows", "chunk", "h0", "h1")] + \
+               [("part_rows", ctypes.c_int64 * 3), ("part_nnz", ctypes.c_int64 * 3)] + \
+               [(n, ctypes.c_int64) for n in ("recv_elems", "send_elems", "recv_bytes_per_step")] + \
+               [(n, ctypes.c_int32) for n in ("direct_recv", "direct_send")]
+
+    def as_dict(self):
+        d = {}
+        for f in self._fields_:
+            v = getattr(self, f[0])
+            d[f[0]] = list(v) if f[0] in ("part_rows", "part_nnz") else v
+        return d
+
+
+PLAN_OVERLAP, PLAN_HALO = 1, 2
+
 _lib = None
 
 
@@ -120,6 +137,14 @@ def lib():
         "spmv_trim_pool": ([i32], i32),
         "spmv_power_iterate": ([H, vp, vp, vp, i64, i64, vp, vp, i64, vp, ctypes.POINTER(ctypes.c_float),
                                 ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int)], i32),
+        "spmv_dist_plan_create": ([ctypes.POINTER(vp), H, vp, i64, u32], i32),
+        "spmv_dist_plan_info": ([vp, ctypes.POINTER(PlanInfo)], i32),
+        "spmv_dist_plan_part": ([vp, i32, ctypes.POINTER(H)], i32),
+        "spmv_dist_plan_iterate": ([vp, vp, vp, vp, i64, vp, ctypes.POINTER(ctypes.c_float),
+                                    ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int)], i32),
+        "spmv_dist_plan_destroy": ([vp], i32),
+        "spmv_dist_local_group": ([i32, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp)], i32),
+        "spmv_create_row_slice": ([ctypes.POINTER(H), H, i64, i64], i32),
         "spmv_dist_unique_id": ([ctypes.c_char_p], i32),
         "spmv_dist_init": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, i32, i32], i32),
         "spmv_dist_destroy": ([vp], i32),
@@ -254,6 +279,55 @@ def spmv_power_iterate(h, x0, buf0, buf1, steps, sums, comm=None, chunk=0, chunk
                                     _ptr(sums), comm, int(chunk), _ptr(chunk_buf), km,
                                     ctypes.byref(lm) if time_loop else None, ctypes.byref(fb)), h)
     return fb.value, (list(km)[:int(steps)] if km is not None else None), (lm.value if time_loop else None)
+
+
+def spmv_create_row_slice(h, row_begin, row_end):
+    out = ctypes.c_void_p()
+    _check(lib().spmv_create_row_slice(ctypes.byref(out), h, int(row_begin), int(row_end)), h)
+    return out
+
+
+def spmv_dist_local_group(world: int, devices=None):
+    """`world` in-process communicators (rank r on devices[r]); drive each
+    rank from its own host thread (ctypes releases the GIL during calls)."""
+    devs = list(devices) if devices is not None else [0] * world
+    arr = (ctypes.c_int * world)(*devs)
+    out = (ctypes.c_void_p * world)()
+    _check(lib().spmv_dist_local_group(int(world), arr, out))
+    return [ctypes.c_void_p(out[r]) for r in range(world)]
+
+
+def spmv_dist_plan_create(h, comm, chunk, flags=PLAN_OVERLAP):
+    out = ctypes.c_void_p()
+    _check(lib().spmv_dist_plan_create(ctypes.byref(out), h, comm, int(chunk), int(flags)), h)
+    return out
+
+
+def spmv_dist_plan_info(plan) -> dict:
+    o = PlanInfo()
+    _check(lib().spmv_dist_plan_info(plan, ctypes.byref(o)))
+    return o.as_dict()
+
+
+def spmv_dist_plan_part(plan, part):
+    out = ctypes.c_void_p()
+    _check(lib().spmv_dist_plan_part(plan, int(part), ctypes.byref(out)))
+    return out if out.value else None
+
+
+def spmv_dist_plan_iterate(plan, x0, buf0, buf1, steps, sums, time_loop=False, time_interior=False):
+    """Returns (final_buf_index, loop_ms or None, interior kernel ms list or None)."""
+    lm = ctypes.c_float(0.0)
+    im = (ctypes.c_float * max(int(steps), 1))() if time_interior else None
+    fb = ctypes.c_int(0)
+    _check(lib().spmv_dist_plan_iterate(plan, _ptr(x0), _ptr(buf0), _ptr(buf1), int(steps), _ptr(sums),
+                                        ctypes.byref(lm) if time_loop else None, im, ctypes.byref(fb)))
+    return fb.value, (lm.value if time_loop else None), (list(im)[:int(steps)] if im is not None else None)
+
+
+def spmv_dist_plan_destroy(plan):
+    if plan is not None:
+        _check(lib().spmv_dist_plan_destroy(plan))
 
 
 def spmv_dist_unique_id() -> bytes:

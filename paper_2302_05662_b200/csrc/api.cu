@@ -13,11 +13,13 @@
 #include <unordered_map>
 #include <vector>
 
+#include "dist.cuh"
 #include "spmv_common.cuh"
 
 namespace spmv {
 
 std::atomic<uint64_t> g_launches{0};
+thread_local int g_sm_reserve = 0;
 
 namespace {
 std::mutex g_mu;
@@ -78,7 +80,7 @@ int64_t persistent_grid(const void* func, int block, int64_t needed_blocks, size
     }
     per_sm = it->second;
   }
-  const int64_t cap = (int64_t)sms * per_sm;
+  const int64_t cap = (int64_t)std::max(sms - std::max(g_sm_reserve, 0), 1) * per_sm;
   return needed_blocks < cap ? needed_blocks : cap;
 }
 
@@ -197,13 +199,15 @@ static bool fused_norms(const spmv_matrix* h, int fmt) {
 }
 
 void power_step_internal(spmv_matrix* h, const void* x, void* y, const double* sums_prev, double* sums_out,
-                         int64_t row_offset) {
+                         int64_t row_offset, int sums_parts, bool pdl) {
   const int fmt = h->active;
   Epilogue e;
   e.mode = 1;
   e.sums_prev = sums_prev;
   e.sums_out = sums_out;
   e.row_offset = row_offset;
+  e.sums_parts = sums_parts;
+  e.pdl = pdl;
   if (h->rows == 0) {
     CK(cudaMemsetAsync(sums_out, 0, 2 * sizeof(double), h->stream));
     return;
@@ -872,6 +876,64 @@ spmv_status_t spmv_power_iterate(spmv_handle_t h, const void* x0, void* buf0, vo
   API_TRY
   DeviceGuard g(h->device);
   power_iterate(h, x0, buf0, buf1, n_full, steps, sums, comm, chunk, chunk_buf, kernel_ms, loop_ms, final_buf);
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_dist_plan_create(spmv_dist_plan_t* out, spmv_handle_t h, void* comm, int64_t chunk,
+                                    uint32_t flags) {
+  if (!out) return SPMV_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!h || (comm && chunk < 1) || (flags & ~(SPMV_PLAN_OVERLAP | SPMV_PLAN_HALO))) return SPMV_ERR_INVALID_ARG;
+  if (!built(h, h->active)) return SPMV_ERR_NOT_CONVERTED;
+  API_TRY
+  DeviceGuard g(h->device);
+  *out = plan_create(h, comm, chunk, flags);
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_dist_plan_info(spmv_dist_plan_t plan, spmv_dist_plan_info_t* out) {
+  if (!plan || !out) return SPMV_ERR_INVALID_ARG;
+  plan_info(plan, out);
+  return SPMV_OK;
+}
+
+spmv_status_t spmv_dist_plan_part(spmv_dist_plan_t plan, int part, spmv_handle_t* out) {
+  if (!plan || !out || part < 0 || part > 2) return SPMV_ERR_INVALID_ARG;
+  *out = plan_part(plan, part);
+  return SPMV_OK;
+}
+
+spmv_status_t spmv_dist_plan_iterate(spmv_dist_plan_t plan, const void* x0, void* buf0, void* buf1, int64_t steps,
+                                     double* sums, float* loop_ms, float* interior_ms, int* final_buf) {
+  if (!plan || !x0 || !buf0 || !buf1 || !sums || steps < 0 || buf0 == buf1) return SPMV_ERR_INVALID_ARG;
+  API_TRY
+  DeviceGuard g(plan_device(plan));
+  plan_iterate(plan, x0, buf0, buf1, steps, sums, loop_ms, interior_ms, final_buf);
+  API_CATCH(kNoHandle)
+}
+
+spmv_status_t spmv_dist_plan_destroy(spmv_dist_plan_t plan) {
+  API_TRY
+  plan_destroy(plan);
+  API_CATCH(kNoHandle)
+}
+
+spmv_status_t spmv_dist_local_group(int world, const int* devices, void** comms) {
+  if (world < 1 || !devices || !comms) return SPMV_ERR_INVALID_ARG;
+  for (int r = 0; r < world; ++r) comms[r] = nullptr;
+  API_TRY
+  std::vector<CommBase*> v = local_group(world, devices);
+  for (int r = 0; r < world; ++r) comms[r] = v[r];
+  API_CATCH(kNoHandle)
+}
+
+spmv_status_t spmv_create_row_slice(spmv_handle_t* out, spmv_handle_t h, int64_t row_begin, int64_t row_end) {
+  if (!out) return SPMV_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!h || row_begin < 0 || row_end < row_begin || row_end > h->rows) return SPMV_ERR_INVALID_ARG;
+  API_TRY
+  DeviceGuard g(h->device);
+  *out = make_row_slice(h, row_begin, row_end);
   API_CATCH(h)
 }
 

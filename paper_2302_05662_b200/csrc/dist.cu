@@ -7,10 +7,14 @@
 // link-time NCCL dependency (single-GPU users and CPU-side tests never need it).
 #include <dlfcn.h>
 
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <vector>
 
+#include "dist.cuh"
 #include "spmv_common.cuh"
 
 namespace spmv {
@@ -22,7 +26,7 @@ typedef struct {
   char internal[128];
 } ncclUniqueId;
 typedef int ncclResult_t;
-constexpr int ncclFloat32 = 7, ncclFloat64 = 8, ncclSumOp = 0;
+constexpr int ncclInt8 = 0, ncclFloat64 = 8, ncclSumOp = 0;
 
 struct NcclApi {
   void* lib = nullptr;
@@ -31,6 +35,10 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -47,9 +55,14 @@ NcclApi& nccl() {
     api.CommDestroy = (decltype(api.CommDestroy))dlsym(l, "ncclCommDestroy");
     api.AllReduce = (decltype(api.AllReduce))dlsym(l, "ncclAllReduce");
     api.AllGather = (decltype(api.AllGather))dlsym(l, "ncclAllGather");
+    api.Send = (decltype(api.Send))dlsym(l, "ncclSend");
+    api.Recv = (decltype(api.Recv))dlsym(l, "ncclRecv");
+    api.GroupStart = (decltype(api.GroupStart))dlsym(l, "ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))dlsym(l, "ncclGroupEnd");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(l, "ncclGetErrorString");
   });
-  if (!api.lib || !api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.AllGather)
+  if (!api.lib || !api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.AllGather || !api.Send ||
+      !api.Recv || !api.GroupStart || !api.GroupEnd)
     fail(SPMV_ERR_NCCL, "libnccl.so.2 not loadable or incomplete");
   return api;
 }
@@ -61,26 +74,167 @@ void nccl_check(ncclResult_t r, const char* what) {
   }
 }
 
-struct Comm {
+// ------------------------------------------------------------------ NCCL
+struct NcclComm : CommBase {
   ncclComm_t c = nullptr;
-  int rank = 0, world = 1, device = 0;
+  const char* kind() const override { return "nccl"; }
+  bool uses_sms() const override { return world > 1; }
+  void allreduce_f64(double* buf, size_t n, cudaStream_t s) override {
+    nccl_check(nccl().AllReduce(buf, buf, n, ncclFloat64, ncclSumOp, c, s), "ncclAllReduce");
+  }
+  void allgather_inplace(void* buf, size_t chunk_bytes, cudaStream_t s) override {
+    char* b = static_cast<char*>(buf);
+    nccl_check(nccl().AllGather(b + (size_t)rank * chunk_bytes, b, chunk_bytes, ncclInt8, c, s), "ncclAllGather");
+  }
+  void exchange(const std::vector<P2P>& sends, const std::vector<P2P>& recvs, cudaStream_t s) override {
+    nccl_check(nccl().GroupStart(), "ncclGroupStart");
+    ncclResult_t r = 0;
+    for (const P2P& p : sends)
+      if (r == 0 && p.bytes) r = nccl().Send(p.ptr, p.bytes, ncclInt8, p.peer, c, s);
+    for (const P2P& p : recvs)
+      if (r == 0 && p.bytes) r = nccl().Recv(p.ptr, p.bytes, ncclInt8, p.peer, c, s);
+    ncclResult_t e = nccl().GroupEnd();
+    nccl_check(r, "ncclSend/ncclRecv");
+    nccl_check(e, "ncclGroupEnd");
+  }
+  ~NcclComm() override {
+    if (c && nccl().CommDestroy) nccl().CommDestroy(c);
+  }
+};
+
+// ------------------------------------------------------------------ in-process group
+constexpr size_t kLocalStage = 64;  // max doubles per local all-reduce
+
+__global__ void k_sum_slots(const double* __restrict__ all, int world, int n, double* __restrict__ out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double a = all[i];
+    for (int q = 1; q < world; ++q) a += all[(size_t)q * n + i];  // rank order
+    out[i] = a;
+  }
+}
+
+struct LocalShared {
+  int world = 1;
+  std::vector<int> devices;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool broken = false;
+  std::vector<cudaEvent_t> ev_in, ev_out;
+  std::vector<void*> posted;
+  std::vector<std::vector<P2P>> posted_sends;
+  std::vector<double*> staging;  // per rank, on its device
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) fail(SPMV_ERR_NCCL, "local group: a peer rank failed");
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; })) {
+      broken = true;
+      cv.notify_all();
+      fail(SPMV_ERR_NCCL, "local group: barrier timed out (a rank did not enter the collective)");
+    }
+    if (gen == g) fail(SPMV_ERR_NCCL, "local group: a peer rank failed");
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    broken = true;
+    cv.notify_all();
+  }
+  ~LocalShared() {
+    for (int r = 0; r < world; ++r) {
+      cudaSetDevice(devices[r]);
+      if (ev_in[r]) cudaEventDestroy(ev_in[r]);
+      if (ev_out[r]) cudaEventDestroy(ev_out[r]);
+      if (staging[r]) cudaFree(staging[r]);
+    }
+  }
+};
+
+struct LocalComm : CommBase {
+  std::shared_ptr<LocalShared> g;
+  double* gather = nullptr;  // [world][kLocalStage] on this rank's device
+  const char* kind() const override { return "local"; }
+  bool uses_sms() const override { return false; }
+  void abort() override { g->abort(); }
+  // Collective entry/exit: every rank's stream waits for every rank's entry
+  // (inputs ready) and, at the end, for every rank's exit (outputs consumed),
+  // like a collective that completes everywhere at once.
+  void enter(cudaStream_t s) {
+    CK(cudaEventRecord(g->ev_in[rank], s));
+    g->barrier();
+    for (int q = 0; q < world; ++q) CK(cudaStreamWaitEvent(s, g->ev_in[q], 0));
+  }
+  void leave(cudaStream_t s) {
+    CK(cudaEventRecord(g->ev_out[rank], s));
+    g->barrier();
+    for (int q = 0; q < world; ++q) CK(cudaStreamWaitEvent(s, g->ev_out[q], 0));
+  }
+  void allreduce_f64(double* buf, size_t n, cudaStream_t s) override {
+    if (n > kLocalStage) fail(SPMV_ERR_INVALID_ARG, "local group: all-reduce of more than 64 doubles");
+    CK(cudaMemcpyAsync(g->staging[rank], buf, n * 8, cudaMemcpyDefault, s));
+    enter(s);
+    for (int q = 0; q < world; ++q)
+      CK(cudaMemcpyAsync(gather + (size_t)q * n, g->staging[q], n * 8, cudaMemcpyDefault, s));
+    LAUNCH(k_sum_slots, 1, 64, 0, s, (const double*)gather, world, (int)n, buf);
+    leave(s);
+  }
+  void allgather_inplace(void* buf, size_t chunk_bytes, cudaStream_t s) override {
+    g->posted[rank] = buf;
+    enter(s);
+    for (int q = 0; q < world; ++q)
+      if (q != rank && chunk_bytes)
+        CK(cudaMemcpyAsync(static_cast<char*>(buf) + (size_t)q * chunk_bytes,
+                           static_cast<const char*>(g->posted[q]) + (size_t)q * chunk_bytes, chunk_bytes,
+                           cudaMemcpyDefault, s));
+    leave(s);
+  }
+  void exchange(const std::vector<P2P>& sends, const std::vector<P2P>& recvs, cudaStream_t s) override {
+    g->posted_sends[rank] = sends;
+    enter(s);
+    std::vector<size_t> used(world, 0);
+    for (const P2P& r : recvs) {
+      const std::vector<P2P>& ps = g->posted_sends[r.peer];
+      size_t k = used[r.peer];
+      while (k < ps.size() && ps[k].peer != rank) ++k;
+      if (k == ps.size()) fail(SPMV_ERR_NCCL, "local group: receive without a matching send");
+      used[r.peer] = k + 1;
+      if (ps[k].bytes != r.bytes) fail(SPMV_ERR_NCCL, "local group: send/receive size mismatch");
+      if (r.bytes) CK(cudaMemcpyAsync(r.ptr, ps[k].ptr, r.bytes, cudaMemcpyDefault, s));
+    }
+    leave(s);
+  }
+  ~LocalComm() override {
+    if (gather) {
+      cudaSetDevice(device);
+      cudaFree(gather);
+    }
+  }
 };
 
 }  // namespace
 
-// Power iteration loop (declared in handle.cuh).
+// Power iteration loop (declared in handle.cuh). z_k is written straight
+// into this rank's chunk of the next replicated buffer; the all-gather is in
+// place (chunk_buf is not needed).
 void power_iterate(spmv_matrix* h, const void* x0, void* buf0, void* buf1, int64_t n_full, int64_t steps,
-                   double* sums, void* comm_v, int64_t chunk, void* chunk_buf, float* kernel_ms, float* loop_ms,
+                   double* sums, void* comm_v, int64_t chunk, void* /*chunk_buf*/, float* kernel_ms, float* loop_ms,
                    int* final_buf) {
   cudaStream_t s = h->stream;
-  Comm* comm = static_cast<Comm*>(comm_v);
+  CommBase* comm = as_comm(comm_v);
   const int vb = h->vbytes;
-  const int dtype = h->dtype == SPMV_R64F ? ncclFloat64 : ncclFloat32;
   if (x0 != buf0) CK(cudaMemcpyAsync(buf0, x0, (size_t)n_full * vb, cudaMemcpyDeviceToDevice, s));
   const int64_t row_offset = comm ? (int64_t)comm->rank * chunk : 0;
+  if (comm && (comm->rank + 1) * chunk > n_full) fail(SPMV_ERR_INVALID_ARG, "power_iterate: world·chunk > n_full");
   // S_0 = ||z_0||² over this rank's rows, then summed over ranks
   spmv_norm2_internal(h, static_cast<char*>(buf0) + row_offset * vb, h->rows, sums);
-  if (comm) nccl_check(nccl().AllReduce(sums, sums, 2, ncclFloat64, ncclSumOp, comm->c, s), "ncclAllReduce");
+  if (comm) comm->allreduce_f64(sums, 2, s);
   std::vector<cudaEvent_t> ev;
   if (kernel_ms) {
     ev.resize(2 * (size_t)steps);
@@ -95,14 +249,13 @@ void power_iterate(spmv_matrix* h, const void* x0, void* buf0, void* buf1, int64
   void* cur = buf0;
   void* nxt = buf1;
   for (int64_t k = 0; k < steps; ++k) {
-    void* y = comm ? chunk_buf : nxt;
+    void* y = static_cast<char*>(nxt) + row_offset * vb;
     if (kernel_ms) CK(cudaEventRecord(ev[2 * k], s));
     power_step_internal(h, cur, y, sums + 2 * k, sums + 2 * (k + 1), row_offset);
     if (kernel_ms) CK(cudaEventRecord(ev[2 * k + 1], s));
-    if (comm) {  // also at world = 1, so the NCCL path is testable on one GPU
-      nccl_check(nccl().AllReduce(sums + 2 * (k + 1), sums + 2 * (k + 1), 2, ncclFloat64, ncclSumOp, comm->c, s),
-                 "ncclAllReduce");
-      nccl_check(nccl().AllGather(chunk_buf, nxt, (size_t)chunk, dtype, comm->c, s), "ncclAllGather");
+    if (comm) {  // also at world = 1, so the collective path is testable on one GPU
+      comm->allreduce_f64(sums + 2 * (k + 1), 2, s);
+      comm->allgather_inplace(nxt, (size_t)chunk * vb, s);
     }
     std::swap(cur, nxt);
   }
@@ -124,7 +277,7 @@ void power_iterate(spmv_matrix* h, const void* x0, void* buf0, void* buf1, int64
 void* dist_init(const uint8_t id[128], int rank, int world, int device) {
   ncclUniqueId u;
   std::memcpy(u.internal, id, 128);
-  Comm* c = new Comm();
+  NcclComm* c = new NcclComm();
   c->rank = rank;
   c->world = world;
   c->device = device;
@@ -135,7 +288,7 @@ void* dist_init(const uint8_t id[128], int rank, int world, int device) {
     delete c;
     throw;
   }
-  return c;
+  return static_cast<CommBase*>(c);
 }
 
 void dist_unique_id(uint8_t out[128]) {
@@ -144,11 +297,40 @@ void dist_unique_id(uint8_t out[128]) {
   std::memcpy(out, u.internal, 128);
 }
 
-void dist_destroy(void* comm) {
-  Comm* c = static_cast<Comm*>(comm);
-  if (!c) return;
-  if (c->c && nccl().CommDestroy) nccl().CommDestroy(c->c);
-  delete c;
+void dist_destroy(void* comm) { delete as_comm(comm); }
+
+std::vector<CommBase*> local_group(int world, const int* devices) {
+  auto g = std::make_shared<LocalShared>();
+  g->world = world;
+  g->devices.assign(devices, devices + world);
+  g->ev_in.assign(world, nullptr);
+  g->ev_out.assign(world, nullptr);
+  g->posted.assign(world, nullptr);
+  g->posted_sends.assign(world, {});
+  g->staging.assign(world, nullptr);
+  std::vector<CommBase*> out;
+  try {
+    for (int r = 0; r < world; ++r) {
+      CK(cudaSetDevice(devices[r]));
+      CK(cudaEventCreateWithFlags(&g->ev_in[r], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&g->ev_out[r], cudaEventDisableTiming));
+      CK(cudaMalloc(&g->staging[r], kLocalStage * sizeof(double)));
+    }
+    for (int r = 0; r < world; ++r) {
+      LocalComm* c = new LocalComm();
+      out.push_back(c);
+      c->g = g;
+      c->rank = r;
+      c->world = world;
+      c->device = devices[r];
+      CK(cudaSetDevice(devices[r]));
+      CK(cudaMalloc(&c->gather, (size_t)world * kLocalStage * sizeof(double)));
+    }
+  } catch (...) {
+    for (CommBase* c : out) delete c;
+    throw;
+  }
+  return out;
 }
 
 }  // namespace spmv

@@ -89,6 +89,9 @@ struct spmv_matrix {
 namespace spmv {
 
 // ingest.cu
+// New handle holding rows [r0, r1) of parent's CSR (same columns, same dtype,
+// stream and device; features not computed, active format CSR).
+spmv_matrix* make_row_slice(spmv_matrix* parent, int64_t r0, int64_t r1);
 void ingest(spmv_matrix* h, const int32_t* row_idx, const int32_t* col_idx, const void* vals,
             spmv_mem_t where);
 
@@ -117,6 +120,8 @@ struct Epilogue {
   double* partials = nullptr;          // mode 1: per-block partials (2 per block)
   unsigned* counter = nullptr;         // mode 1: last-block counter (zero at rest)
   int64_t row_offset = 0;              // mode 1: x_own = x[row_offset + i]
+  int sums_parts = 1;                  // modes 1/3: alpha = 1/sqrt(Σ_p sums_prev[2p]) (row-block parts)
+  bool pdl = true;                     // mode 1: programmatic dependent launch after the previous kernel
 };
 
 // spmv kernels (launchers). All asynchronous on h->stream.
@@ -135,12 +140,20 @@ void run_norms(spmv_matrix* h, const Epilogue& e, const void* x, const void* y, 
 
 // Power step / norm (api.cu) and the native loop + NCCL (dist.cu).
 void power_step_internal(spmv_matrix* h, const void* x, void* y, const double* sums_prev, double* sums_out,
-                         int64_t row_offset);
+                         int64_t row_offset, int sums_parts = 1, bool pdl = true);
 void spmv_norm2_internal(spmv_matrix* h, const void* x, int64_t n, double* sums_out);
 void power_iterate(spmv_matrix* h, const void* x0, void* buf0, void* buf1, int64_t n_full, int64_t steps,
                    double* sums, void* comm, int64_t chunk, void* chunk_buf, float* kernel_ms, float* loop_ms,
                    int* final_buf);
 void* dist_init(const uint8_t id[128], int rank, int world, int device);
+// plan.cu: the distributed plan (interior/halo split, overlap, halo exchange).
+spmv_dist_plan* plan_create(spmv_matrix* h, void* comm, int64_t chunk, uint32_t flags);
+void plan_destroy(spmv_dist_plan* P);
+void plan_iterate(spmv_dist_plan* P, const void* x0, void* buf0, void* buf1, int64_t steps, double* sums,
+                  float* loop_ms, float* interior_ms, int* final_buf);
+void plan_info(const spmv_dist_plan* P, spmv_dist_plan_info_t* o);
+spmv_matrix* plan_part(spmv_dist_plan* P, int p);
+int plan_device(const spmv_dist_plan* P);
 void dist_unique_id(uint8_t out[128]);
 void dist_destroy(void* comm);
 
@@ -159,7 +172,9 @@ void* ensure_fixup_scratch(spmv_matrix* h, size_t bytes);
 
 // Resolve a launch variant to the defaults of its kernel.
 spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t& L);
-// Grid for a persistent (grid-stride) kernel: min(needed, SMs × resident blocks per SM).
+// Grid for a persistent (grid-stride) kernel: min(needed, SMs × resident blocks per SM),
+// minus g_sm_reserve SMs' worth of residency (left free for concurrent NCCL kernels).
+extern thread_local int g_sm_reserve;
 int64_t persistent_grid(const void* func, int block, int64_t needed_blocks, size_t dyn_smem = 0);
 // Opt in to `bytes` of dynamic shared memory for func (cached).
 void set_max_dynamic_smem(const void* func, size_t bytes);

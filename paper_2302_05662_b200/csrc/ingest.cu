@@ -5,6 +5,7 @@
 // saved in a third array called Row Index") — fused into ONE pass
 // over the triplets when the input is already sorted (28 B/nnz for fp64).
 // Unsorted input is radix-sorted by (row, col) first.
+#include <algorithm>
 #include <cstdlib>
 
 #include "handle.cuh"
@@ -236,6 +237,76 @@ void ingest_typed(spmv_matrix* h, const int32_t* row_idx, const int32_t* col_idx
 }
 
 }  // namespace
+
+namespace {
+template <class RI, class RO>
+__global__ void k_slice_rp(const RI* __restrict__ in, int64_t r0, int64_t n, RO* __restrict__ out) {
+  const int64_t base = (int64_t)in[r0];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = (RO)((int64_t)in[r0 + i] - base);
+}
+
+template <class RI>
+void slice_rp(const spmv_matrix* p, spmv_matrix* h, int64_t r0) {
+  const unsigned g = grid_for(h->rows + 1, 256);
+  if (h->rp64)
+    LAUNCH((k_slice_rp<RI, int64_t>), g, 256, 0, h->stream, static_cast<const RI*>(p->row_ptr), r0, h->rows + 1,
+           static_cast<int64_t*>(h->row_ptr));
+  else
+    LAUNCH((k_slice_rp<RI, int32_t>), g, 256, 0, h->stream, static_cast<const RI*>(p->row_ptr), r0, h->rows + 1,
+           static_cast<int32_t*>(h->row_ptr));
+}
+}  // namespace
+
+// Row block [r0, r1) of the parent's CSR as a new handle (the interior/halo
+// split of the distributed power iteration). The row
+// pointers are rebased to 0; col/val are copied (the slice owns its memory).
+spmv_matrix* make_row_slice(spmv_matrix* p, int64_t r0, int64_t r1) {
+  cudaStream_t s = p->stream;
+  int64_t lohi[2] = {0, 0};
+  if (p->rp64) {
+    CK(cudaMemcpyAsync(&lohi[0], static_cast<int64_t*>(p->row_ptr) + r0, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&lohi[1], static_cast<int64_t*>(p->row_ptr) + r1, 8, cudaMemcpyDeviceToHost, s));
+  } else {
+    int32_t t[2];
+    CK(cudaMemcpyAsync(&t[0], static_cast<int32_t*>(p->row_ptr) + r0, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&t[1], static_cast<int32_t*>(p->row_ptr) + r1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    lohi[0] = t[0];
+    lohi[1] = t[1];
+  }
+  CK(cudaStreamSynchronize(s));
+  spmv_matrix* h = new spmv_matrix();
+  h->device = p->device;
+  h->stream = s;
+  h->dtype = p->dtype;
+  h->vbytes = p->vbytes;
+  h->rows = r1 - r0;
+  h->cols = p->cols;
+  h->nnz = lohi[1] - lohi[0];
+  for (auto& L : h->launch) L = spmv_launch_t{0, 0, -1, 0};
+  try {
+    h->rp64 = p->rp64 && h->nnz > 0 && (h->nnz > (int64_t)INT32_MAX || (getenv("SPMV_FORCE_RP64") && getenv("SPMV_FORCE_RP64")[0] == '1'));
+    h->row_ptr = h->rp64 ? (void*)dalloc_n<int64_t>(h->rows + 1, s) : (void*)dalloc_n<int32_t>(h->rows + 1, s);
+    h->col = dalloc_n<int32_t>(h->nnz, s);
+    h->val = dalloc((size_t)std::max<int64_t>(h->nnz, 1) * h->vbytes, s);
+    if (p->rp64) slice_rp<int64_t>(p, h, r0);
+    else slice_rp<int32_t>(p, h, r0);
+    if (h->nnz > 0) {
+      CK(cudaMemcpyAsync(h->col, p->col + lohi[0], (size_t)h->nnz * 4, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(h->val, static_cast<const char*>(p->val) + lohi[0] * p->vbytes,
+                         (size_t)h->nnz * p->vbytes, cudaMemcpyDeviceToDevice, s));
+    }
+  } catch (...) {
+    dfree(h->row_ptr, s);
+    dfree(h->col, s);
+    dfree(h->val, s);
+    delete h;
+    throw;
+  }
+  return h;
+}
 
 void ingest(spmv_matrix* h, const int32_t* row_idx, const int32_t* col_idx, const void* vals,
             spmv_mem_t where) {

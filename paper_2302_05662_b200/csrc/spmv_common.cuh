@@ -62,9 +62,12 @@ __device__ __forceinline__ void load_cols(const int* p, int (&out)[N]) {
 
 // Epilogue modes: 0 y = alpha·s + beta·y; 1 y = alpha_dev·s (power step);
 // 2 y += alpha·s (HYB tail); 3 y += alpha_dev·s (HYB tail in a power step).
-// alpha_dev = 1/sqrt(sums_prev[0]).
+// alpha_dev = 1/sqrt(sums_prev[0] + sums_prev[2] + ...) over e.sums_parts row-block parts.
 __device__ __forceinline__ double epi_alpha(const Epilogue& e) {
-  return (e.mode == 1 || e.mode == 3) ? 1.0 / sqrt(__ldcg(e.sums_prev)) : e.alpha;
+  if (e.mode != 1 && e.mode != 3) return e.alpha;
+  double s = __ldcg(e.sums_prev);
+  for (int p = 1; p < e.sums_parts; ++p) s += __ldcg(e.sums_prev + 2 * p);  // fixed order: same on every rank
+  return 1.0 / sqrt(s);
 }
 
 // Final value of row r given its accumulated Σ a·x.

@@ -25,7 +25,7 @@ void launch_sliced(spmv_matrix* h, kern::SlicedParams& p, int C, const spmv_laun
     p.e.counter = h->pi_counter;
   }
   void* args[] = {&p};
-  if (p.e.mode == 1) {
+  if (p.e.mode == 1 && p.e.pdl) {
     // power step: programmatic dependent launch (see k_sliced)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
