@@ -70,13 +70,14 @@ class PowerIteration:
     slab's z_k and its two partial sums; local_norm2(x_local, sums_out)
     computes Σ x_local². Both are the C-ABI calls on the GPU path."""
 
-    def __init__(self, layout: Layout, rank: int, local_step, local_norm2, group=None):
+    def __init__(self, layout: Layout, rank: int, local_step, local_norm2, group=None, halo=None):
         import torch.distributed as dist
         self.layout = layout
         self.rank = rank
         self.local_step = local_step
         self.local_norm2 = local_norm2
         self.group = group
+        self.halo = halo  # HaloExchange: exchange only the referenced remote entries
         self.dist = dist if (dist.is_available() and dist.is_initialized() and layout.world > 1) else None
 
     def _allreduce(self, t):
@@ -113,7 +114,11 @@ class PowerIteration:
                 y_local = chunk_buf[:nloc]
                 self.local_step(cur, y_local, sums[k], sums[k + 1], self.rank * L.chunk)
                 self._allreduce(sums[k + 1])
-                self._allgather(nxt, chunk_buf)
+                if self.halo is not None:
+                    nxt[self.rank * L.chunk: self.rank * L.chunk + nloc] = y_local
+                    self.halo.exchange(nxt)
+                else:
+                    self._allgather(nxt, chunk_buf)
             cur, nxt = nxt, cur
             if on_step is not None:
                 on_step(k)
@@ -133,6 +138,58 @@ class PowerIteration:
         """lambda_k = D_k / sqrt(S_{k-1}) for k = 1..steps (host numpy)."""
         s = sums.detach().cpu().numpy() if hasattr(sums, "detach") else np.asarray(sums)
         return s[1:, 1] / np.sqrt(s[:-1, 0])
+
+
+class HaloExchange:
+    """Point-to-point exchange of exactly the remote entries of x a row slab
+    references — the torch.distributed mirror of the native plan's
+    SPMV_PLAN_HALO lists (plan.cu build_halo_lists / exchange_step):
+    sorted unique remote padded positions grouped by owner; counts all-gathered
+    once; request lists sent to the owners once; per step each owner sends the
+    requested values and the receiver scatters them into its vector."""
+
+    def __init__(self, layout: Layout, rank: int, slab_cols, group=None):
+        import torch
+        import torch.distributed as dist
+        L = layout
+        a, b = L.rows_of(rank)
+        lo, hi = rank * L.chunk, rank * L.chunk + (b - a)
+        cols = np.asarray(slab_cols, np.int64)
+        remote = np.unique(cols[(cols < lo) | (cols >= hi)])
+        owner = remote // L.chunk
+        self.need = {int(q): remote[owner == q] for q in np.unique(owner)}
+        counts = torch.zeros(L.world, dtype=torch.int64)
+        for q, v in self.need.items():
+            counts[q] = len(v)
+        allc = [torch.zeros(L.world, dtype=torch.int64) for _ in range(L.world)]
+        dist.all_gather(allc, counts, group=group)
+        give_cnt = {r: int(allc[r][rank]) for r in range(L.world) if int(allc[r][rank]) > 0}
+        reqs, bufs = [], {}
+        for q, v in self.need.items():
+            reqs.append(dist.isend(torch.from_numpy(v.copy()), q, group=group))
+        for r, c in give_cnt.items():
+            bufs[r] = torch.empty(c, dtype=torch.int64)
+            reqs.append(dist.irecv(bufs[r], r, group=group))
+        for q in reqs:
+            q.wait()
+        self.give = {r: t for r, t in bufs.items()}
+        self.need_t = {q: torch.from_numpy(v.copy()) for q, v in self.need.items()}
+        self.group = group
+        self.recv_elems = int(sum(len(v) for v in self.need.values()))
+
+    def exchange(self, x_full):
+        import torch
+        import torch.distributed as dist
+        reqs, bufs = [], {}
+        for r, idx in self.give.items():
+            reqs.append(dist.isend(x_full[idx].contiguous(), r, group=self.group))
+        for q, idx in self.need_t.items():
+            bufs[q] = torch.empty(len(idx), dtype=x_full.dtype)
+            reqs.append(dist.irecv(bufs[q], q, group=self.group))
+        for q in reqs:
+            q.wait()
+        for q, idx in self.need_t.items():
+            x_full[idx] = bufs[q]
 
 
 class NativeComm:

@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 import oracle
 import paper_2302_05662_b200 as P
 import spmv_inputs as si
-from paper_2302_05662_b200.dist import Layout, PowerIteration
+from paper_2302_05662_b200.dist import HaloExchange, Layout, PowerIteration
 
 STEPS = 6
 
@@ -28,7 +28,7 @@ def _free_port():
 
 
 
-def _worker(rank, world, port, q, kind):
+def _worker(rank, world, port, q, kind, halo=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -60,25 +60,36 @@ def _worker(rank, world, port, q, kind):
             so[0] = float(np.dot(v, v))
             so[1] = 0.0
 
-        pi = PowerIteration(L, rank, local_step, local_norm2)
+        hx = HaloExchange(L, rank, C) if halo else None
+        pi = PowerIteration(L, rank, local_step, local_norm2, halo=hx)
         x0 = L.to_padded(si.vector(n))
         z, sums = pi.run(torch.from_numpy(x0), STEPS)
+        # own chunk of the final iterate from every rank (halo mode keeps only own + halo entries)
+        a0, b0 = L.rows_of(rank)
+        own = z[rank * L.chunk: rank * L.chunk + (b0 - a0)].clone()
+        parts = [torch.zeros(L.chunk, dtype=own.dtype) for _ in range(world)]
+        padded = torch.zeros(L.chunk, dtype=own.dtype)
+        padded[: b0 - a0] = own
+        dist.all_gather(parts, padded)
         if rank == 0:
-            q.put((L.from_padded(z.numpy()), PowerIteration.lambdas(sums)))
+            zf = torch.cat(parts).numpy()
+            q.put((L.from_padded(zf), PowerIteration.lambdas(sums), hx.recv_elems if hx else None))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["lap2d", "rmat"])
-def test_power_iteration_gloo_world2(kind):
+@pytest.mark.parametrize("kind,halo", [("lap2d", False), ("rmat", False), ("lap2d", True), ("rmat", True)])
+def test_power_iteration_gloo_world2(kind, halo):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, kind)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, kind, halo)) for r in range(world)]
     for p in procs:
         p.start()
-    z_dist, lam_dist = q.get(timeout=240)
+    z_dist, lam_dist, recv = q.get(timeout=240)
+    if halo and kind == "lap2d":
+        assert recv == 24   # one grid row of the 24x24 Laplacian from the neighbour
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
