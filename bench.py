@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--launch", default="", help="block,maxreg,carveout,knob (skips the launch sweep)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--index16", type=int, default=-1, choices=[-1, 0, 1],
+                    help="ELL/SELL column storage with --format: -1 auto (16-bit offsets when they fit), 0 int32, 1 16-bit")
     ap.add_argument("--plan", default="overlap,halo",
                     help="N>1 schedule: comma list of overlap (interior SpMV overlaps the exchange) and halo "
                          "(exchange only referenced remote entries); 'none' = split + all-gather, serialised")
@@ -324,13 +326,14 @@ def run_ours(args):
         rep = P.spmv_tune(h, flags, expected_iterations=E)
         fmt = rep.format
         params = dict(csr_alg=rep.params.csr_alg, csr_T=rep.params.csr_T, sell_C=rep.params.sell_C,
-                      sell_sigma=rep.params.sell_sigma, hyb_K=rep.params.hyb_K)
+                      sell_sigma=rep.params.sell_sigma, hyb_K=rep.params.hyb_K, bell_b=rep.params.bell_b,
+                      index16=rep.params.index16)
         launch = P.spmv_get_launch(h, fmt)
         decision = P.spmv_decision_log(h)
     else:
         fmt = P.FORMATS[args.format]
-        params = {}
-        P.spmv_convert(h, fmt)
+        params = {"index16": args.index16} if fmt in (P.FMT_ELL, P.FMT_SELL) else {}
+        P.spmv_convert(h, fmt, **params)
         if args.launch:
             P.spmv_set_launch(h, fmt, *[int(v) for v in args.launch.split(",")])
         elif not args.no_tune_launch:
@@ -341,7 +344,12 @@ def run_ours(args):
     if fmt != P.FMT_CSR:
         params = {k: v for k, v in params.items() if k != "csr_alg" or fmt == P.FMT_CSR}
     if fmt == P.FMT_SELL:
-        params = dict(sell_C=params.get("sell_C", 0), sell_sigma=params.get("sell_sigma", 0))
+        params = dict(sell_C=params.get("sell_C", 0), sell_sigma=params.get("sell_sigma", 0),
+                      index16=params.get("index16", 0))
+    elif fmt == P.FMT_ELL:
+        params = dict(index16=params.get("index16", 0))
+    elif fmt == P.FMT_BELL:
+        params = dict(bell_b=params.get("bell_b", 0))
     elif fmt == P.FMT_HYB:
         params = dict(hyb_K=params.get("hyb_K", -1))
     elif fmt == P.FMT_CSR:

@@ -88,7 +88,9 @@ typedef struct {
   int32_t sell_sigma; /* sorting window: 1 (no sort) or a multiple of sell_C; 0 = 1 */
   int64_t hyb_K;      /* HYB ELL width; -1 = automatic (CUSP/Bell–Garland rule, R12) */
   int32_t bell_b;     /* BELL square block dimension in {2,3,4}; 0 = 2 (the paper's 2×2) */
-  int32_t reserved;
+  int32_t index16;    /* ELL/SELL column storage: 0 = int32 columns (default); 1 = 16-bit offsets
+                         d = col − row (10 instead of 12 B per fp64 slot; SPMV_ERR_UNSUPPORTED unless
+                         every |col − row| <= 32767); -1 = 16-bit when they fit, else int32 */
 } spmv_format_params_t;
 
 /* Table 2 features + the north star's max and bandwidth.
@@ -128,6 +130,14 @@ typedef struct {
 #define SPMV_TUNE_OBJ_POWER (2u << 4)
 #define SPMV_TUNE_OBJ_EFFICIENCY (3u << 4)
 #define SPMV_TUNE_OBJ_MASK (3u << 4)
+/* With SPMV_TUNE_FORMAT: the paper's run-time mode with LEARNED models
+ * instead of measuring every
+ * candidate: features -> decision-tree class (best format) -> predicted speed
+ * ratio vs CSR-vector and predicted conversion latency -> convert iff
+ * expected_iterations·(t_csr − ratio·t_csr) > f_latency + c_latency_pred.
+ * Only t_csr is measured. Latency objective only (SPMV_ERR_UNSUPPORTED with
+ * another objective): the models are trained on latency. */
+#define SPMV_TUNE_PREDICT 4u
 
 typedef struct {
   int32_t format;                /* chosen spmv_format_t (active after the call) */
@@ -161,6 +171,7 @@ typedef struct {
   int64_t n_empty_rows;  /* COO: rows without entries */
   int64_t stored_bytes;  /* bytes of the format's arrays (padding included) */
   int64_t block;         /* BELL block dimension b (K = blocks per block row, n_pad = padded block rows) */
+  int64_t index_bytes;   /* bytes per stored column index (2 with ELL/SELL index16, else 4; 0 = CSR/COO arrays) */
 } spmv_format_info_t;
 
 typedef enum {
@@ -181,7 +192,9 @@ typedef enum {
   SPMV_ARR_HYB_TAIL_VAL = 14,
   SPMV_ARR_COO_EMPTY_ROWS = 15, /* int32 [n_empty_rows], ascending */
   SPMV_ARR_BELL_COL = 16,     /* int32 [K·n_pad]: block column of slot (I, k) at k·n_pad + I, pad −1 */
-  SPMV_ARR_BELL_VAL = 17      /* value [K·b·b·n_pad]: entry (r, c) of slot (I, k) at (k·b·b + r·b + c)·n_pad + I */
+  SPMV_ARR_BELL_VAL = 17,     /* value [K·b·b·n_pad]: entry (r, c) of slot (I, k) at (k·b·b + r·b + c)·n_pad + I */
+  SPMV_ARR_ELL_COL16 = 18,    /* int16 [K·n_pad] when index16: d = col − row, pad −32768 (ELL_COL is then absent) */
+  SPMV_ARR_SELL_COL16 = 19    /* int16 [slots] when index16: d = col − row of the slot's (permuted) row, pad −32768 */
 } spmv_array_t;
 
 /* ---------------------------------------------------------------- core API */
@@ -243,6 +256,22 @@ spmv_status_t spmv_get_launch(spmv_handle_t h, spmv_format_t fmt, spmv_launch_t*
  *   Synchronous. Decisions appended to the JSON log. */
 spmv_status_t spmv_tune(spmv_handle_t h, uint32_t flags, int64_t expected_iterations,
                         spmv_tune_report_t* out);
+
+/* The learned selector alone (host-only, no device work): class index into
+ * {CSR-vector, CSR-merge, ELL, SELL, HYB, COO, BELL-2, BELL-3}, the format and
+ * parameters it maps to, the predicted t_format / t_CSR-vector, and the
+ * predicted conversion and feature-extraction latencies in seconds. The
+ * model (tools/train_selector.py, profiles/selector_model.json) is compiled
+ * into the library. */
+typedef struct {
+  int32_t cls;
+  int32_t format;
+  spmv_format_params_t params;
+  double speed_ratio;
+  double c_latency_s;
+  double f_latency_s;
+} spmv_prediction_t;
+spmv_status_t spmv_predict(const spmv_features_t* features, spmv_dtype_t dtype, spmv_prediction_t* out);
 
 /* ---------------------------------------------------------------- power iteration
  * Power iteration (not in the paper):

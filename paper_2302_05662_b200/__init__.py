@@ -29,10 +29,13 @@ FORMATS = {"COO": FMT_COO, "CSR": FMT_CSR, "ELL": FMT_ELL, "HYB": FMT_HYB, "SELL
 FORMAT_NAMES = {v: k for k, v in FORMATS.items()}
 CSR_AUTO, CSR_SCALAR, CSR_VECTOR, CSR_MERGE, CSR_STREAM = 0, 1, 2, 3, 4
 TUNE_LAUNCH, TUNE_FORMAT, TUNE_ALL = 1, 2, 3
+TUNE_PREDICT = 4  # with TUNE_FORMAT: learned selector + overhead estimators instead of measuring candidates
+SELECTOR_CLASSES = ["CSR-vector", "CSR-merge", "ELL", "SELL", "HYB", "COO", "BELL-2", "BELL-3"]
 OBJECTIVES = {"latency": 0, "energy": 1, "power": 2, "efficiency": 3}   # OR-ed into flags as value << 4
 (ARR_CSR_ROW_PTR, ARR_CSR_COL, ARR_CSR_VAL, ARR_COO_ROW, ARR_ELL_COL, ARR_ELL_VAL, ARR_SELL_PERM,
  ARR_SELL_SLICE_PTR, ARR_SELL_COL, ARR_SELL_VAL, ARR_HYB_ELL_COL, ARR_HYB_ELL_VAL, ARR_HYB_TAIL_ROW,
- ARR_HYB_TAIL_COL, ARR_HYB_TAIL_VAL, ARR_COO_EMPTY_ROWS, ARR_BELL_COL, ARR_BELL_VAL) = range(18)
+ ARR_HYB_TAIL_COL, ARR_HYB_TAIL_VAL, ARR_COO_EMPTY_ROWS, ARR_BELL_COL, ARR_BELL_VAL, ARR_ELL_COL16,
+ ARR_SELL_COL16) = range(20)
 
 
 class SpmvError(RuntimeError):
@@ -44,7 +47,7 @@ class SpmvError(RuntimeError):
 class FormatParams(ctypes.Structure):
     _fields_ = [("csr_alg", ctypes.c_int32), ("csr_T", ctypes.c_int32), ("sell_C", ctypes.c_int32),
                 ("sell_sigma", ctypes.c_int32), ("hyb_K", ctypes.c_int64), ("bell_b", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("index16", ctypes.c_int32)]
 
 
 class Features(ctypes.Structure):
@@ -78,7 +81,12 @@ class TuneReport(ctypes.Structure):
 class FormatInfo(ctypes.Structure):
     _fields_ = [("present", ctypes.c_int32), ("row_ptr_is64", ctypes.c_int32)] + \
                [(n, ctypes.c_int64) for n in ("K", "n_pad", "C", "sigma", "n_slices", "slots", "tail_nnz",
-                                              "n_empty_rows", "stored_bytes", "block")]
+                                              "n_empty_rows", "stored_bytes", "block", "index_bytes")]
+
+
+class Prediction(ctypes.Structure):
+    _fields_ = [("cls", ctypes.c_int32), ("format", ctypes.c_int32), ("params", FormatParams),
+                ("speed_ratio", ctypes.c_double), ("c_latency_s", ctypes.c_double), ("f_latency_s", ctypes.c_double)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -137,6 +145,7 @@ def lib():
         "spmv_trim_pool": ([i32], i32),
         "spmv_power_iterate": ([H, vp, vp, vp, i64, i64, vp, vp, i64, vp, ctypes.POINTER(ctypes.c_float),
                                 ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int)], i32),
+        "spmv_predict": ([ctypes.POINTER(Features), i32, ctypes.POINTER(Prediction)], i32),
         "spmv_dist_plan_create": ([ctypes.POINTER(vp), H, vp, i64, u32], i32),
         "spmv_dist_plan_info": ([vp, ctypes.POINTER(PlanInfo)], i32),
         "spmv_dist_plan_part": ([vp, i32, ctypes.POINTER(H)], i32),
@@ -217,8 +226,8 @@ def spmv_create(rows, cols, row_idx, col_idx, vals, device: int = 0, stream=None
     return h
 
 
-def spmv_convert(h, fmt, csr_alg=0, csr_T=0, sell_C=0, sell_sigma=0, hyb_K=-1, bell_b=0):
-    p = FormatParams(csr_alg, csr_T, sell_C, sell_sigma, hyb_K, bell_b, 0)
+def spmv_convert(h, fmt, csr_alg=0, csr_T=0, sell_C=0, sell_sigma=0, hyb_K=-1, bell_b=0, index16=0):
+    p = FormatParams(csr_alg, csr_T, sell_C, sell_sigma, hyb_K, bell_b, index16)
     _check(lib().spmv_convert(h, fmt, ctypes.byref(p)), h)
 
 
@@ -279,6 +288,18 @@ def spmv_power_iterate(h, x0, buf0, buf1, steps, sums, comm=None, chunk=0, chunk
                                     _ptr(sums), comm, int(chunk), _ptr(chunk_buf), km,
                                     ctypes.byref(lm) if time_loop else None, ctypes.byref(fb)), h)
     return fb.value, (list(km)[:int(steps)] if km is not None else None), (lm.value if time_loop else None)
+
+
+def spmv_predict(features: dict, dtype="f64") -> dict:
+    """Learned selector on a features dict (spmv_features output); host only."""
+    f = Features()
+    for k, v in features.items():
+        setattr(f, k, v)
+    o = Prediction()
+    _check(lib().spmv_predict(ctypes.byref(f), R32F if dtype == "f32" else R64F, ctypes.byref(o)))
+    return {"cls": o.cls, "class": SELECTOR_CLASSES[o.cls], "format": o.format,
+            "params": {k[0]: getattr(o.params, k[0]) for k in FormatParams._fields_},
+            "speed_ratio": o.speed_ratio, "c_latency_s": o.c_latency_s, "f_latency_s": o.f_latency_s}
 
 
 def spmv_create_row_slice(h, row_begin, row_end):

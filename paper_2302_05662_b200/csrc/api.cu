@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "dist.cuh"
+#include "selector.cuh"
 #include "spmv_common.cuh"
 
 namespace spmv {
@@ -487,8 +488,8 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
       if (!was) {
         switch (fmt) {
           case SPMV_FMT_BELL: build_bell(h, bell_b_try); break;
-          case SPMV_FMT_ELL: build_ell(h); break;
-          case SPMV_FMT_SELL: build_sell(h, h->dtype == SPMV_R64F ? 64 : 128, 1); break;
+          case SPMV_FMT_ELL: build_ell(h, -1); break;
+          case SPMV_FMT_SELL: build_sell(h, h->dtype == SPMV_R64F ? 64 : 128, 1, -1); break;
           case SPMV_FMT_HYB: build_hyb(h, -1); break;
           case SPMV_FMT_COO: build_coo(h); break;
         }
@@ -604,6 +605,82 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
     rep->params.sell_sigma = (int32_t)h->sell_sigma;
     rep->params.hyb_K = h->hyb_K;
     rep->params.bell_b = (int32_t)h->bell_b;
+    rep->params.index16 = (h->active == SPMV_FMT_ELL && h->ell_col16) || (h->active == SPMV_FMT_SELL && h->sell_col16);
+  }
+}
+
+// Run-time mode with the learned models (SPMV_TUNE_PREDICT):
+// features -> predicted format -> estimated overhead -> gate.
+static void tune_predict(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tune_report_t* rep) {
+  if (!h->have_features) compute_features(h);
+  const spmv_features_t& f = h->feat;
+  double x[kSelectorFeatures];
+  selector_features(f, h->vbytes, x);
+  const int cls = selector_class(x);
+  int fmt;
+  spmv_format_params_t q;
+  selector_class_format(cls, &fmt, &q);
+  const int orig_alg = h->csr_alg;
+  h->csr_alg = SPMV_CSR_VECTOR;
+  const double t_csr =
+      time_variant(h, SPMV_FMT_CSR, resolve_launch(h, SPMV_FMT_CSR, spmv_launch_t{0, 0, -1, 0}), ts.x, ts.y);
+  h->csr_alg = orig_alg;
+  const double ratio = selector_speed_ratio(cls, x);
+  const double t_pred = t_csr * ratio;
+  const double c_pred = (fmt == SPMV_FMT_CSR) ? 0.0 : selector_c_latency(cls, x);
+  const double gain = (double)iters * (t_csr - t_pred);
+  const double overhead = h->f_latency + c_pred;
+  bool convert = cls != 0 && gain > overhead;
+  std::ostringstream os;
+  os.precision(9);
+  os << "{\"kind\":\"format_predict\",\"x\":[";
+  for (int i = 0; i < kSelectorFeatures; ++i) os << x[i] << (i + 1 < kSelectorFeatures ? "," : "");
+  os << "],\"class\":\"" << selector_class_name(cls) << "\",\"speed_ratio\":" << ratio << ",\"t_csr_s\":" << t_csr
+     << ",\"t_pred_s\":" << t_pred << ",\"gate\":{\"expected_iterations\":" << iters << ",\"gain_s\":" << gain
+     << ",\"f_latency_s\":" << h->f_latency << ",\"c_latency_pred_s\":" << c_pred << ",\"overhead\":" << overhead
+     << ",\"convert\":" << (convert ? "true" : "false") << "}";
+  if (convert) {
+    try {
+      switch (fmt) {
+        case SPMV_FMT_CSR: h->csr_alg = q.csr_alg; break;
+        case SPMV_FMT_ELL: if (!built(h, fmt)) build_ell(h, -1); break;
+        case SPMV_FMT_SELL: if (!built(h, fmt)) build_sell(h, h->dtype == SPMV_R64F ? 64 : 128, 1, -1); break;
+        case SPMV_FMT_HYB: if (!built(h, fmt)) build_hyb(h, -1); break;
+        case SPMV_FMT_COO: if (!built(h, fmt)) build_coo(h); break;
+        case SPMV_FMT_BELL:
+          if (built(h, fmt) && h->bell_b != q.bell_b) free_format(h, fmt);
+          if (!built(h, fmt)) build_bell(h, q.bell_b);
+          break;
+      }
+      h->active = fmt;
+    } catch (const SpmvError& e) {
+      cudaGetLastError();
+      convert = false;
+      os << ",\"build_failed\":\"" << e.msg << "\"";
+    }
+  }
+  if (!convert) {
+    h->active = SPMV_FMT_CSR;
+    h->csr_alg = SPMV_CSR_VECTOR;
+  }
+  os << ",\"chosen\":\"" << (convert ? selector_class_name(cls) : "CSR-vector") << "\"}";
+  log_append(h, os.str());
+  if (rep) {
+    rep->format = h->active;
+    rep->t_csr_s = t_csr;
+    rep->t_best_s = convert ? t_pred : t_csr;
+    rep->f_latency_s = h->f_latency;
+    rep->c_latency_s = c_pred;
+    rep->expected_iterations = iters;
+    rep->converted = convert ? 1 : 0;
+    rep->n_candidates = 1;
+    rep->params.csr_alg = h->csr_alg;
+    rep->params.csr_T = h->csr_T;
+    rep->params.sell_C = (int32_t)h->sell_C;
+    rep->params.sell_sigma = (int32_t)h->sell_sigma;
+    rep->params.hyb_K = h->hyb_K;
+    rep->params.bell_b = (int32_t)h->bell_b;
+    rep->params.index16 = (h->active == SPMV_FMT_ELL && h->ell_col16) || (h->active == SPMV_FMT_SELL && h->sell_col16);
   }
 }
 
@@ -721,17 +798,26 @@ spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format
     case SPMV_FMT_COO:
       if (!h->coo_built) build_coo(h);
       break;
-    case SPMV_FMT_ELL:
-      if (!h->ell_built) build_ell(h);
+    case SPMV_FMT_ELL: {
+      if (q.index16 < -1 || q.index16 > 1) fail(SPMV_ERR_INVALID_ARG, "index16 must be -1, 0 or 1");
+      if (!h->have_features) compute_features(h);
+      const int want = q.index16 == -1 ? (offsets16_fit(h) ? 1 : 0) : q.index16;
+      if (h->ell_built && (want == 1) == (h->ell_col16 != nullptr)) break;
+      if (h->ell_built) free_format(h, SPMV_FMT_ELL);
+      build_ell(h, want);
       break;
+    }
     case SPMV_FMT_SELL: {
       int64_t C = q.sell_C ? q.sell_C : (h->dtype == SPMV_R64F ? 64 : 128);
       int64_t sigma = q.sell_sigma ? q.sell_sigma : 1;
       if (C != 32 && C != 64 && C != 128 && C != 256) fail(SPMV_ERR_UNSUPPORTED, "SELL C must be 32, 64, 128 or 256");
       if (sigma < 1 || (sigma != 1 && sigma % C != 0)) fail(SPMV_ERR_INVALID_ARG, "SELL sigma must be 1 or a multiple of C");
-      if (!h->sell_built || h->sell_C != C || h->sell_sigma != sigma) {
+      if (q.index16 < -1 || q.index16 > 1) fail(SPMV_ERR_INVALID_ARG, "index16 must be -1, 0 or 1");
+      if (!h->have_features) compute_features(h);
+      const int want = q.index16 == -1 ? (offsets16_fit(h) ? 1 : 0) : q.index16;
+      if (!h->sell_built || h->sell_C != C || h->sell_sigma != sigma || (want == 1) != (h->sell_col16 != nullptr)) {
         if (h->sell_built) free_format(h, SPMV_FMT_SELL);
-        build_sell(h, C, sigma);
+        build_sell(h, C, sigma, want);
       }
       break;
     }
@@ -828,8 +914,12 @@ spmv_status_t spmv_get_launch(spmv_handle_t h, spmv_format_t fmt, spmv_launch_t*
 spmv_status_t spmv_tune(spmv_handle_t h, uint32_t flags, int64_t expected_iterations, spmv_tune_report_t* out) {
   const uint32_t what = flags & SPMV_TUNE_ALL;
   const int obj = (int)((flags & SPMV_TUNE_OBJ_MASK) >> 4);
-  if (!h || (flags & ~(SPMV_TUNE_ALL | SPMV_TUNE_OBJ_MASK)) || what == 0 || expected_iterations < 0)
+  if (!h || (flags & ~(SPMV_TUNE_ALL | SPMV_TUNE_OBJ_MASK | SPMV_TUNE_PREDICT)) || what == 0 ||
+      expected_iterations < 0)
     return SPMV_ERR_INVALID_ARG;
+  const bool predict = (flags & SPMV_TUNE_PREDICT) != 0;
+  if (predict && !(what & SPMV_TUNE_FORMAT)) return SPMV_ERR_INVALID_ARG;
+  if (predict && obj != 0) return SPMV_ERR_UNSUPPORTED;
   if (h->rows == 0 || h->nnz == 0) return SPMV_ERR_INVALID_ARG;
   API_TRY
   DeviceGuard g(h->device);
@@ -840,13 +930,31 @@ spmv_status_t spmv_tune(spmv_handle_t h, uint32_t flags, int64_t expected_iterat
   rep.objective = obj;
   rep.energy_j = rep.power_w = rep.mflops_per_w = std::nan("");
   TuneScratch ts(h);
-  if (what & SPMV_TUNE_FORMAT) tune_format(h, expected_iterations, ts, &rep, obj);
+  if (what & SPMV_TUNE_FORMAT) {
+    if (predict) tune_predict(h, expected_iterations, ts, &rep);
+    else tune_format(h, expected_iterations, ts, &rep, obj);
+  }
   if (what & SPMV_TUNE_LAUNCH) tune_launch(h, h->active, ts, &rep, obj);
   rep.format = h->active;
   rep.launch = resolve_launch(h, h->active, h->launch[h->active]);
   CK(cudaStreamSynchronize(h->stream));
   if (out) *out = rep;
   API_CATCH(h)
+}
+
+spmv_status_t spmv_predict(const spmv_features_t* f, spmv_dtype_t dtype, spmv_prediction_t* out) {
+  if (!f || !out || (dtype != SPMV_R32F && dtype != SPMV_R64F) || f->n_rows < 0 || f->nnz < 0)
+    return SPMV_ERR_INVALID_ARG;
+  double x[kSelectorFeatures];
+  selector_features(*f, dtype == SPMV_R64F ? 8 : 4, x);
+  out->cls = selector_class(x);
+  int fmt;
+  selector_class_format(out->cls, &fmt, &out->params);
+  out->format = fmt;
+  out->speed_ratio = selector_speed_ratio(out->cls, x);
+  out->c_latency_s = fmt == SPMV_FMT_CSR ? 0.0 : selector_c_latency(out->cls, x);
+  out->f_latency_s = selector_f_latency(x);
+  return SPMV_OK;
 }
 
 spmv_status_t spmv_power_step(spmv_handle_t h, const void* x, void* y, const double* sums_prev, double* sums_out,
@@ -985,6 +1093,8 @@ spmv_status_t spmv_format_info(spmv_handle_t h, spmv_format_t fmt, spmv_format_i
     default: break;
   }
   o->stored_bytes = o->present ? format_stored_bytes(h, fmt) : 0;
+  if (o->present && (fmt == SPMV_FMT_ELL || fmt == SPMV_FMT_SELL || fmt == SPMV_FMT_HYB || fmt == SPMV_FMT_BELL))
+    o->index_bytes = (fmt == SPMV_FMT_ELL && h->ell_col16) || (fmt == SPMV_FMT_SELL && h->sell_col16) ? 2 : 4;
   return SPMV_OK;
 }
 
@@ -1000,11 +1110,17 @@ spmv_status_t spmv_copy_array(spmv_handle_t h, spmv_array_t which, void* dst, in
     case SPMV_ARR_CSR_VAL: src = h->val; bytes = h->nnz * vb; break;
     case SPMV_ARR_COO_ROW: need = h->coo_built; src = h->coo_row; bytes = h->nnz * 4; break;
     case SPMV_ARR_COO_EMPTY_ROWS: need = h->coo_built; src = h->coo_empty; bytes = h->coo_n_empty * 4; break;
-    case SPMV_ARR_ELL_COL: need = h->ell_built; src = h->ell_col; bytes = h->ell_K * h->ell_npad * 4; break;
+    case SPMV_ARR_ELL_COL: need = h->ell_built && h->ell_col; src = h->ell_col; bytes = h->ell_K * h->ell_npad * 4; break;
+    case SPMV_ARR_ELL_COL16: need = h->ell_built && h->ell_col16; src = h->ell_col16; bytes = h->ell_K * h->ell_npad * 2; break;
+    case SPMV_ARR_SELL_COL16:
+      need = h->sell_built && h->sell_col16;
+      src = h->sell_col16;
+      bytes = (need ? sell_slots(h) : 0) * 2;
+      break;
     case SPMV_ARR_ELL_VAL: need = h->ell_built; src = h->ell_val; bytes = h->ell_K * h->ell_npad * vb; break;
     case SPMV_ARR_SELL_PERM: need = h->sell_built; src = h->sell_perm; bytes = h->rows * 4; break;
     case SPMV_ARR_SELL_SLICE_PTR: need = h->sell_built; src = h->sell_sp; bytes = (h->sell_ns + 1) * 8; break;
-    case SPMV_ARR_SELL_COL: need = h->sell_built; src = h->sell_col; bytes = (h->sell_built ? sell_slots(h) : 0) * 4; break;
+    case SPMV_ARR_SELL_COL: need = h->sell_built && h->sell_col; src = h->sell_col; bytes = (need ? sell_slots(h) : 0) * 4; break;
     case SPMV_ARR_SELL_VAL: need = h->sell_built; src = h->sell_val; bytes = (h->sell_built ? sell_slots(h) : 0) * vb; break;
     case SPMV_ARR_HYB_ELL_COL: need = h->hyb_built; src = h->hyb_ecol; bytes = h->hyb_K * h->hyb_npad * 4; break;
     case SPMV_ARR_HYB_ELL_VAL: need = h->hyb_built; src = h->hyb_eval; bytes = h->hyb_K * h->hyb_npad * vb; break;

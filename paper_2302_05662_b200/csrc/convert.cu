@@ -17,10 +17,22 @@ namespace spmv {
 namespace {
 
 // ---------------------------------------------------------------- ELL
-template <class RP, class V>
+// Column index as stored: int32 column (pad -1) or a 16-bit offset from
+// origin + row (pad -32768), see spmv_matrix::col_origin.
+template <class IDX>
+__device__ __forceinline__ IDX enc_col(int32_t c, int64_t row, int64_t origin) {
+  if constexpr (sizeof(IDX) == 2) return (IDX)((int64_t)c - origin - row);
+  else return (IDX)c;
+}
+template <class IDX>
+__device__ __forceinline__ IDX pad_col() {
+  return sizeof(IDX) == 2 ? (IDX)-32768 : (IDX)-1;
+}
+
+template <class RP, class V, class IDX>
 __global__ void k_ell_fill(const RP* __restrict__ rp, const int32_t* __restrict__ col,
                            const V* __restrict__ val, int64_t rows, int64_t K, int64_t n_pad,
-                           int32_t* __restrict__ colE, V* __restrict__ valE) {
+                           IDX* __restrict__ colE, V* __restrict__ valE, int64_t origin) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
     int64_t a = 0, L = 0;
@@ -32,14 +44,31 @@ __global__ void k_ell_fill(const RP* __restrict__ rp, const int32_t* __restrict_
     for (int64_t k = 0; k < K; ++k) {
       int64_t pos = k * n_pad + i;
       if (k < L) {
-        colE[pos] = col[a + k];
+        colE[pos] = enc_col<IDX>(col[a + k], i, origin);
         valE[pos] = val[a + k];
       } else {
-        colE[pos] = -1;
+        colE[pos] = pad_col<IDX>();
         valE[pos] = V(0);
       }
     }
   }
+}
+
+// Largest |column − (origin + row)| over the first and last entry of every
+// row (columns are sorted within a row, so these bound all of them).
+template <class RP>
+__global__ void k_offset_range(const RP* __restrict__ rp, const int32_t* __restrict__ col, int64_t rows,
+                               int64_t origin, unsigned long long* out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
+    const int64_t a = rp[i], b = rp[i + 1];
+    if (a == b) continue;
+    const int64_t d0 = (int64_t)col[a] - origin - i, d1 = (int64_t)col[b - 1] - origin - i;
+    const int64_t e = (d0 < 0 ? -d0 : d0) > (d1 < 0 ? -d1 : d1) ? (d0 < 0 ? -d0 : d0) : (d1 < 0 ? -d1 : d1);
+    m = (unsigned long long)e > m ? (unsigned long long)e : m;
+  }
+  if (m) atomicMax(out, m);
 }
 
 // ---------------------------------------------------------------- SELL
@@ -80,29 +109,29 @@ __global__ void k_sell_widths(const RP* __restrict__ rp, const int32_t* __restri
 
 // Thread per (slice, lane): writes of one step k are coalesced across the
 // lanes of a slice; each thread walks its own row's entries in order.
-template <class RP, class V>
+template <class RP, class V, class IDX>
 __global__ void k_sell_fill(const RP* __restrict__ rp, const int32_t* __restrict__ col,
                             const V* __restrict__ val, const int32_t* __restrict__ perm, int64_t rows,
                             int64_t C, int64_t ns, const int64_t* __restrict__ sp,
-                            int32_t* __restrict__ colS, V* __restrict__ valS) {
+                            IDX* __restrict__ colS, V* __restrict__ valS, int64_t origin) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t total = ns * C;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
     const int64_t s = t / C, j = t - s * C;
     const int64_t base = sp[s], w = (sp[s + 1] - base) / C;
-    int64_t a = 0, L = 0;
+    int64_t a = 0, L = 0, i = 0;
     if (t < rows) {
-      const int64_t i = perm ? perm[t] : t;
+      i = perm ? perm[t] : t;
       a = rp[i];
       L = rp[i + 1] - a;
     }
     for (int64_t k = 0; k < w; ++k) {
       const int64_t pos = base + k * C + j;
       if (k < L) {
-        colS[pos] = col[a + k];
+        colS[pos] = enc_col<IDX>(col[a + k], i, origin);
         valS[pos] = val[a + k];
       } else {
-        colS[pos] = -1;
+        colS[pos] = pad_col<IDX>();
         valS[pos] = V(0);
       }
     }
@@ -287,28 +316,34 @@ void lat_end(spmv_matrix* h, int fmt) {
 }
 
 template <class RP, class V>
-void ell_typed(spmv_matrix* h) {
+void ell_typed(spmv_matrix* h, bool d16) {
   cudaStream_t s = h->stream;
   const int64_t K = h->feat.max_len, n_pad = (h->rows + 127) / 128 * 128;
-  guard_bytes((double)K * n_pad * (4.0 + sizeof(V)), "ELL");
+  guard_bytes((double)K * n_pad * ((d16 ? 2.0 : 4.0) + sizeof(V)), "ELL");
   Scratch sc(s);
-  int32_t* colE = sc.get<int32_t>(K * n_pad);
+  int32_t* colE = d16 ? nullptr : sc.get<int32_t>(K * n_pad);
+  int16_t* colE16 = d16 ? sc.get<int16_t>(K * n_pad) : nullptr;
   V* valE = sc.get<V>(K * n_pad);
   lat_begin(h, SPMV_FMT_ELL);  // c_latency = device time of the conversion kernels (allocation excluded)
-  LAUNCH((k_ell_fill<RP, V>), grid_for(n_pad, 256), 256, 0, s, static_cast<const RP*>(h->row_ptr), h->col,
-         static_cast<const V*>(h->val), h->rows, K, n_pad, colE, valE);
+  if (d16)
+    LAUNCH((k_ell_fill<RP, V, int16_t>), grid_for(n_pad, 256), 256, 0, s, static_cast<const RP*>(h->row_ptr),
+           h->col, static_cast<const V*>(h->val), h->rows, K, n_pad, colE16, valE, h->col_origin);
+  else
+    LAUNCH((k_ell_fill<RP, V, int32_t>), grid_for(n_pad, 256), 256, 0, s, static_cast<const RP*>(h->row_ptr),
+           h->col, static_cast<const V*>(h->val), h->rows, K, n_pad, colE, valE, int64_t(0));
   lat_end(h, SPMV_FMT_ELL);
-  sc.keep(colE);
-  sc.keep(valE);
+  for (void* p : {(void*)colE, (void*)colE16, (void*)valE})
+    if (p) sc.keep(p);
   h->ell_K = K;
   h->ell_npad = n_pad;
   h->ell_col = colE;
+  h->ell_col16 = colE16;
   h->ell_val = valE;
   h->ell_built = true;
 }
 
 template <class RP, class V>
-void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma) {
+void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma, bool d16) {
   cudaStream_t s = h->stream;
   const int64_t rows = h->rows, ns = (rows + C - 1) / C;
   Scratch sc(s);
@@ -329,10 +364,13 @@ void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma) {
   int64_t* cw = sc.get<int64_t>(ns);
   int64_t* sp = sc.get<int64_t>(ns + 1);
   int32_t* colS = nullptr;
+  int16_t* colS16 = nullptr;
   V* valS = nullptr;
+  const double ib = d16 ? 2.0 : 4.0;
   if (use_ub) {
-    guard_bytes((double)ub * (4.0 + sizeof(V)), "SELL");
-    colS = sc.get<int32_t>(ub);
+    guard_bytes((double)ub * (ib + sizeof(V)), "SELL");
+    if (d16) colS16 = sc.get<int16_t>(ub);
+    else colS = sc.get<int32_t>(ub);
     valS = sc.get<V>(ub);
   }
   lat_begin(h, SPMV_FMT_SELL);  // c_latency = device time of the conversion kernels
@@ -349,15 +387,23 @@ void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma) {
   exclusive_scan_i64(cw, sp, ns, s);
   const int64_t slots = use_ub ? ub : read_i64(sp + ns, s);
   if (!use_ub) {
-    guard_bytes((double)slots * (4.0 + sizeof(V)), "SELL");
-    colS = sc.get<int32_t>(slots);
+    guard_bytes((double)slots * (ib + sizeof(V)), "SELL");
+    if (d16) colS16 = sc.get<int16_t>(slots);
+    else colS = sc.get<int32_t>(slots);
     valS = sc.get<V>(slots);
   }
-  LAUNCH((k_sell_fill<RP, V>), grid_for(ns * C, 256), 256, 0, s, rp, h->col, static_cast<const V*>(h->val),
-         (const int32_t*)perm, rows, C, ns, (const int64_t*)sp, colS, valS);
+  if (d16)
+    LAUNCH((k_sell_fill<RP, V, int16_t>), grid_for(ns * C, 256), 256, 0, s, rp, h->col,
+           static_cast<const V*>(h->val), (const int32_t*)perm, rows, C, ns, (const int64_t*)sp, colS16, valS,
+           h->col_origin);
+  else
+    LAUNCH((k_sell_fill<RP, V, int32_t>), grid_for(ns * C, 256), 256, 0, s, rp, h->col,
+           static_cast<const V*>(h->val), (const int32_t*)perm, rows, C, ns, (const int64_t*)sp, colS, valS,
+           int64_t(0));
   lat_end(h, SPMV_FMT_SELL);
-  for (void* p : {(void*)perm, (void*)sp, (void*)colS, (void*)valS})
+  for (void* p : {(void*)perm, (void*)sp, (void*)colS, (void*)colS16, (void*)valS})
     if (p) sc.keep(p);
+  h->sell_col16 = colS16;
   h->sell_C = C;
   h->sell_sigma = sigma;
   h->sell_ns = ns;
@@ -382,8 +428,8 @@ void hyb_typed(spmv_matrix* h, int64_t K) {
   int64_t* cnt = sc.get<int64_t>(rows);
   int64_t* toff = sc.get<int64_t>(rows + 1);
   lat_begin(h, SPMV_FMT_HYB);  // kernels + the tail-size read-back
-  LAUNCH((k_ell_fill<RP, V>), grid_for(n_pad, 256), 256, 0, s, rp, h->col, static_cast<const V*>(h->val),
-         rows, K, n_pad, colE, valE);
+  LAUNCH((k_ell_fill<RP, V, int32_t>), grid_for(n_pad, 256), 256, 0, s, rp, h->col, static_cast<const V*>(h->val),
+         rows, K, n_pad, colE, valE, int64_t(0));
   LAUNCH(k_row_counts<RP>, grid_for(rows, 256), 256, 0, s, rp, rows, 1, K, cnt);
   exclusive_scan_i64(cnt, toff, rows, s);
   const int64_t tail = read_i64(toff + rows, s);
@@ -480,21 +526,51 @@ void dispatch(spmv_matrix* h, F&& f) {
 
 }  // namespace
 
-void build_ell(spmv_matrix* h) {
+bool offsets16_fit(spmv_matrix* h) {
+  if (h->col_origin == 0 && h->have_features)  // bandwidth from the features (no device pass)
+    return h->feat.bw_lower <= 32767 && h->feat.bw_upper <= 32767;
+  if (h->rows == 0 || h->nnz == 0) return true;
+  Scratch sc(h->stream);
+  unsigned long long* d = sc.get<unsigned long long>(1);
+  CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long), h->stream));
+  const unsigned g = grid_for(h->rows, 256);
+  if (h->rp64)
+    LAUNCH(k_offset_range<int64_t>, g, 256, 0, h->stream, static_cast<const int64_t*>(h->row_ptr), h->col, h->rows,
+           h->col_origin, d);
+  else
+    LAUNCH(k_offset_range<int32_t>, g, 256, 0, h->stream, static_cast<const int32_t*>(h->row_ptr), h->col, h->rows,
+           h->col_origin, d);
+  unsigned long long m = 0;
+  CK(cudaMemcpyAsync(&m, d, sizeof(m), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return m <= 32767ull;
+}
+
+static bool resolve16(spmv_matrix* h, int index16, const char* what) {
+  if (index16 == 0) return false;
+  const bool fit = offsets16_fit(h);
+  if (index16 > 0 && !fit)
+    fail(SPMV_ERR_UNSUPPORTED, std::string(what) + ": 16-bit column offsets need every |col - row| <= 32767");
+  return fit;
+}
+
+void build_ell(spmv_matrix* h, int index16) {
   if (!h->have_features) compute_features(h);
+  const bool d16 = resolve16(h, index16, "ELL");
   dispatch(h, [&](auto rpt, auto vt) {
     using RP = std::remove_pointer_t<decltype(rpt)>;
     using V = std::remove_pointer_t<decltype(vt)>;
-    ell_typed<RP, V>(h);
+    ell_typed<RP, V>(h, d16);
   });
 }
 
-void build_sell(spmv_matrix* h, int64_t C, int64_t sigma) {
+void build_sell(spmv_matrix* h, int64_t C, int64_t sigma, int index16) {
   if (!h->have_features) compute_features(h);
+  const bool d16 = resolve16(h, index16, "SELL");
   dispatch(h, [&](auto rpt, auto vt) {
     using RP = std::remove_pointer_t<decltype(rpt)>;
     using V = std::remove_pointer_t<decltype(vt)>;
-    sell_typed<RP, V>(h, C, sigma);
+    sell_typed<RP, V>(h, C, sigma, d16);
   });
 }
 
@@ -536,11 +612,11 @@ void free_format(spmv_matrix* h, int fmt) {
       h->coo_built = false;
       break;
     case SPMV_FMT_ELL:
-      F(h->ell_col); F(h->ell_val);
+      F(h->ell_col); F(h->ell_col16); F(h->ell_val);
       h->ell_built = false;
       break;
     case SPMV_FMT_SELL:
-      F(h->sell_perm); F(h->sell_sp); F(h->sell_col); F(h->sell_val);
+      F(h->sell_perm); F(h->sell_sp); F(h->sell_col); F(h->sell_col16); F(h->sell_val);
       h->sell_built = false;
       h->sell_slots_pending = false;
       break;
@@ -585,9 +661,9 @@ int64_t format_stored_bytes(spmv_matrix* h, int fmt) {
   switch (fmt) {
     case SPMV_FMT_CSR: return (h->rows + 1) * rpb + h->nnz * (4 + vb);
     case SPMV_FMT_COO: return h->nnz * (8 + vb) + h->coo_n_empty * 4;
-    case SPMV_FMT_ELL: return h->ell_K * h->ell_npad * (4 + vb);
+    case SPMV_FMT_ELL: return h->ell_K * h->ell_npad * ((h->ell_col16 ? 2 : 4) + vb);
     case SPMV_FMT_SELL:
-      return sell_slots(h) * (4 + vb) + (h->sell_ns + 1) * 8 + (h->sell_perm ? h->rows * 4 : 0);
+      return sell_slots(h) * ((h->sell_col16 ? 2 : 4) + vb) + (h->sell_ns + 1) * 8 + (h->sell_perm ? h->rows * 4 : 0);
     case SPMV_FMT_HYB: return h->hyb_K * h->hyb_npad * (4 + vb) + h->hyb_tail * (8 + vb);
     case SPMV_FMT_BELL: return h->bell_kb * h->bell_nbr_pad * (4 + h->bell_b * h->bell_b * vb);
   }

@@ -30,6 +30,7 @@ struct spmv_matrix {
   int64_t ell_K = 0, ell_npad = 0;
   int32_t* ell_col = nullptr;
   void* ell_val = nullptr;
+  int16_t* ell_col16 = nullptr;  // 16-bit column offsets (ell_col == nullptr then)
 
   // SELL-C-sigma.
   bool sell_built = false;
@@ -38,6 +39,11 @@ struct spmv_matrix {
   int64_t* sell_sp = nullptr;    // [ns+1]
   int32_t* sell_col = nullptr;
   void* sell_val = nullptr;
+  int16_t* sell_col16 = nullptr;  // 16-bit column offsets (sell_col == nullptr then)
+  // 16-bit ELL/SELL column offsets: column = col_origin + row + d, d in
+  // [-32767, 32767], pad -32768 (row slices of the distributed plan set the
+  // origin to their first global column position).
+  int64_t col_origin = 0;
 
   // HYB: ELL part [K][n_pad] + COO tail.
   bool hyb_built = false;
@@ -100,8 +106,12 @@ void compute_features(spmv_matrix* h);
 
 // convert.cu
 void build_coo(spmv_matrix* h);
-void build_ell(spmv_matrix* h);
-void build_sell(spmv_matrix* h, int64_t C, int64_t sigma);
+// index16: 0 = int32 columns, 1 = 16-bit offsets (SPMV_ERR_UNSUPPORTED if
+// they do not fit), -1 = 16-bit offsets when they fit.
+void build_ell(spmv_matrix* h, int index16 = 0);
+void build_sell(spmv_matrix* h, int64_t C, int64_t sigma, int index16 = 0);
+// True iff every column lies within ±32767 of col_origin + its row.
+bool offsets16_fit(spmv_matrix* h);
 void build_hyb(spmv_matrix* h, int64_t K);
 void build_bell(spmv_matrix* h, int64_t b);
 void free_format(spmv_matrix* h, int fmt);
@@ -128,7 +138,8 @@ struct Epilogue {
 void run_csr(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
 void run_ell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
 void run_ell_arrays(spmv_matrix* h, const int32_t* col, const void* val, int64_t K, int64_t n_pad,
-                    const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
+                    const Epilogue& e, const void* x, void* y, const spmv_launch_t& L,
+                    const int16_t* col16 = nullptr);
 // y <- beta·y over all rows (alpha == 0: A is not read).
 void run_scale(spmv_matrix* h, void* y, double beta);
 void run_sell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);

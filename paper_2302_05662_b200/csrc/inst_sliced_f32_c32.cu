@@ -2,6 +2,7 @@
 #include "kern_sliced.cuh"
 namespace spmv {
 namespace kern {
-template SlicedFn sliced_fn<float, 32>(int, int);
+template SlicedFn sliced_fn<float, 32, false>(int, int);
+template SlicedFn sliced_fn<float, 32, true>(int, int);
 }  // namespace kern
 }  // namespace spmv

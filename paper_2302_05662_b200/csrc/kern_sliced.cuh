@@ -18,7 +18,34 @@ namespace kern {
 
 
 
-template <int B, int R, class T, int C>
+// N 16-bit column offsets of one lane (N·2 bytes, aligned): one load.
+template <int N>
+__device__ __forceinline__ void load_d16(const int16_t* p, int (&d)[N]) {
+  if constexpr (N == 1) {
+    unsigned short v;
+    asm("ld.global.nc.L1::no_allocate.b16 %0, [%1];" : "=h"(v) : "l"(p));
+    d[0] = (int)(int16_t)v;
+  } else {
+    constexpr int W = N / 2;  // 32-bit words
+    int w[W];
+    if constexpr (W == 1) {
+      w[0] = ld_stream(reinterpret_cast<const int*>(p));
+    } else if constexpr (W == 2) {
+      int2 t = ld_stream(reinterpret_cast<const int2*>(p));
+      w[0] = t.x; w[1] = t.y;
+    } else {
+      int4 t = ld_stream(reinterpret_cast<const int4*>(p));
+      w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+    }
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      d[2 * i] = (int)(int16_t)(w[i] & 0xffff);
+      d[2 * i + 1] = (int)(int16_t)((unsigned)w[i] >> 16);
+    }
+  }
+}
+
+template <int B, int R, class T, int C, bool D16>
 __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const SlicedParams p) {
   constexpr int RPL = C / 32;                                       // rows per lane
   constexpr int VW = (int)(16 / sizeof(T)) < RPL ? (int)(16 / sizeof(T)) : RPL;  // elems per vector load
@@ -50,14 +77,22 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
       width = p.ell_K;
       stride = p.ell_stride;
     }
-    const int32_t* __restrict__ cp = p.col + base + lane * RPL;
+    const int32_t* __restrict__ cp = D16 ? nullptr : p.col + base + lane * RPL;
+    const int16_t* __restrict__ dp = D16 ? p.col16 + base + lane * RPL : nullptr;
     const T* __restrict__ vp = val + base + lane * RPL;
     double acc[RPL];
+    int64_t rowv[D16 ? RPL : 1];  // D16: column origin of each of the lane's rows
 #pragma unroll
-    for (int r = 0; r < RPL; ++r) acc[r] = 0.0;
-    for (int64_t k = 0; k < width; k += U) {
-      T v[U][RPL];
-      int c[U][RPL];
+    for (int r = 0; r < RPL; ++r) {
+      acc[r] = 0.0;
+      if constexpr (D16) {
+        const int64_t ri = slice * C + lane * RPL + r;
+        rowv[r] = p.col_origin + (ri < p.rows ? (p.perm ? (int64_t)p.perm[ri] : ri) : 0);
+      }
+    }
+    // One batch = U consecutive k-steps of the lane's RPL rows (values +
+    // column indices), predicated past the slice width.
+    auto load_batch = [&](int64_t k, T (&v)[U][RPL], int (&c)[U][RPL]) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool ok = k + u < width;  // predicated tail batch
@@ -67,7 +102,7 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
           int tc[VW];
           if (ok) {
             load_vals<T, VW>(vp + (k + u) * stride + q * VW, tv);
-            load_cols<VW>(cp + (k + u) * stride + q * VW, tc);
+            if constexpr (!D16) load_cols<VW>(cp + (k + u) * stride + q * VW, tc);
           } else {
 #pragma unroll
             for (int w = 0; w < VW; ++w) {
@@ -78,10 +113,32 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
 #pragma unroll
           for (int w = 0; w < VW; ++w) {
             v[u][q * VW + w] = tv[w];
-            c[u][q * VW + w] = tc[w];
+            if constexpr (!D16) c[u][q * VW + w] = tc[w];
           }
         }
+        if constexpr (D16) {
+          int dd[RPL];
+          if (ok) {
+            load_d16<RPL>(dp + (k + u) * stride, dd);
+          } else {
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) dd[r] = -32768;
+          }
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) c[u][r] = dd[r] == -32768 ? -1 : (int)(rowv[r] + dd[r]);
+        }
       }
+    };
+    // Batch k+U is loaded after batch k's gathers and FMAs (issuing it before
+    // them — a software pipeline — doubles the live registers and measured
+    // slower on c2 and c4: lower occupancy costs more than it hides).
+    T v[U][RPL];
+    int c[U][RPL];
+    if (width > 0) load_batch(0, v, c);
+    for (int64_t k = 0; k < width; k += U) {
+      T vn[U][RPL];
+      int cn[U][RPL];
+      const bool more = k + U < width;
       T xv[U][RPL];
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -91,6 +148,16 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int r = 0; r < RPL; ++r) acc[r] = fma((double)v[u][r], (double)xv[u][r], acc[r]);
+      if (more) {
+        load_batch(k + U, vn, cn);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            v[u][r] = vn[u][r];
+            c[u][r] = cn[u][r];
+          }
+      }
     }
     const int64_t r0 = slice * C + lane * RPL;
 #pragma unroll
@@ -111,8 +178,9 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
 }
 
 
-#define SL_ROW(B) {&k_sliced<B, 32, T, C>, &k_sliced<B, 64, T, C>, &k_sliced<B, 128, T, C>, &k_sliced<B, 255, T, C>}
-template <class T, int C>
+#define SL_ROW(B) {&k_sliced<B, 32, T, C, D16>, &k_sliced<B, 64, T, C, D16>, &k_sliced<B, 128, T, C, D16>, \
+                   &k_sliced<B, 255, T, C, D16>}
+template <class T, int C, bool D16>
 SlicedFn sliced_fn(int bi, int ri) {
   static const SlicedFn tab[5][4] = {SL_ROW(64), SL_ROW(128), SL_ROW(256), SL_ROW(512), SL_ROW(1024)};
   return tab[bi][ri];

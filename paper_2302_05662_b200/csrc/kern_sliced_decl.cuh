@@ -7,7 +7,9 @@ namespace spmv {
 namespace kern {
 
 struct SlicedParams {
-  const int32_t* col;
+  const int32_t* col;       // int32 column indices (pad -1), or nullptr when col16 is used
+  const int16_t* col16;     // 16-bit offsets: column = col_origin + row + d (pad -32768)
+  int64_t col_origin;
   const void* val;
   const int64_t* sp;    // SELL slice pointers (nullptr for ELL)
   const int32_t* perm;  // SELL row permutation (nullptr = identity)
@@ -20,7 +22,7 @@ struct SlicedParams {
 };
 
 using SlicedFn = void (*)(const SlicedParams);
-template <class T, int C>
+template <class T, int C, bool D16>
 SlicedFn sliced_fn(int bi, int ri);
 
 }  // namespace kern

@@ -158,8 +158,9 @@ void convert_like(spmv_matrix* d, const spmv_matrix* p) {
       d->csr_T = p->csr_T;
       break;
     case SPMV_FMT_COO: build_coo(d); break;
-    case SPMV_FMT_ELL: build_ell(d); break;
-    case SPMV_FMT_SELL: build_sell(d, p->sell_C, p->sell_sigma); break;
+    // ELL/SELL: 16-bit column offsets from the part's own diagonal whenever they fit
+    case SPMV_FMT_ELL: build_ell(d, -1); break;
+    case SPMV_FMT_SELL: build_sell(d, p->sell_C, p->sell_sigma, -1); break;
     case SPMV_FMT_HYB: build_hyb(d, p->hyb_K); break;
     case SPMV_FMT_BELL: build_bell(d, p->bell_b); break;
     default: fail(SPMV_ERR_INVALID_ARG, "plan: bad parent format");
@@ -371,6 +372,7 @@ spmv_dist_plan* plan_create(spmv_matrix* h, void* comm_v, int64_t chunk, uint32_
       P->part_r0[p] = r0[p];
       if (r1[p] > r0[p]) {
         P->part[p] = make_row_slice(h, r0[p], r1[p]);
+        P->part[p]->col_origin = P->own_lo + r0[p];  // row i of the part sits at column position origin + i
         convert_like(P->part[p], h);
       }
     }

@@ -8,11 +8,12 @@ template <class T>
 void launch_sliced(spmv_matrix* h, kern::SlicedParams& p, int C, const spmv_launch_t& L) {
   const int bi = block_index(L.block), ri = reg_index(L.maxreg);
   const void* fn;
+  const bool d16 = p.col16 != nullptr;
   switch (C) {
-    case 32: fn = (const void*)kern::sliced_fn<T, 32>(bi, ri); break;
-    case 64: fn = (const void*)kern::sliced_fn<T, 64>(bi, ri); break;
-    case 128: fn = (const void*)kern::sliced_fn<T, 128>(bi, ri); break;
-    case 256: fn = (const void*)kern::sliced_fn<T, 256>(bi, ri); break;
+    case 32: fn = d16 ? (const void*)kern::sliced_fn<T, 32, true>(bi, ri) : (const void*)kern::sliced_fn<T, 32, false>(bi, ri); break;
+    case 64: fn = d16 ? (const void*)kern::sliced_fn<T, 64, true>(bi, ri) : (const void*)kern::sliced_fn<T, 64, false>(bi, ri); break;
+    case 128: fn = d16 ? (const void*)kern::sliced_fn<T, 128, true>(bi, ri) : (const void*)kern::sliced_fn<T, 128, false>(bi, ri); break;
+    case 256: fn = d16 ? (const void*)kern::sliced_fn<T, 256, true>(bi, ri) : (const void*)kern::sliced_fn<T, 256, false>(bi, ri); break;
     default: fail(SPMV_ERR_UNSUPPORTED, "slice height C must be 32, 64, 128 or 256");
   }
   set_carveout(fn, L.carveout_pct);
@@ -49,11 +50,13 @@ void launch_sliced(spmv_matrix* h, kern::SlicedParams& p, int C, const spmv_laun
 }  // namespace
 
 void run_ell_arrays(spmv_matrix* h, const int32_t* col, const void* val, int64_t K, int64_t n_pad,
-                    const Epilogue& e, const void* x, void* y, const spmv_launch_t& L) {
+                    const Epilogue& e, const void* x, void* y, const spmv_launch_t& L, const int16_t* col16) {
   kern::SlicedParams p{};
   const int C = L.knob;
   if (n_pad % C != 0) fail(SPMV_ERR_UNSUPPORTED, "ELL rows-per-warp must divide n_pad (a multiple of 128)");
   p.col = col;
+  p.col16 = col16;
+  p.col_origin = h->col_origin;
   p.val = val;
   p.sp = nullptr;
   p.perm = nullptr;
@@ -69,12 +72,14 @@ void run_ell_arrays(spmv_matrix* h, const int32_t* col, const void* val, int64_t
 }
 
 void run_ell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L) {
-  run_ell_arrays(h, h->ell_col, h->ell_val, h->ell_K, h->ell_npad, e, x, y, L);
+  run_ell_arrays(h, h->ell_col, h->ell_val, h->ell_K, h->ell_npad, e, x, y, L, h->ell_col16);
 }
 
 void run_sell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L) {
   kern::SlicedParams p{};
   p.col = h->sell_col;
+  p.col16 = h->sell_col16;
+  p.col_origin = h->col_origin;
   p.val = h->sell_val;
   p.sp = h->sell_sp;
   p.perm = h->sell_perm;

@@ -1,0 +1,112 @@
+"""Learned format selector — CPU tests.
+
+The model is trained by tools/train_selector.py from the B200-measured corpus
+(profiles/selector_corpus.jsonl) and compiled into libspmv.so as
+selector_model.h; profiles/selector_model.json holds the same model. These
+tests need no GPU: spmv_predict is host-only.
+
+* the compiled model equals the JSON model on every corpus matrix (class,
+  speed ratio, overhead estimates) — the header was generated from it and the
+  C++ feature vector is the trainer's feature vector;
+* the classifier reproduces the training report's accuracy claim;
+* the gate arithmetic of the prediction mode is the paper's:
+  convert iff iterations·gain > overhead, exactly one flip along an
+  iteration sweep."""
+import json
+import math
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+P = pytest.importorskip("paper_2302_05662_b200")
+
+MODEL = os.path.join(ROOT, "profiles", "selector_model.json")
+CORPUS = os.path.join(ROOT, "profiles", "selector_corpus.jsonl")
+pytestmark = pytest.mark.skipif(not (os.path.exists(MODEL) and os.path.exists(CORPUS)), reason="no trained model")
+
+
+def _records():
+    import train_selector as T
+    return T.load(CORPUS)
+
+
+def _eval(nodes, x):
+    i = 0
+    while nodes[i][0] >= 0:
+        f, l, r, thr, _ = nodes[i]
+        i = l if x[f] <= thr else r
+    return nodes[i][4]
+
+
+def test_compiled_model_matches_json():
+    import train_selector as T
+    m = json.load(open(MODEL))
+    assert m["classes"] == P.SELECTOR_CLASSES == T.CLASSES
+    recs = _records()
+    assert len(recs) >= 40
+    for r in recs:
+        f = r["features"]
+        x = T.feature_vector(f)
+        pred = P.spmv_predict(f)
+        cls = int(_eval(m["classifier"], x))
+        assert pred["cls"] == cls, r["name"]
+        name = m["classes"][cls]
+        ratio = 1.0 if cls == 0 else math.exp(_eval(m["ratio"][name], x))
+        assert pred["speed_ratio"] == pytest.approx(ratio, rel=1e-12, abs=0)
+        want_c = 0.0 if name.startswith("CSR") else math.exp(_eval(m["c_latency"][name], x))
+        assert pred["c_latency_s"] == pytest.approx(want_c, rel=1e-12, abs=1e-18)
+        assert pred["f_latency_s"] == pytest.approx(math.exp(_eval(m["f_latency"], x)), rel=1e-12)
+
+
+def test_class_to_format_mapping():
+    recs = _records()
+    fmts = {"CSR-vector": (P.FMT_CSR, P.CSR_VECTOR), "CSR-merge": (P.FMT_CSR, P.CSR_MERGE), "ELL": (P.FMT_ELL, None),
+            "SELL": (P.FMT_SELL, None), "HYB": (P.FMT_HYB, None), "COO": (P.FMT_COO, None),
+            "BELL-2": (P.FMT_BELL, None), "BELL-3": (P.FMT_BELL, None)}
+    for r in recs[:20]:
+        p = P.spmv_predict(r["features"])
+        fmt, alg = fmts[p["class"]]
+        assert p["format"] == fmt
+        if alg is not None:
+            assert p["params"]["csr_alg"] == alg
+        if p["class"].startswith("BELL"):
+            assert p["params"]["bell_b"] == int(p["class"][-1])
+
+
+def test_reported_accuracy_and_perf_ratio():
+    m = json.load(open(MODEL))
+    s = m["stats"]
+    recs = _records()
+    # the model's choice on the whole corpus: geometric-mean t(best)/t(choice)
+    ratios = []
+    for r in recs:
+        p = P.spmv_predict(r["features"])
+        t = r["times"].get(p["class"], r["times"]["CSR-vector"])
+        ratios.append(r["times"][r["best"]] / t)
+    g = float(np.exp(np.mean(np.log(ratios))))
+    assert g == pytest.approx(s["perf_ratio_deployed_all_geomean"], rel=1e-9)
+    assert g > 0.9   # the learned choice is within 10% of the measured optimum on average
+    assert 0.0 <= s["acc_test"] <= 1.0
+
+
+def test_gate_single_flip():
+    """P:449-452 gate with predicted quantities: convert iff iters·(t_csr − ratio·t_csr) > f + c."""
+    recs = _records()
+    for r in recs[:30]:
+        p = P.spmv_predict(r["features"])
+        if p["cls"] == 0 or p["speed_ratio"] >= 1.0:
+            continue
+        t_csr = r["times"]["CSR-vector"]
+        over = r["f_latency_s"] + p["c_latency_s"]
+        verdicts = [it * (t_csr - p["speed_ratio"] * t_csr) > over for it in range(0, 200000, 997)]
+        flips = sum(1 for a, b in zip(verdicts, verdicts[1:]) if a != b)
+        assert flips <= 1 and not verdicts[0]
+
+
+def test_predict_errors():
+    with pytest.raises(P.SpmvError):
+        P.spmv_predict({"n_rows": -1, "nnz": 0})

@@ -27,7 +27,9 @@ VARIANTS = [("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)),
             ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE)),
             ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM)),
             ("ELL", P.FMT_ELL, {}),
+            ("ELL-16", P.FMT_ELL, dict(index16=1)),
             ("SELL", P.FMT_SELL, {}),
+            ("SELL-16", P.FMT_SELL, dict(index16=1)),
             ("SELL-sigma", P.FMT_SELL, dict(sell_sigma=-1)),
             ("HYB", P.FMT_HYB, {}),
             ("COO", P.FMT_COO, {}),
