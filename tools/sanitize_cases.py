@@ -18,7 +18,9 @@ from gpu_cases import corpus  # noqa: E402
 FMTS = [(P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)), (P.FMT_CSR, dict(csr_alg=P.CSR_SCALAR)),
         (P.FMT_CSR, dict(csr_alg=P.CSR_MERGE)), (P.FMT_ELL, {}), (P.FMT_SELL, {}),
         (P.FMT_SELL, dict(sell_C=32, sell_sigma=64)), (P.FMT_HYB, {}), (P.FMT_COO, {}),
-        (P.FMT_CSR, dict(csr_alg=P.CSR_STREAM)), (P.FMT_BELL, dict(bell_b=2)), (P.FMT_BELL, dict(bell_b=3))]
+        (P.FMT_CSR, dict(csr_alg=P.CSR_STREAM)), (P.FMT_BELL, dict(bell_b=2)), (P.FMT_BELL, dict(bell_b=3)),
+        (P.FMT_ELL, dict(index16=-1)), (P.FMT_SELL, dict(index16=-1)), (P.FMT_SELL, dict(sell_C=32, sell_sigma=64,
+                                                                                       index16=-1))]
 
 
 def main():
@@ -57,7 +59,19 @@ def main():
                       torch.from_numpy(coo.val).cuda())
     P.spmv_tune(h, P.TUNE_FORMAT, 100)
     P.spmv_destroy(h)
+    h = P.spmv_create(coo.rows, coo.cols, torch.from_numpy(coo.row).cuda(), torch.from_numpy(coo.col).cuda(),
+                      torch.from_numpy(coo.val).cuda())
+    P.spmv_tune(h, P.TUNE_FORMAT | P.TUNE_PREDICT, 100)
+    P.spmv_destroy(h)
     print("ok tune")
+    # distributed plan: 3 in-process ranks, overlap + halo lists, direct and staged exchange
+    from test_gpu_plan import run_plan
+    for staged in ("0", "1"):
+        os.environ["SPMV_PLAN_FORCE_STAGED"] = staged
+        for flags in (P.PLAN_OVERLAP | P.PLAN_HALO, 0):
+            run_plan(si.stencil27(8, random_values=True), 3, flags, [2], P.FMT_SELL, {"index16": -1})
+    os.environ.pop("SPMV_PLAN_FORCE_STAGED", None)
+    print("ok plan")
 
 
 if __name__ == "__main__":
