@@ -111,7 +111,9 @@ typedef struct {
   int32_t block;        /* 64, 128, 256, 512, 1024 */
   int32_t maxreg;       /* 32, 64, 128, 255 */
   int32_t carveout_pct; /* -1 = driver default, else 0..100 */
-  int32_t knob;
+  int32_t knob;         /* CSR-vector: lanes per row; merge-path: items per thread; COO/HYB: entries
+                           per lane; ELL: rows per warp (32/64/128/256) in the low 16 bits; ELL and
+                           SELL: bit 16 (65536) selects the carried-batch loop (see kern_sliced.cuh) */
 } spmv_launch_t;
 
 /* spmv_tune flags */

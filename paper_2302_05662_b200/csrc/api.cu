@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "dist.cuh"
+#include "kern_sliced_decl.cuh"
 #include "selector.cuh"
 #include "spmv_common.cuh"
 
@@ -154,8 +155,8 @@ spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t&
         else if (h->csr_alg == SPMV_CSR_SCALAR) r.knob = 1;
         else r.knob = csr_default_lanes(h);
         break;
-      case SPMV_FMT_ELL: r.knob = h->dtype == SPMV_R64F ? 64 : 128; break;
-      case SPMV_FMT_SELL: r.knob = (int)h->sell_C; break;
+      case SPMV_FMT_ELL: r.knob = (h->dtype == SPMV_R64F ? 64 : 128) | kern::kSlicedCarry; break;
+      case SPMV_FMT_SELL: r.knob = (int)h->sell_C | kern::kSlicedCarry; break;
       case SPMV_FMT_COO: r.knob = 4; break;
       case SPMV_FMT_HYB: r.knob = 4; break;
       case SPMV_FMT_BELL: r.knob = (int)h->bell_b; break;
@@ -349,9 +350,9 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
         if (t * 2 <= 32) v.push_back(t * 2);
         return v;
       }
-    case SPMV_FMT_ELL:
-      return h->dtype == SPMV_R64F ? std::vector<int>{32, 64, 128} : std::vector<int>{32, 64, 128};
-    case SPMV_FMT_SELL: return {(int)h->sell_C};
+    case SPMV_FMT_ELL:  // rows per warp × batch loop (kern::kSlicedCarry)
+      return {32, 64, 128, 32 | kern::kSlicedCarry, 64 | kern::kSlicedCarry, 128 | kern::kSlicedCarry};
+    case SPMV_FMT_SELL: return {(int)h->sell_C, (int)h->sell_C | kern::kSlicedCarry};
     case SPMV_FMT_COO: return {2, 4, 8};
     case SPMV_FMT_HYB: return {2, 4, 8};
     case SPMV_FMT_BELL: return {(int)h->bell_b};

@@ -45,7 +45,12 @@ __device__ __forceinline__ void load_d16(const int16_t* p, int (&d)[N]) {
   }
 }
 
-template <int B, int R, class T, int C, bool D16>
+// CARRY selects the batch loop (a launch-tuner knob, SPMV_SLICED_CARRY):
+//  CARRY = 1: batch k+U is loaded under a branch after batch k's FMAs and
+//             carried in registers (fastest on stencils: c2 ELL-16 96 µs);
+//  CARRY = 0: the batch load is unconditional and predicated per k-step
+//             (fastest on scattered gathers: c4 ELL 539 vs 564 µs).
+template <int B, int R, class T, int C, bool D16, bool CARRY>
 __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const SlicedParams p) {
   constexpr int RPL = C / 32;                                       // rows per lane
   constexpr int VW = (int)(16 / sizeof(T)) < RPL ? (int)(16 / sizeof(T)) : RPL;  // elems per vector load
@@ -132,13 +137,13 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
     // Batch k+U is loaded after batch k's gathers and FMAs (issuing it before
     // them — a software pipeline — doubles the live registers and measured
     // slower on c2 and c4: lower occupancy costs more than it hides).
+    // CARRY = 1 guards the reload with a branch, CARRY = 0 predicates it.
     T v[U][RPL];
     int c[U][RPL];
     if (width > 0) load_batch(0, v, c);
     for (int64_t k = 0; k < width; k += U) {
       T vn[U][RPL];
       int cn[U][RPL];
-      const bool more = k + U < width;
       T xv[U][RPL];
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -148,8 +153,8 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int r = 0; r < RPL; ++r) acc[r] = fma((double)v[u][r], (double)xv[u][r], acc[r]);
-      if (more) {
-        load_batch(k + U, vn, cn);
+      if (!CARRY || k + U < width) {
+        load_batch(k + U, vn, cn);  // predicated: nothing is read past the width
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -178,9 +183,9 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
 }
 
 
-#define SL_ROW(B) {&k_sliced<B, 32, T, C, D16>, &k_sliced<B, 64, T, C, D16>, &k_sliced<B, 128, T, C, D16>, \
-                   &k_sliced<B, 255, T, C, D16>}
-template <class T, int C, bool D16>
+#define SL_ROW(B) {&k_sliced<B, 32, T, C, D16, CARRY>, &k_sliced<B, 64, T, C, D16, CARRY>, \
+                   &k_sliced<B, 128, T, C, D16, CARRY>, &k_sliced<B, 255, T, C, D16, CARRY>}
+template <class T, int C, bool D16, bool CARRY>
 SlicedFn sliced_fn(int bi, int ri) {
   static const SlicedFn tab[5][4] = {SL_ROW(64), SL_ROW(128), SL_ROW(256), SL_ROW(512), SL_ROW(1024)};
   return tab[bi][ri];

@@ -22,8 +22,10 @@ struct SlicedParams {
 };
 
 using SlicedFn = void (*)(const SlicedParams);
-template <class T, int C, bool D16>
+template <class T, int C, bool D16, bool CARRY>
 SlicedFn sliced_fn(int bi, int ri);
+// launch knob flag of ELL/SELL: the carried-batch loop (see k_sliced)
+constexpr int kSlicedCarry = 1 << 16;
 
 }  // namespace kern
 }  // namespace spmv

@@ -9,6 +9,7 @@
 // inside the chunk are written by the chunk; rows crossing chunk boundaries
 // leave head/tail partials that k_seg_fixup combines in chunk order.
 #include "kern_coo_decl.cuh"
+#include "kern_sliced_decl.cuh"
 
 namespace spmv {
 namespace {
@@ -192,7 +193,7 @@ void run_hyb(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const sp
   // ELL part writes every row (alpha·s_ell + beta·y); the COO tail then adds
   // alpha·s_tail to the rows that have one (mode 2, or 3 with device alpha).
   spmv_launch_t le = L;
-  le.knob = h->dtype == SPMV_R64F ? 64 : 128;
+  le.knob = (h->dtype == SPMV_R64F ? 64 : 128) | kern::kSlicedCarry;
   run_ell_arrays(h, h->hyb_ecol, h->hyb_eval, h->hyb_K, h->hyb_npad, e, x, y, le);
   Epilogue et = e;
   et.mode = (e.mode == 1) ? 3 : 2;

@@ -9,13 +9,20 @@ void launch_sliced(spmv_matrix* h, kern::SlicedParams& p, int C, const spmv_laun
   const int bi = block_index(L.block), ri = reg_index(L.maxreg);
   const void* fn;
   const bool d16 = p.col16 != nullptr;
+  const bool carry = (L.knob & kern::kSlicedCarry) != 0;
+#define SL_PICK(CC)                                                                                         \
+  fn = d16 ? (carry ? (const void*)kern::sliced_fn<T, CC, true, true>(bi, ri)                               \
+                    : (const void*)kern::sliced_fn<T, CC, true, false>(bi, ri))                             \
+           : (carry ? (const void*)kern::sliced_fn<T, CC, false, true>(bi, ri)                              \
+                    : (const void*)kern::sliced_fn<T, CC, false, false>(bi, ri))
   switch (C) {
-    case 32: fn = d16 ? (const void*)kern::sliced_fn<T, 32, true>(bi, ri) : (const void*)kern::sliced_fn<T, 32, false>(bi, ri); break;
-    case 64: fn = d16 ? (const void*)kern::sliced_fn<T, 64, true>(bi, ri) : (const void*)kern::sliced_fn<T, 64, false>(bi, ri); break;
-    case 128: fn = d16 ? (const void*)kern::sliced_fn<T, 128, true>(bi, ri) : (const void*)kern::sliced_fn<T, 128, false>(bi, ri); break;
-    case 256: fn = d16 ? (const void*)kern::sliced_fn<T, 256, true>(bi, ri) : (const void*)kern::sliced_fn<T, 256, false>(bi, ri); break;
+    case 32: SL_PICK(32); break;
+    case 64: SL_PICK(64); break;
+    case 128: SL_PICK(128); break;
+    case 256: SL_PICK(256); break;
     default: fail(SPMV_ERR_UNSUPPORTED, "slice height C must be 32, 64, 128 or 256");
   }
+#undef SL_PICK
   set_carveout(fn, L.carveout_pct);
   const int64_t warps_per_block = L.block / 32;
   const int64_t grid = persistent_grid(fn, L.block, (p.nslices + warps_per_block - 1) / warps_per_block);
@@ -52,8 +59,8 @@ void launch_sliced(spmv_matrix* h, kern::SlicedParams& p, int C, const spmv_laun
 void run_ell_arrays(spmv_matrix* h, const int32_t* col, const void* val, int64_t K, int64_t n_pad,
                     const Epilogue& e, const void* x, void* y, const spmv_launch_t& L, const int16_t* col16) {
   kern::SlicedParams p{};
-  const int C = L.knob;
-  if (n_pad % C != 0) fail(SPMV_ERR_UNSUPPORTED, "ELL rows-per-warp must divide n_pad (a multiple of 128)");
+  const int C = L.knob & 0xffff;
+  if (C == 0 || n_pad % C != 0) fail(SPMV_ERR_UNSUPPORTED, "ELL rows-per-warp must divide n_pad (a multiple of 128)");
   p.col = col;
   p.col16 = col16;
   p.col_origin = h->col_origin;

@@ -112,7 +112,7 @@ def test_index16_spmv_parity(name, dtype, fmt, params):
             assert P.spmv_format_info(h, fmt)["index_bytes"] == 2
         for alpha, beta in [(1.0, 0.0), (2.5, -0.5)]:
             check_y(h, coo, dtype, fmt, alpha, beta)
-        for knob in ([32, 64, 128] if fmt == P.FMT_ELL else [0]):
+        for knob in ([32, 64, 128, 128 | (1 << 16)] if fmt == P.FMT_ELL else [0, 64]):
             P.spmv_set_launch(h, fmt, 256, 64, -1, knob)
             check_y(h, coo, dtype, fmt, 1.0, 0.0)
     finally:

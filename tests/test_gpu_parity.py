@@ -248,8 +248,8 @@ def test_spmv_parity(name, dtype, fname, fmt, params):
     ("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR), [1, 2, 4, 8, 16, 32]),
     ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), [4, 8, 16]),
     ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM), [16, 32, 64]),
-    ("ELL", P.FMT_ELL, {}, [32, 64, 128]),
-    ("SELL", P.FMT_SELL, {}, [0]),
+    ("ELL", P.FMT_ELL, {}, [32, 64, 128, 64 | (1 << 16), 256 | (1 << 16)]),
+    ("SELL", P.FMT_SELL, {}, [0, 64, 64 | (1 << 16)]),
     ("COO", P.FMT_COO, {}, [2, 4, 8]),
     ("HYB", P.FMT_HYB, {}, [2, 4, 8]),
     ("BELL", P.FMT_BELL, {"bell_b": 3}, [0])])
