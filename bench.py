@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--iters", type=int, default=100, help="power-iteration steps per step (E)")
-    ap.add_argument("--format", default="auto", help="auto (spmv_tune) or COO/CSR/ELL/HYB/SELL")
+    ap.add_argument("--format", default="auto", help="auto (spmv_tune) or COO/CSR/CSR-vector/CSR-merge/CSR-stream/ELL/HYB/SELL/BELL")
     ap.add_argument("--no-tune-launch", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--launch", default="", help="block,maxreg,carveout,knob (skips the launch sweep)")
@@ -331,8 +331,11 @@ def run_ours(args):
         launch = P.spmv_get_launch(h, fmt)
         decision = P.spmv_decision_log(h)
     else:
-        fmt = P.FORMATS[args.format]
+        csr_algs = {"CSR-vector": P.CSR_VECTOR, "CSR-merge": P.CSR_MERGE, "CSR-stream": P.CSR_STREAM}
+        fmt = P.FMT_CSR if args.format in csr_algs else P.FORMATS[args.format]
         params = {"index16": args.index16} if fmt in (P.FMT_ELL, P.FMT_SELL) else {}
+        if args.format in csr_algs:
+            params = {"csr_alg": csr_algs[args.format]}
         P.spmv_convert(h, fmt, **params)
         if args.launch:
             P.spmv_set_launch(h, fmt, *[int(v) for v in args.launch.split(",")])
@@ -356,6 +359,8 @@ def run_ours(args):
         params = dict(csr_alg=params.get("csr_alg", 0), csr_T=params.get("csr_T", 0))
     else:
         params = {}
+    fmt_label = P.FORMAT_NAMES[fmt] + ({P.CSR_MERGE: "-merge", P.CSR_STREAM: "-stream", P.CSR_VECTOR: "-vector"}
+                                       .get(params.get("csr_alg", 0), "") if fmt == P.FMT_CSR else "")
 
     stream = torch.cuda.current_stream()
     state = {"kms": []}
@@ -521,7 +526,7 @@ def run_ours(args):
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            if pj.get("format") == P.FORMAT_NAMES[fmt]:
+            if pj.get("format") == (fmt_label if fmt == P.FMT_CSR else P.FORMAT_NAMES[fmt]):
                 traffic = pj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -590,7 +595,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype,
             "data": "synthetic",
             "config": {"workload": args.config, "desc": cfgd["desc"], "n": n_global, "nnz": int(nnz_total),
-                       "power_iterations_per_step": E, "format": P.FORMAT_NAMES[fmt], "format_params": params,
+                       "power_iterations_per_step": E, "format": fmt_label, "format_params": params,
                        "launch": {"block": launch[0], "maxreg": launch[1], "carveout_pct": launch[2],
                                   "knob": launch[3]},
                        "partition": "row, nnz-balanced" if world > 1 else "none",
@@ -600,7 +605,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (matrix arrays > 126 MB; x stays L2-resident by design)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": f"{P.FORMAT_NAMES[fmt]} SpMV (power-step epilogue)" + (
+                         "kernel": f"{fmt_label} SpMV (power-step epilogue)" + (
                              "" if world == 1 else ", interior rows"),
                          "kernel_timing": ("CUDA events around the E back-to-back SpMV launches of each step / E "
                                            "(includes launch gaps)") if world == 1 else

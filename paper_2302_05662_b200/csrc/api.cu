@@ -453,7 +453,13 @@ static double sell_padding(spmv_matrix* h) {
 }
 
 // Run-time mode analog: features -> candidates -> measure -> gate.
-static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tune_report_t* rep, int obj) {
+// With tune_each (spmv_tune LAUNCH|FORMAT) every candidate is launch-tuned
+// before the comparison, so the gate compares the end states it would
+// produce (the compile-time mode inside the run-time mode); conversion
+// latencies are measured on a warm rebuild (the first build of a process
+// also pays lazy module loading, which a later conversion does not).
+static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tune_report_t* rep, int obj,
+                        bool tune_each) {
   if (!h->have_features) compute_features(h);
   const spmv_features_t& f = h->feat;
   const int orig_alg = h->csr_alg;
@@ -462,39 +468,67 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
   os << "{\"kind\":\"format_select\",\"features\":{\"n\":" << f.n_rows << ",\"nnz\":" << f.nnz
      << ",\"mean\":" << f.mean << ",\"var\":" << f.var << ",\"std\":" << f.std << ",\"max\":" << f.max_len
      << ",\"ell_ratio\":" << f.ell_ratio << ",\"median\":" << f.median << ",\"mode\":" << f.mode
-     << ",\"bandwidth\":" << f.bandwidth << "},\"candidates\":[";
+     << ",\"bandwidth\":" << f.bandwidth << "},\"tuned_candidates\":" << (tune_each ? "true" : "false")
+     << ",\"candidates\":[";
   struct Cand {
     int fmt;
     int alg;
     double t, c;
     std::string why;
     Measured m;
+    spmv_launch_t L;
   };
   std::vector<Cand> cands;
+  // time one candidate (format fmt, the active CSR algorithm for CSR) from launch L
+  auto measure = [&](int fmt, spmv_launch_t L) -> std::pair<double, spmv_launch_t> {
+    L = resolve_launch(h, fmt, L);
+    if (tune_each) {
+      h->launch[fmt] = L;
+      tune_launch(h, fmt, ts, rep, obj);
+      L = resolve_launch(h, fmt, h->launch[fmt]);
+    }
+    return {time_variant(h, fmt, L, ts.x, ts.y), L};
+  };
+  const spmv_launch_t csr_launch0 = h->launch[SPMV_FMT_CSR];
+  const spmv_launch_t dflt{0, 0, -1, 0};
   // CSR (paper default): CSR-vector with T from the mean.
   h->csr_alg = SPMV_CSR_VECTOR;
-  double t_csr = time_variant(h, SPMV_FMT_CSR, resolve_launch(h, SPMV_FMT_CSR, spmv_launch_t{0, 0, -1, 0}), ts.x, ts.y);
-  cands.push_back({SPMV_FMT_CSR, SPMV_CSR_VECTOR, t_csr, 0.0, "default"});
+  auto mc = measure(SPMV_FMT_CSR, dflt);
+  double t_csr = mc.first;
+  cands.push_back({SPMV_FMT_CSR, SPMV_CSR_VECTOR, t_csr, 0.0, "default", Measured{}, mc.second});
   const bool skewed = (f.mean > 0 && f.std / f.mean > 1.0) || (double)f.max_len > 32.0 * f.mean;
   if (skewed) {
     h->csr_alg = SPMV_CSR_MERGE;
-    double t = time_variant(h, SPMV_FMT_CSR, resolve_launch(h, SPMV_FMT_CSR, spmv_launch_t{0, 0, -1, 0}), ts.x, ts.y);
-    cands.push_back({SPMV_FMT_CSR, SPMV_CSR_MERGE, t, 0.0, "std/mean>1 or max>32*mean"});
+    auto m = measure(SPMV_FMT_CSR, dflt);
+    cands.push_back({SPMV_FMT_CSR, SPMV_CSR_MERGE, m.first, 0.0, "std/mean>1 or max>32*mean", Measured{}, m.second});
+  } else {
+    // CSR-stream (TMA-staged tiles, thread per row): no conversion at all
+    h->csr_alg = SPMV_CSR_STREAM;
+    try {
+      auto m = measure(SPMV_FMT_CSR, dflt);
+      cands.push_back({SPMV_FMT_CSR, SPMV_CSR_STREAM, m.first, 0.0, "regular rows (no conversion)", Measured{},
+                       m.second});
+    } catch (const SpmvError& e) {
+      cudaGetLastError();
+      os << "{\"format\":\"CSR\",\"alg\":\"stream\",\"rejected\":\"" << e.msg << "\"},";
+    }
   }
   h->csr_alg = orig_alg;
+  h->launch[SPMV_FMT_CSR] = csr_launch0;
   int64_t bell_b_try = 2;
+  auto do_build = [&](int fmt) {
+    switch (fmt) {
+      case SPMV_FMT_BELL: build_bell(h, bell_b_try); break;
+      case SPMV_FMT_ELL: build_ell(h, -1); break;
+      case SPMV_FMT_SELL: build_sell(h, h->dtype == SPMV_R64F ? 64 : 128, 1, -1); break;
+      case SPMV_FMT_HYB: build_hyb(h, -1); break;
+      case SPMV_FMT_COO: build_coo(h); break;
+    }
+  };
   auto try_build = [&](int fmt, const char* why) {
     bool was = built(h, fmt);
     try {
-      if (!was) {
-        switch (fmt) {
-          case SPMV_FMT_BELL: build_bell(h, bell_b_try); break;
-          case SPMV_FMT_ELL: build_ell(h, -1); break;
-          case SPMV_FMT_SELL: build_sell(h, h->dtype == SPMV_R64F ? 64 : 128, 1, -1); break;
-          case SPMV_FMT_HYB: build_hyb(h, -1); break;
-          case SPMV_FMT_COO: build_coo(h); break;
-        }
-      }
+      if (!was) do_build(fmt);
     } catch (const SpmvError& e) {
       cudaGetLastError();
       os << "{\"format\":\"" << fmt_name(fmt) << "\",\"rejected\":\"" << e.msg << "\"},";
@@ -515,10 +549,15 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
         return;
       }
     }
-    double t = time_variant(h, fmt, resolve_launch(h, fmt, h->launch[fmt]), ts.x, ts.y);
-    cands.push_back({fmt, 0, t, format_latency(h, fmt), why});
+    if (!was) {  // warm conversion latency: rebuild once the kernels are loaded
+      free_format(h, fmt);
+      do_build(fmt);
+    }
+    auto m = measure(fmt, h->launch[fmt]);
+    cands.push_back({fmt, 0, m.first, format_latency(h, fmt), why, Measured{}, m.second});
   };
   if (f.ell_ratio >= 0.9) try_build(SPMV_FMT_ELL, "ell_ratio>=0.9");
+  if (!skewed) try_build(SPMV_FMT_SELL, "SELL padding<=10%");
   // BELL: only block-structured matrices keep block padding <= 10%
   if (!skewed && f.mean >= 4.0) {
     if (built(h, SPMV_FMT_BELL)) {
@@ -540,39 +579,40 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
     c.m.t = c.t;
     if (obj != 0) {  // energy / power / efficiency: NVML window per candidate
       if (c.fmt == SPMV_FMT_CSR) h->csr_alg = c.alg;
-      measure_objective(h, c.fmt, resolve_launch(h, c.fmt, c.fmt == SPMV_FMT_CSR ? spmv_launch_t{0, 0, -1, 0}
-                                                                              : h->launch[c.fmt]),
-                        ts.x, ts.y, c.m);
+      measure_objective(h, c.fmt, c.L, ts.x, ts.y, c.m);
       h->csr_alg = orig_alg;
     }
   }
   size_t bi = 0;
   for (size_t i = 0; i < cands.size(); ++i) {
     const Cand& c = cands[i];
-    os << "{\"format\":\"" << fmt_name(c.fmt) << "\"" << (c.alg == SPMV_CSR_MERGE ? ",\"alg\":\"merge\"" : "")
+    os << "{\"format\":\"" << fmt_name(c.fmt) << "\""
+       << (c.alg == SPMV_CSR_MERGE ? ",\"alg\":\"merge\"" : (c.alg == SPMV_CSR_STREAM ? ",\"alg\":\"stream\"" : ""))
        << ",\"t_s\":" << c.t << ",\"c_latency_s\":" << c.c << ",\"why\":\"" << c.why << "\"";
     if (obj != 0)
       os << ",\"j_per_spmv\":" << c.m.ej << ",\"w\":" << c.m.w << ",\"mflops_per_w\":" << c.m.eff;
     os << "}" << (i + 1 < cands.size() ? "," : "");
-    if (objective_value(obj, c.m) < objective_value(obj, cands[bi].m)) bi = i;
   }
-  const Cand& best = cands[bi];
   const Cand& csr = cands[0];
-  double gain, overhead;
-  bool convert;
-  if (obj == 0) {  // time (strict >)
-    gain = (double)iters * (t_csr - best.t);
-    overhead = h->f_latency + best.c;
-    convert = gain > overhead;
-  } else if (obj == 2) {  // average power: no amortisation, the lower draw wins
-    gain = csr.m.w - best.m.w;
-    overhead = 0.0;
-    convert = gain > overhead;
-  } else {  // energy / efficiency: joules, conversion energy at CSR's average power
-    gain = (double)iters * (csr.m.ej - best.m.ej);
-    overhead = csr.m.w * (h->f_latency + best.c);
-    convert = gain > overhead;
-  }
+  // Gate (strict >): a candidate's gain over the default
+  // CSR minus its overhead. Among several candidates the one with the largest
+  // net benefit wins (reading R19): with a short run a conversion-free
+  // candidate can beat a slightly faster one that needs a conversion.
+  auto gain_of = [&](const Cand& c) {
+    if (obj == 0) return (double)iters * (t_csr - c.t);
+    if (obj == 2) return csr.m.w - c.m.w;  // average power: no amortisation, the lower draw wins
+    return (double)iters * (csr.m.ej - c.m.ej);  // energy / efficiency: joules
+  };
+  auto overhead_of = [&](const Cand& c) {
+    if (obj == 0) return h->f_latency + c.c;
+    if (obj == 2) return 0.0;
+    return csr.m.w * (h->f_latency + c.c);  // conversion energy at CSR's average power
+  };
+  for (size_t i = 1; i < cands.size(); ++i)
+    if (bi == 0 || gain_of(cands[i]) - overhead_of(cands[i]) > gain_of(cands[bi]) - overhead_of(cands[bi])) bi = i;
+  const Cand& best = cands[bi];
+  const double gain = bi ? gain_of(best) : 0.0, overhead = bi ? overhead_of(best) : 0.0;
+  const bool convert = bi != 0 && gain > overhead;
   const int chosen = convert ? best.fmt : SPMV_FMT_CSR;
   const int chosen_alg = convert ? best.alg : SPMV_CSR_VECTOR;
   os << "],\"objective\":\"" << Objective::name(obj) << "\",\"gate\":{\"expected_iterations\":" << iters
@@ -580,13 +620,20 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
      << ",\"gain\":" << gain << ",\"overhead\":" << overhead
      << ",\"f_latency_s\":" << h->f_latency << ",\"c_latency_s\":" << best.c
      << ",\"convert\":" << (convert ? "true" : "false") << "},\"chosen\":\"" << fmt_name(chosen)
-     << (chosen == SPMV_FMT_CSR && chosen_alg == SPMV_CSR_MERGE ? "-merge" : "") << "\"}";
+     << (chosen == SPMV_FMT_CSR && chosen_alg == SPMV_CSR_MERGE ? "-merge" : "")
+     << (chosen == SPMV_FMT_CSR && chosen_alg == SPMV_CSR_STREAM ? "-stream" : "") << "\"}";
   log_append(h, os.str());
   // release candidates that were built here and not chosen
   for (const Cand& c : cands)
     if (c.fmt != chosen && c.fmt != SPMV_FMT_CSR) free_format(h, c.fmt);
   h->active = chosen;
   if (chosen == SPMV_FMT_CSR) h->csr_alg = chosen_alg;
+  if (tune_each) {  // the chosen end state keeps its tuned launch
+    const Cand& kept = convert ? best : csr;
+    h->launch[kept.fmt] = kept.L;
+  } else if (chosen == SPMV_FMT_CSR && chosen_alg != orig_alg) {
+    h->launch[SPMV_FMT_CSR] = spmv_launch_t{0, 0, -1, 0};  // another kernel: defaults
+  }
   if (rep) {
     rep->format = chosen;
     rep->t_csr_s = t_csr;
@@ -933,9 +980,10 @@ spmv_status_t spmv_tune(spmv_handle_t h, uint32_t flags, int64_t expected_iterat
   TuneScratch ts(h);
   if (what & SPMV_TUNE_FORMAT) {
     if (predict) tune_predict(h, expected_iterations, ts, &rep);
-    else tune_format(h, expected_iterations, ts, &rep, obj);
+    else tune_format(h, expected_iterations, ts, &rep, obj, (what & SPMV_TUNE_LAUNCH) != 0);
   }
-  if (what & SPMV_TUNE_LAUNCH) tune_launch(h, h->active, ts, &rep, obj);
+  // after a measured format selection with LAUNCH the chosen launch is already tuned
+  if ((what & SPMV_TUNE_LAUNCH) && (predict || !(what & SPMV_TUNE_FORMAT))) tune_launch(h, h->active, ts, &rep, obj);
   rep.format = h->active;
   rep.launch = resolve_launch(h, h->active, h->launch[h->active]);
   CK(cudaStreamSynchronize(h->stream));

@@ -13,6 +13,7 @@
 
 #pragma once
 #include "kern_csr_decl.cuh"
+#include "tma.cuh"
 
 namespace spmv {
 namespace kern {
@@ -92,71 +93,151 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_vector(cons
 }
 
 // ------------------------------------------------------------------ CSR-stream
-// A block owns B consecutive rows per step (persistent grid-stride). If their
-// nnz fits the block's shared-memory segment (B·EPT entries), the block copies
-// the contiguous CSR segment into shared memory with coalesced 128-bit loads
-// and then thread t accumulates row r0+t from shared memory: at every step k
-// the 32 lanes of a warp gather the k-th entry of 32 consecutive rows, which
-// for banded/stencil matrices are adjacent x values (4 lines per instruction,
-// like ELL) instead of one row's scattered neighbours. Blocks with longer
-// rows fall back to warp-per-row accumulation over global memory.
+// Thread per row over a shared-memory copy of the tile's CSR segment, fed by a
+// TMA pipeline. A tile is B consecutive rows; its entries [rp[r0], rp[r0+B])
+// are contiguous in col/val, so one producer warp moves them into a ring of
+// two shared-memory stages with cp.async.bulk (mbarrier transaction counts,
+// L2 evict-first) while the B consumer threads work on the other stage. The
+// consumers then read row r0+t from shared memory: at step k the 32 lanes of
+// a warp gather the k-th entry of 32 consecutive rows, which for banded /
+// stencil matrices are adjacent x values (a few lines per instruction, like
+// ELL) instead of one row's scattered neighbours (CSR-vector), and the matrix
+// stream never occupies L1TEX. Tiles whose segment exceeds the stage (long
+// rows) are handled warp-per-row straight from global memory.
 template <int B, int R, class T, int EPT, class RP>
-__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_stream(const CsrParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* s_val = reinterpret_cast<T*>(smem_raw);
-  int32_t* s_col = reinterpret_cast<int32_t*>(smem_raw + (size_t)B * EPT * sizeof(T));
+__global__ void __launch_bounds__(B + 32) __maxnreg__(regcap(B + 32, R)) k_csr_stream(const CsrParams p) {
   constexpr int CAP = B * EPT;
+  constexpr int NS = kStreamStages;
+  constexpr int VP = StreamStage<T>::kValPad;
+  constexpr int U = sizeof(T) == 8 ? 16 : 16;  // entries per gather batch (independent loads in flight)
+  constexpr size_t STAGE = StreamStage<T>::bytes(CAP);
+  constexpr size_t COLB = StreamStage<T>::col_bytes(CAP);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS];
+  __shared__ int64_t meta_s0[NS];
+  __shared__ int meta_staged[NS];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) {
+    for (int s = 0; s < NS; ++s) {
+      tma::mbar_init(&full_bar[s], 32);          // the 32 producer lanes arrive (lane 0 also adds the tx)
+      tma::mbar_init(&empty_bar[s], B / 32);     // one arrival per consumer warp
+    }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const RP* __restrict__ rp = static_cast<const RP*>(p.rp);
   const T* __restrict__ val = static_cast<const T*>(p.val);
   const T* __restrict__ x = static_cast<const T*>(p.x);
   T* __restrict__ y = static_cast<T*>(p.y);
-  const double alpha = epi_alpha(p.e);
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t ntiles = (p.rows + B - 1) / B;
   double yy = 0.0, xy = 0.0;
-  for (int64_t r0 = (int64_t)blockIdx.x * B; r0 < p.rows; r0 += (int64_t)gridDim.x * B) {
-    const int64_t r1 = r0 + B < p.rows ? r0 + B : p.rows;
-    const int64_t s0 = rp[r0], s1 = rp[r1];
-    const int64_t seg = s1 - s0;
-    if (seg <= CAP) {
-      // coalesced staging: align the copy to 16 B so the bulk uses vector loads
-      for (int64_t j = t; j < seg; j += B) {
-        s_col[j] = ld_stream(p.col + s0 + j);
-        s_val[j] = ld_stream(val + s0 + j);
+  if (warp == B / 32) {
+    // ------------------------------------------------------------ producer
+    const uint64_t pol = tma::policy_evict_first();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t r0 = tile * B, r1 = r0 + B < p.rows ? r0 + B : p.rows;
+      const int64_t s0 = (int64_t)rp[r0], s1 = (int64_t)rp[r1];
+      const bool staged = s1 - s0 <= CAP;
+      tma::mbar_wait(&empty_bar[stage], phase ^ 1);
+      unsigned char* st = smem_raw + (size_t)stage * STAGE;
+      int32_t* s_col = reinterpret_cast<int32_t*>(st);
+      T* s_val = reinterpret_cast<T*>(st + COLB);
+      if (lane == 0) {
+        meta_s0[stage] = s0;
+        meta_staged[stage] = staged;
       }
-      __syncthreads();
-      const int64_t row = r0 + t;
-      if (row < r1) {
-        const int a = (int)(rp[row] - s0), b = (int)(rp[row + 1] - s0);
-        double acc = 0.0;
-        int k = a;
-        for (; k + 3 < b; k += 4) {
-          const int c0 = s_col[k], c1 = s_col[k + 1], c2 = s_col[k + 2], c3 = s_col[k + 3];
-          const T x0 = ld_x(x + c0), x1 = ld_x(x + c1), x2 = ld_x(x + c2), x3 = ld_x(x + c3);
-          acc = fma((double)s_val[k], (double)x0, acc);
-          acc = fma((double)s_val[k + 1], (double)x1, acc);
-          acc = fma((double)s_val[k + 2], (double)x2, acc);
-          acc = fma((double)s_val[k + 3], (double)x3, acc);
-        }
-        for (; k < b; ++k) acc = fma((double)s_val[k], (double)ld_x(x + s_col[k]), acc);
-        const T out = epi_value<T>(p.e, alpha, acc, y, row);
-        y[row] = out;
-        if (p.e.mode == 1) {
-          yy += (double)out * (double)out;
-          xy += (double)x[p.e.row_offset + row] * (double)out;
-        }
-      }
-      __syncthreads();
-    } else {
-      // long rows: warp per row over global memory, shuffle reduction
-      for (int64_t row = r0 + warp; row < r1; row += B / 32) {
-        const int64_t a = rp[row], b = rp[row + 1];
-        double acc = 0.0;
-        for (int64_t k = a + lane; k < b; k += 32)
-          acc = fma((double)ld_stream(val + k), (double)ld_x(x + ld_stream(p.col + k)), acc);
-        acc = warp_sum(acc);
+      if (staged && s1 > s0) {
+        // 16-byte aligned inner ranges go by bulk copy; the (< 16 B) head and
+        // tail of each array are copied by the lanes.
+        const int64_t cb = s0 & ~3LL;
+        int64_t ci0 = (s0 + 3) & ~3LL, ci1 = s1 & ~3LL;
+        if (ci1 <= ci0) ci0 = ci1 = s1;
+        const int64_t vb = s0 & ~(int64_t)(VP - 1);
+        int64_t vi0 = (s0 + VP - 1) & ~(int64_t)(VP - 1), vi1 = s1 & ~(int64_t)(VP - 1);
+        if (vi1 <= vi0) vi0 = vi1 = s1;
         if (lane == 0) {
+          const uint32_t tx = (uint32_t)((ci1 - ci0) * 4 + (vi1 - vi0) * (int64_t)sizeof(T));
+          if (tx) tma::mbar_expect_tx(&full_bar[stage], tx);
+          if (ci1 > ci0)
+            tma::bulk_g2s(s_col + (ci0 - cb), p.col + ci0, (uint32_t)((ci1 - ci0) * 4), &full_bar[stage], pol);
+          if (vi1 > vi0)
+            tma::bulk_g2s(s_val + (vi0 - vb), val + vi0, (uint32_t)((vi1 - vi0) * sizeof(T)), &full_bar[stage], pol);
+        }
+        const int ch = (int)(ci0 - s0), ct = (int)(s1 - ci1);
+        if (lane < ch) s_col[s0 + lane - cb] = ld_stream(p.col + s0 + lane);
+        else if (lane >= 16 && lane - 16 < ct) s_col[ci1 + lane - 16 - cb] = ld_stream(p.col + ci1 + lane - 16);
+        const int vh = (int)(vi0 - s0), vt = (int)(s1 - vi1);
+        if (lane < vh) s_val[s0 + lane - vb] = ld_stream(val + s0 + lane);
+        else if (lane >= 16 && lane - 16 < vt) s_val[vi1 + lane - 16 - vb] = ld_stream(val + vi1 + lane - 16);
+      }
+      tma::mbar_arrive(&full_bar[stage]);  // releases this lane's plain stores
+      if (++stage == NS) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    const double alpha = epi_alpha(p.e);
+    int stage = 0;
+    uint32_t phase = 0;
+    int64_t tile = blockIdx.x;
+    int64_t a_nx = 0, b_nx = 0;
+    if (tile < ntiles) {
+      const int64_t row = tile * B + t;
+      if (row < p.rows) {
+        a_nx = (int64_t)rp[row];
+        b_nx = (int64_t)rp[row + 1];
+      }
+    }
+    for (; tile < ntiles; tile += gridDim.x) {
+      const int64_t r0 = tile * B, r1 = r0 + B < p.rows ? r0 + B : p.rows;
+      const int64_t row = r0 + t;
+      const int64_t a_g = a_nx, b_g = b_nx;
+      {  // prefetch the next tile's row bounds
+        const int64_t nrow = row + (int64_t)gridDim.x * B;
+        if (nrow < p.rows) {
+          a_nx = (int64_t)rp[nrow];
+          b_nx = (int64_t)rp[nrow + 1];
+        }
+      }
+      tma::mbar_wait(&full_bar[stage], phase);
+      const unsigned char* st = smem_raw + (size_t)stage * STAGE;
+      if (meta_staged[stage]) {
+        // local entry j of the tile sits at s_col[j + oc], s_val[j + ov]
+        const int64_t s0 = meta_s0[stage];
+        const int32_t* s_col = reinterpret_cast<const int32_t*>(st) + (int)(s0 & 3);
+        const T* s_val = reinterpret_cast<const T*>(st + COLB) + (int)(s0 & (VP - 1));
+        if (row < r1) {
+          double acc = 0.0;
+          const int ka = (int)(a_g - s0), kb = (int)(b_g - s0), len = kb - ka;
+          // Rows whose length is a multiple of 8 would put the lanes of a warp
+          // on the same banks (stride len words): such a row is walked from a
+          // lane-dependent rotation. Other lengths (the stencil's 27) keep
+          // k-aligned lanes, so the gathers of a step stay on adjacent x.
+          int rot = (len & 7) == 0 && len > 0 ? lane : 0;
+          if (rot >= len) rot %= len;
+          for (int k = 0; k < len; k += U) {
+            int c[U];
+            T v[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+              const bool ok = k + j < len;
+              int q = k + j + rot;
+              q = q >= len ? q - len : q;
+              c[j] = ok ? s_col[ka + q] : 0;
+              v[j] = ok ? s_val[ka + q] : T(0);
+            }
+            T xv[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) xv[j] = k + j < len ? ld_x(x + c[j]) : T(0);
+#pragma unroll
+            for (int j = 0; j < U; ++j) acc = fma((double)v[j], (double)xv[j], acc);
+          }
           const T out = epi_value<T>(p.e, alpha, acc, y, row);
           y[row] = out;
           if (p.e.mode == 1) {
@@ -164,6 +245,29 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_stream(cons
             xy += (double)x[p.e.row_offset + row] * (double)out;
           }
         }
+      } else {
+        // long rows: warp per row over global memory, shuffle reduction
+        for (int64_t rr = r0 + warp; rr < r1; rr += B / 32) {
+          const int64_t a = rp[rr], b = rp[rr + 1];
+          double acc = 0.0;
+          for (int64_t k = a + lane; k < b; k += 32)
+            acc = fma((double)ld_stream(val + k), (double)ld_x(x + ld_stream(p.col + k)), acc);
+          acc = warp_sum(acc);
+          if (lane == 0) {
+            const T out = epi_value<T>(p.e, alpha, acc, y, rr);
+            y[rr] = out;
+            if (p.e.mode == 1) {
+              yy += (double)out * (double)out;
+              xy += (double)x[p.e.row_offset + rr] * (double)out;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&empty_bar[stage]);
+      if (++stage == NS) {
+        stage = 0;
+        phase ^= 1;
       }
     }
   }
@@ -336,8 +440,14 @@ CsrFn csr_vector_fn(int bi, int ri) {
 #undef CSRV_TAB
 #undef CSRV_ROW
 
-#define CSRS_ROW(B, E) {&k_csr_stream<B, 32, T, E, RP>, &k_csr_stream<B, 64, T, E, RP>, \
-                        &k_csr_stream<B, 128, T, E, RP>, &k_csr_stream<B, 255, T, E, RP>}
+// B + 32 threads per block (one producer warp): B = 1024 has no variant.
+template <int B, int R, class T, int E, class RP>
+constexpr CsrFn stream_ptr() {
+  if constexpr (B + 32 > 1024) return nullptr;
+  else return &k_csr_stream<B, R, T, E, RP>;
+}
+#define CSRS_ROW(B, E) {stream_ptr<B, 32, T, E, RP>(), stream_ptr<B, 64, T, E, RP>(), \
+                        stream_ptr<B, 128, T, E, RP>(), stream_ptr<B, 255, T, E, RP>()}
 #define CSRS_TAB(E) {CSRS_ROW(64, E), CSRS_ROW(128, E), CSRS_ROW(256, E), CSRS_ROW(512, E), CSRS_ROW(1024, E)}
 template <class T, class RP, int E>
 CsrFn csr_stream_fn(int bi, int ri) {

@@ -27,10 +27,24 @@ template <class T, class RP, int IPT>
 CsrFn csr_merge_fn(int bi, int ri);
 template <class T, class RP, int EPT>
 CsrFn csr_stream_fn(int bi, int ri);
-// Dynamic shared memory of a CSR-stream block: B rows × EPT entries of (col, value).
+// Shared-memory stage of the CSR-stream pipeline holding `cap` entries: the
+// column region (cap + 4 ints) then the value region (cap + 16/sizeof(T)
+// values), both 16-byte aligned (the slack absorbs the alignment of the
+// tile's first entry).
+template <class T>
+struct StreamStage {
+  static constexpr int kValPad = 16 / (int)sizeof(T);
+  __host__ __device__ static constexpr size_t col_bytes(int cap) { return ((size_t)(cap + 4) * 4 + 15) / 16 * 16; }
+  __host__ __device__ static constexpr size_t bytes(int cap) {
+    return col_bytes(cap) + ((size_t)(cap + kValPad) * sizeof(T) + 15) / 16 * 16;
+  }
+};
+constexpr int kStreamStages = 2;
+// Dynamic shared memory of a CSR-stream block: kStreamStages stages of
+// B rows × EPT entries of (col, value).
 template <class T>
 constexpr size_t stream_smem_bytes(int block, int ept) {
-  return (size_t)block * (size_t)ept * (4 + sizeof(T));
+  return (size_t)kStreamStages * StreamStage<T>::bytes(block * ept);
 }
 // Dynamic shared memory of a merge-path block of `block` threads.
 // Per-warp slice: ITEMS fp64 products then ITEMS+1 int32 row ends, padded to 16 B.

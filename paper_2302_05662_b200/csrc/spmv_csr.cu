@@ -24,11 +24,15 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
       case 64: fn = (const void*)kern::csr_stream_fn<T, RP, 64>(bi, ri); break;
       default: fail(SPMV_ERR_INVALID_ARG, "CSR-stream entries per row slot must be 16, 32 or 64");
     }
+    if (!fn) fail(SPMV_ERR_UNSUPPORTED, "CSR-stream: block + producer warp exceeds 1024 threads");
     const size_t smem = kern::stream_smem_bytes<T>(L.block, ept);
-    if (smem > 227 * 1024) fail(SPMV_ERR_UNSUPPORTED, "CSR-stream block × entries exceeds shared memory");
+    if (smem > 227 * 1024 - 1024) fail(SPMV_ERR_UNSUPPORTED, "CSR-stream block × entries exceeds shared memory");
+    if (((uintptr_t)h->col | (uintptr_t)h->val) & 15)
+      fail(SPMV_ERR_UNSUPPORTED, "CSR-stream: col/val must be 16-byte aligned for the bulk copies");
     set_carveout(fn, L.carveout_pct);
     set_max_dynamic_smem(fn, smem);
-    const int64_t grid = persistent_grid(fn, L.block, (h->rows + L.block - 1) / L.block, smem);
+    const int threads = L.block + 32;  // B consumer threads + one TMA producer warp
+    const int64_t grid = persistent_grid(fn, threads, (h->rows + L.block - 1) / L.block, smem);
     if (grid <= 0) return;
     if (e.mode == 1) {
       ensure_pi_scratch(h, (size_t)grid);
@@ -36,7 +40,7 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
       p.e.counter = h->pi_counter;
     }
     void* args[] = {&p};
-    launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, smem, h->stream);
+    launch_checked(fn, dim3((unsigned)grid), dim3(threads), args, smem, h->stream);
     return;
   }
   if (!merge) {
