@@ -526,8 +526,11 @@ def run_ours(args):
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            if pj.get("format") == (fmt_label if fmt == P.FMT_CSR else P.FORMAT_NAMES[fmt]):
+            key = fmt_label if fmt == P.FMT_CSR else P.FORMAT_NAMES[fmt]
+            if pj.get("format") == key:  # legacy single-format layout
                 traffic = pj.get("dram_bytes_per_launch")
+            elif isinstance(pj.get(key), dict):
+                traffic = pj[key].get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     kernel_share = sum(kernel_ms) / ms if ms > 0 else None

@@ -33,6 +33,11 @@ def corpus():
     g.append(("rmat10", si.rmat(10, dtype=np.float64)))
     g.append(("lap2d_20", si.lap2d(20, random_values=True)))
     g.append(("stencil27_9", si.stencil27(9, random_values=True)))
+    # staged and overflowing tiles of the TMA kernels side by side (a 3000-entry
+    # row every 700 rows), segment starts at every 16-byte residue
+    Lm = _lengths(7, 3000, 20, 0.15)
+    Lm[::700] = 3000
+    g.append(("mixed_tiles", si.random_coo(3000, 5000, 0, 7, lengths=Lm)))
     g.append(("wide_3x70000", si.random_coo(3, 70000, 0, 6, lengths=np.array([66000, 0, 65536]))))
     return g
 

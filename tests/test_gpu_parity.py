@@ -273,6 +273,33 @@ def test_launch_variants_parity(fname, fmt, params, knobs, dtype):
         P.spmv_destroy(h)
 
 
+@pytest.mark.parametrize("case", ["mixed_tiles", "long_rows", "rmat10", "stencil27_9", "ragged_empty"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_csr_stream_tma_all_launches(case, dtype):
+    """The TMA-pipelined CSR-stream kernel over every block size, stage size
+    and register cap on matrices mixing staged and overflowing tiles, with
+    segment starts at every 16-byte residue (bulk-copied interior, lane-copied
+    head/tail): O9 parity; block 1024 (+ producer warp) must be refused."""
+    coo = CASES[case]
+    h = create(coo, dtype)
+    try:
+        ref = oracle_csr(coo)
+        P.spmv_convert(h, P.FMT_CSR, csr_alg=P.CSR_STREAM)
+        for block in (64, 128, 256, 512, 1024):
+            for maxreg in (32, 255):
+                for ept in (16, 32, 64):
+                    P.spmv_set_launch(h, P.FMT_CSR, block, maxreg, -1, ept)
+                    try:
+                        check_y(h, coo, dtype, P.FMT_CSR, 2.5, -0.5, ref)
+                        check_y(h, coo, dtype, P.FMT_CSR, 1.0, 0.0, ref, nan_y=True)
+                    except P.SpmvError as ex:   # block + producer warp > 1024 or stages > shared memory
+                        assert ex.status == P.ERR_UNSUPPORTED
+                        assert block == 1024 or block * ept * (12 if dtype == "f64" else 8) * 2 > 200 * 1024
+                        torch.cuda.synchronize()
+    finally:
+        P.spmv_destroy(h)
+
+
 def test_determinism_bitwise():
     coo = CASES["long_rows"]
     h = create(coo)

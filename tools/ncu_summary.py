@@ -77,8 +77,16 @@ def full(rep, config, fmt, alg_bytes, prefix):
                "dram_GBps_under_ncu": [t / (u * 1e-6) / 1e9 for t, u in zip(traffic, times)],
                "metrics": [{k: " ".join(v) for k, v in d.items()} for d in launches_]}
     json.dump(summary, open(f"{prefix}.json", "w"), indent=1)
-    json.dump({"format": fmt, "dram_bytes_per_launch": mean_t, "source": rep},
-              open(f"profiles/ncu_traffic_{config}.json", "w"), indent=1)
+    # per-config traffic file, one entry per format label (bench.py reads its own)
+    tpath = f"profiles/ncu_traffic_{config}.json"
+    try:
+        tj = json.load(open(tpath))
+    except (OSError, ValueError):
+        tj = {}
+    if "format" in tj:  # legacy single-format layout
+        tj = {tj["format"]: {"dram_bytes_per_launch": tj["dram_bytes_per_launch"], "source": tj.get("source")}}
+    tj[fmt] = {"dram_bytes_per_launch": mean_t, "source": rep}
+    json.dump(tj, open(tpath, "w"), indent=1)
     print(json.dumps({k: v for k, v in summary.items() if k != "metrics"}, indent=1))
 
 
