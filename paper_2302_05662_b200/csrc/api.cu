@@ -596,7 +596,7 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
   const Cand& csr = cands[0];
   // Gate (strict >): a candidate's gain over the default
   // CSR minus its overhead. Among several candidates the one with the largest
-  // net benefit wins (reading R19): with a short run a conversion-free
+  // net benefit wins (reading R31): with a short run a conversion-free
   // candidate can beat a slightly faster one that needs a conversion.
   auto gain_of = [&](const Cand& c) {
     if (obj == 0) return (double)iters * (t_csr - c.t);

@@ -389,8 +389,8 @@ def test_power_step_parity(fname, fmt, params):
 
 
 def gate_net_best(sel, objective="latency"):
-    """The candidate the gate must pick (reading R19): the largest net benefit
-    gain - overhead over the default CSR (first measured candidate)."""
+    """The candidate the gate must pick : the largest net benefit
+    gain - overhead over the default CSR (first measured candidate), reading R31."""
     cands = [c for c in sel["candidates"] if "t_s" in c]
     csr, g = cands[0], sel["gate"]
     it, f = g["expected_iterations"], g["f_latency_s"]
