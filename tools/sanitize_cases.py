@@ -25,7 +25,7 @@ FMTS = [(P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)), (P.FMT_CSR, dict(csr_alg=P.CSR_
 
 def main():
     names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["ragged_empty", "long_rows", "appendix_d", "empty_7x5",
-                                                              "rmat10"]
+                                                              "rmat10", "mixed_tiles"]
     cases = {n: c for n, c in corpus()}
     for name in names:
         coo = cases[name]
