@@ -94,3 +94,52 @@ def test_fullsize_selected_format(cfg):
                 zprev = zk
     finally:
         P.spmv_destroy(h)
+
+
+FULL_FORMATS = {
+    "c2": [("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)), ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM)),
+           ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE)), ("ELL", P.FMT_ELL, dict(index16=0)),
+           ("ELL-16", P.FMT_ELL, dict(index16=1)), ("SELL", P.FMT_SELL, dict(index16=0)),
+           ("SELL-16", P.FMT_SELL, dict(index16=1)), ("HYB", P.FMT_HYB, {}), ("COO", P.FMT_COO, {})],
+    "c3": [("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)), ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE)),
+           ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM)), ("HYB", P.FMT_HYB, {}), ("COO", P.FMT_COO, {})],
+    "c4": [("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)), ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM)),
+           ("ELL", P.FMT_ELL, {}), ("SELL", P.FMT_SELL, {}), ("COO", P.FMT_COO, {})],
+}
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_fullsize_every_format(cfg):
+    """Every format's kernel at the full BASELINE size (default launch, the
+    TMA-staged CSR-stream included): y on sampled rows against the oracle."""
+    coo = si.config_device(cfg)
+    dtype = si.CONFIGS[cfg]["dtype"]
+    dt = coo.val.dtype
+    R = coo.row.cpu().numpy()
+    Cc = coo.col.cpu().numpy()
+    V = coo.val.cpu().numpy().astype(np.float64)
+    n = coo.rows
+    h = P.spmv_create(coo.rows, coo.cols, coo.row, coo.col, coo.val)
+    del coo
+    try:
+        rp = oracle.csr(n, R)
+        rows_sel = sample_rows(rp, n, seed=9, k=2000)
+        srp, sc, sv = sub_csr(rp, Cc, V, rows_sel)
+        x = si.vector_device(P.spmv_features(h)["n_cols"], dtype=dt)
+        xh = x.cpu().numpy().astype(np.float64)
+        yin = si.vector_device(n, seed=si.Y_SEED, dtype=dt)
+        yinh = yin.cpu().numpy().astype(np.float64)[rows_sel]
+        y_ref, a_ref = oracle.spmv_csr(len(rows_sel), srp, sc, sv, xh, 2.5, -0.5, yinh)
+        for name, fmt, params in FULL_FORMATS[cfg]:
+            P.spmv_convert(h, fmt, **params)
+            y = yin.clone()
+            P.spmv_run(h, 2.5, x, -0.5, y)
+            torch.cuda.synchronize()
+            yg = y.cpu().numpy().astype(np.float64)[rows_sel]
+            ok, worst, bad = oracle.parity_check(yg, y_ref, a_ref, 2.5, -0.5, yinh, TAU[dtype])
+            assert ok, (cfg, name, worst, rows_sel[bad[:5]])
+            if fmt != P.FMT_CSR:
+                P.spmv_convert(h, P.FMT_CSR)
+    finally:
+        P.spmv_destroy(h)

@@ -19,6 +19,7 @@ ap.add_argument("format")
 ap.add_argument("launches", nargs="+")
 ap.add_argument("--csr-alg", type=int, default=0)
 ap.add_argument("--index16", type=int, default=0)
+ap.add_argument("--reps", type=int, default=20)
 a = ap.parse_args()
 coo = si.config_device(a.config)
 x = si.vector_device(coo.cols, dtype=coo.val.dtype)
@@ -39,11 +40,11 @@ for L in a.launches:
         ts = []
         for _ in range(5):
             e0.record(s)
-            for _ in range(20):
+            for _ in range(a.reps):
                 P.spmv_run(h, 1.0, x, 0.0, y)
             e1.record(s)
             torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1) / 20 * 1e3)
+            ts.append(e0.elapsed_time(e1) / a.reps * 1e3)
         print(f"{a.config} {a.format} alg={a.csr_alg} launch={L}: {statistics.median(ts):.2f} us", flush=True)
     except P.SpmvError as ex:
         torch.cuda.synchronize()
