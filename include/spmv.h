@@ -68,10 +68,14 @@ typedef enum {
 
 /* CSR kernel algorithms: scalar (thread per row), vector (T lanes per row,
  * the "coordination among threads within a warp" of P:159), merge-path, and
- * stream (a block stages the CSR segment of its rows in shared memory with
- * coalesced loads, then a thread per row gathers x — consecutive rows gather
- * together, as in ELL, without ELL's padding; blocks whose segment does not
- * fit fall back to warp-per-row). */
+ * stream (tiles of consecutive rows: a producer warp bulk-copies each tile's
+ * contiguous col/val segment into a two-stage shared-memory ring with TMA
+ * (cp.async.bulk + mbarrier), then a thread per row gathers x — consecutive
+ * rows gather together, as in ELL, without ELL's padding and without a
+ * conversion; tiles whose segment does not fit a stage fall back to
+ * warp-per-row; meant for regular rows — the selector measures it only when
+ * rows are not skewed; launch knob = entries per row slot, 16/32/64; block
+ * 1024 is refused since the producer warp makes it 1056 threads). */
 typedef enum {
   SPMV_CSR_AUTO = 0,
   SPMV_CSR_SCALAR = 1,
