@@ -71,6 +71,7 @@ void selector_class_format(int cls, int* fmt, spmv_format_params_t* p) {
     case 5: *fmt = SPMV_FMT_COO; break;
     case 6: *fmt = SPMV_FMT_BELL; p->bell_b = 2; break;
     case 7: *fmt = SPMV_FMT_BELL; p->bell_b = 3; break;
+    case 8: *fmt = SPMV_FMT_CSR; p->csr_alg = SPMV_CSR_STREAM; break;
     default: *fmt = SPMV_FMT_CSR; p->csr_alg = SPMV_CSR_VECTOR; break;
   }
 }

@@ -66,8 +66,8 @@ def test_class_to_format_mapping():
     recs = _records()
     fmts = {"CSR-vector": (P.FMT_CSR, P.CSR_VECTOR), "CSR-merge": (P.FMT_CSR, P.CSR_MERGE), "ELL": (P.FMT_ELL, None),
             "SELL": (P.FMT_SELL, None), "HYB": (P.FMT_HYB, None), "COO": (P.FMT_COO, None),
-            "BELL-2": (P.FMT_BELL, None), "BELL-3": (P.FMT_BELL, None)}
-    for r in recs[:20]:
+            "BELL-2": (P.FMT_BELL, None), "BELL-3": (P.FMT_BELL, None), "CSR-stream": (P.FMT_CSR, P.CSR_STREAM)}
+    for r in recs:
         p = P.spmv_predict(r["features"])
         fmt, alg = fmts[p["class"]]
         assert p["format"] == fmt

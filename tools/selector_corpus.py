@@ -31,7 +31,8 @@ VARIANTS = [("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)),
             ("HYB", P.FMT_HYB, {}),
             ("COO", P.FMT_COO, {}),
             ("BELL-2", P.FMT_BELL, dict(bell_b=2)),
-            ("BELL-3", P.FMT_BELL, dict(bell_b=3))]
+            ("BELL-3", P.FMT_BELL, dict(bell_b=3)),
+            ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM))]
 
 
 # ---------------------------------------------------------------- inputs (seeded, vectorised numpy)
@@ -130,7 +131,7 @@ def time_kernel(h, fmt, x, y):
     return statistics.median(ts) * 1e-3
 
 
-def measure(name, coo, tune=True):
+def measure(name, coo, tune=True, variants=None, rec=None):
     t0 = time.time()
     row = torch.from_numpy(coo.row).cuda()
     col = torch.from_numpy(coo.col).cuda()
@@ -138,14 +139,19 @@ def measure(name, coo, tune=True):
     n, m = coo.rows, coo.cols
     x = torch.from_numpy(si.vector(m)).cuda()
     y = torch.empty(n, dtype=torch.float64, device="cuda")
-    rec = {"name": name, "n": n, "cols": m, "nnz": int(coo.row.shape[0]), "formats": {}}
     h = P.spmv_create(n, m, row, col, val)
     feats = P.spmv_features(h)
     f_lat, _ = P.spmv_overheads(h)
-    rec["features"] = feats
-    rec["f_latency_s"] = f_lat
+    if rec is None:  # a fresh record (else: add the requested variants to an existing one)
+        rec = {"name": name, "n": n, "cols": m, "nnz": int(coo.row.shape[0]), "formats": {}}
+        rec["features"] = feats
+        rec["f_latency_s"] = f_lat
+    else:
+        assert rec["features"] == feats, name  # the same seeded matrix
     del row, col, val
     for vname, fmt, params in VARIANTS:
+        if variants and vname not in variants:
+            continue
         r = {}
         if vname.startswith("BELL") and (feats["mean"] < 4 or feats["std"] > feats["mean"]):
             r["skipped"] = "not block-like (mean < 4 or std > mean)"
@@ -183,15 +189,25 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "selector_corpus.jsonl"))
     ap.add_argument("--only", default="", help="comma list of name prefixes")
     ap.add_argument("--no-tune", action="store_true")
+    ap.add_argument("--variants", default="", help="comma list of variant names to measure (default all)")
+    ap.add_argument("--merge", default="", help="existing corpus .jsonl: add the measured variants to its records")
     a = ap.parse_args()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    variants = a.variants.split(",") if a.variants else None
+    old = {}
+    if a.merge:
+        for line in open(a.merge):
+            r = json.loads(line)
+            old[r["name"]] = r
     with open(a.out, "w") as f:
         for name, gen in corpus_specs():
             if a.only and not any(name.startswith(p) for p in a.only.split(",")):
                 continue
             try:
                 coo = gen()
-                rec = measure(name, coo, tune=not a.no_tune)
+                prev = old.get(name)
+                rec = measure(name, coo, tune=not a.no_tune, variants=variants,
+                              rec=prev if prev and "formats" in prev else None)
             except Exception as e:  # record and continue
                 rec = {"name": name, "error": repr(e)[:200]}
             f.write(json.dumps(rec) + "\n")

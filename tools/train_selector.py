@@ -27,7 +27,7 @@ import sys
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-CLASSES = ["CSR-vector", "CSR-merge", "ELL", "SELL", "HYB", "COO", "BELL-2", "BELL-3"]
+CLASSES = ["CSR-vector", "CSR-merge", "ELL", "SELL", "HYB", "COO", "BELL-2", "BELL-3", "CSR-stream"]
 FEATURES = ["log2_rows", "log2_nnz", "mean", "var", "std", "ell_ratio", "median", "mode", "max_len", "min_len",
             "empty_frac", "bandwidth_frac", "cv", "max_over_mean", "vbytes"]
 
