@@ -143,3 +143,90 @@ def test_fullsize_every_format(cfg):
                 P.spmv_convert(h, P.FMT_CSR)
     finally:
         P.spmv_destroy(h)
+
+
+def c5_windows(n, plane):
+    """Row windows of c5 checked against the oracle: the first and last rows
+    (boundary planes), a plane seam, the middle, and scattered single rows."""
+    w = [(0, 700), (n - 700, n), (plane - 350, plane + 350), (n // 2 - 350, n // 2 + 350)]
+    rng = np.random.default_rng(11)
+    w += [(int(r), int(r) + 1) for r in rng.choice(n - 1, size=40, replace=False)]
+    return w
+
+
+@pytest.mark.timeout(2400)
+def test_fullsize_c5_bench_configuration():
+    """c5 (27-point 512^3, 3.61e9 nnz, int64 row pointers) on one GPU, in the
+    configuration bench.py --config c5 times (spmv_tune decision), plus the
+    CSR-stream and ELL kernels: y on sampled row windows against the oracle,
+    the window rows regenerated on the host (the full matrix is 58 GB of
+    triplets, too large for the oracle); then three native power steps."""
+    coo = si.config_device("c5")
+    n = coo.rows
+    nnz = coo.nnz
+    h = P.spmv_create(coo.rows, coo.cols, coo.row, coo.col, coo.val)
+    del coo
+    torch.cuda.empty_cache()
+    try:
+        fd = P.spmv_features(h)
+        # closed forms for the 27-point stencil on N^3 (SURVEY §8.0): nnz = (3N-2)^3, bandwidth N^2+N+1
+        N = 512
+        assert nnz == (3 * N - 2) ** 3 == fd["nnz"] == 3609741304
+        assert fd["max_len"] == 27 and fd["min_len"] == 8 and fd["n_empty"] == 0
+        assert fd["bandwidth"] == N * N + N + 1 and fd["median"] == 27.0 and fd["mode"] == 27
+        assert P.spmv_format_info(h, P.FMT_CSR)["row_ptr_is64"]
+        wins = c5_windows(n, N * N)
+        x = si.vector_device(n)
+        xh = x.cpu().numpy()
+        yin = si.vector_device(n, seed=si.Y_SEED)
+        refs = []
+        for r0, r1 in wins:
+            w = si.stencil(si.STENCIL27, N, r0, r1, random_values=True)
+            st, R, C, V = oracle.canonicalize(w.rows, w.cols, w.row, w.col, w.val)
+            refs.append((r0, r1, oracle.csr(r1 - r0, R), C, V))
+        sel = np.concatenate([np.arange(r0, r1) for r0, r1, *_ in refs])
+
+        def check(y, alpha, beta, xv, yinh, label):
+            yg = y.cpu().numpy()
+            for r0, r1, rp, C, V in refs:
+                yi = None if yinh is None else yinh[r0:r1]
+                y_ref, a_ref = oracle.spmv_csr(r1 - r0, rp, C, V, xv, alpha, beta, yi)
+                ok, worst, bad = oracle.parity_check(yg[r0:r1], y_ref, a_ref, alpha, beta, yi, 1e-12)
+                assert ok, (label, r0, worst, bad[:5])
+
+        rep = P.spmv_tune(h, P.TUNE_ALL, expected_iterations=100)
+        yinh = yin.cpu().numpy()
+        cases = [("tuned:" + P.FORMAT_NAMES[rep.format], None, None),
+                 ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM)), ("ELL", P.FMT_ELL, {})]
+        for label, fmt, params in cases:
+            if fmt is not None:
+                P.spmv_convert(h, fmt, **params)
+            y = yin.clone()
+            P.spmv_run(h, 2.5, x, -0.5, y)
+            torch.cuda.synchronize()
+            check(y, 2.5, -0.5, xh, yinh, label)
+            del y
+            if fmt == P.FMT_ELL:
+                break
+            if fmt is not None:
+                P.spmv_convert(h, P.FMT_CSR)
+        # three native power steps on the ELL kernel (bench's c5 hot loop shape)
+        from paper_2302_05662_b200.dist import Layout, native_power_iteration
+        layout = Layout.from_bounds(np.array([0, n]))
+        zprev = None
+        for steps in (1, 2):
+            bufs = {"cur": torch.zeros(n, dtype=torch.float64, device="cuda"),
+                    "nxt": torch.zeros(n, dtype=torch.float64, device="cuda"),
+                    "chunk": torch.zeros(1, dtype=torch.float64, device="cuda"),
+                    "sums": torch.zeros(steps + 1, 2, dtype=torch.float64, device="cuda")}
+            z, sums, _ = native_power_iteration(h, layout, 0, x, bufs, steps)
+            torch.cuda.synchronize()
+            zk = z.cpu().numpy()
+            if steps == 2:
+                xk = zprev / np.sqrt(sums[1, 0].item())
+                check(z, 1.0, 0.0, xk, None, "power step 2")
+            zprev = zk
+            del bufs, z
+        assert len(sel) > 2800
+    finally:
+        P.spmv_destroy(h)
