@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -39,6 +40,12 @@ void* dalloc(size_t bytes, cudaStream_t s) {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      // Handles on different streams must not serialise through the pool: a
+      // block freed on stream A is reused on stream B only once A's free has
+      // completed (opportunistic), never by making B wait on A's work.
+      const char* dep = std::getenv("SPMV_POOL_INTERNAL_DEPS");
+      int no = (dep && dep[0] == '1') ? 1 : 0;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
     }
     g_pool_ready[dev] = true;
   }
@@ -58,6 +65,26 @@ void* dalloc(size_t bytes, cudaStream_t s) {
   return p;
 }
 
+// Small device->host read-backs go through a per-thread pinned buffer: a copy
+// into pageable memory is staged by the driver and was measured waiting for
+// another stream's bulk host upload (two handles in flight, bench e2e).
+void d2h_sync(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t s) {
+  thread_local void* pin = nullptr;
+  thread_local size_t pin_bytes = 0;
+  if (bytes == 0) return;
+  if (pin_bytes < bytes) {
+    if (pin) cudaFreeHost(pin);
+    pin = nullptr;
+    pin_bytes = 0;
+    const size_t want = std::max<size_t>(bytes, 64 << 10);
+    CK(cudaMallocHost(&pin, want));
+    pin_bytes = want;
+  }
+  CK(cudaMemcpyAsync(pin, dev_src, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::memcpy(host_dst, pin, bytes);
+}
+
 void dfree(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
 }
@@ -73,7 +100,11 @@ int64_t persistent_grid(const void* func, int block, int64_t needed_blocks, size
       CK(cudaGetDevice(&dev));
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    const uint64_t key = (uint64_t)(uintptr_t)func ^ ((uint64_t)block << 48) ^ ((uint64_t)dyn_smem << 20);
+    // the carveout set on func changes the shared-memory-limited occupancy
+    auto cv = g_carveout.find(func);
+    const uint64_t carve = cv == g_carveout.end() ? 127 : (uint64_t)cv->second;
+    const uint64_t key = (uint64_t)(uintptr_t)func ^ ((uint64_t)block << 48) ^ ((uint64_t)dyn_smem << 20) ^
+                         (carve << 56);
     auto it = occ.find(key);
     if (it == occ.end()) {
       int nb = 0;

@@ -276,8 +276,7 @@ __global__ void k_bell_fill(const RP* __restrict__ rp, const int32_t* __restrict
 
 int64_t read_i64(const int64_t* d, cudaStream_t s) {
   int64_t v = 0;
-  CK(cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  d2h_sync(&v, d, sizeof(v), s);
   return v;
 }
 
@@ -492,8 +491,7 @@ void bell_typed(spmv_matrix* h, int64_t b) {
   CK(cudaMemsetAsync(d_kb, 0, sizeof(unsigned long long), s));
   if (nbr > 0) LAUNCH(k_bell_count<RP>, grid_for(nbr, 256), 256, 0, s, rp, h->col, rows, b, nbr, d_kb);
   unsigned long long kbu = 0;
-  CK(cudaMemcpyAsync(&kbu, d_kb, sizeof(kbu), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  d2h_sync(&kbu, d_kb, sizeof(kbu), s);
   const int64_t kb = (int64_t)kbu;
   guard_bytes((double)kb * nbr_pad * (4.0 + b * b * sizeof(V)), "BELL");
   int32_t* bcol = sc.get<int32_t>(kb * nbr_pad);
@@ -541,8 +539,7 @@ bool offsets16_fit(spmv_matrix* h) {
     LAUNCH(k_offset_range<int32_t>, g, 256, 0, h->stream, static_cast<const int32_t*>(h->row_ptr), h->col, h->rows,
            h->col_origin, d);
   unsigned long long m = 0;
-  CK(cudaMemcpyAsync(&m, d, sizeof(m), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
+  d2h_sync(&m, d, sizeof(m), h->stream);
   return m <= 32767ull;
 }
 
@@ -648,8 +645,7 @@ double format_latency(spmv_matrix* h, int fmt) {
 int64_t sell_slots(spmv_matrix* h) {
   if (h->sell_built && h->sell_slots_pending) {
     int64_t v = 0;
-    CK(cudaMemcpyAsync(&v, h->sell_sp + h->sell_ns, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    d2h_sync(&v, h->sell_sp + h->sell_ns, sizeof(v), h->stream);
     h->sell_slots = v;
     h->sell_slots_pending = false;
   }

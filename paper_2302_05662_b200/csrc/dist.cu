@@ -223,13 +223,34 @@ struct LocalComm : CommBase {
 // Power iteration loop (declared in handle.cuh). z_k is written straight
 // into this rank's chunk of the next replicated buffer; the all-gather is in
 // place (chunk_buf is not needed).
+// Device-to-device copy as a kernel: a cudaMemcpyAsync would go to a copy
+// engine, where it can queue behind another stream's host upload.
+__global__ void k_copy16(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) dst[i] = src[i];
+}
+__global__ void k_copy1(unsigned char* __restrict__ dst, const unsigned char* __restrict__ src, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
+}
+static void device_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  if ((((uintptr_t)dst | (uintptr_t)src | bytes) & 15) == 0) {
+    const int64_t n16 = (int64_t)(bytes / 16);
+    LAUNCH(k_copy16, grid_for(n16, 256), 256, 0, s, static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16);
+  } else {
+    LAUNCH(k_copy1, grid_for((int64_t)bytes, 256), 256, 0, s, static_cast<unsigned char*>(dst),
+           static_cast<const unsigned char*>(src), (int64_t)bytes);
+  }
+}
+
 void power_iterate(spmv_matrix* h, const void* x0, void* buf0, void* buf1, int64_t n_full, int64_t steps,
                    double* sums, void* comm_v, int64_t chunk, void* /*chunk_buf*/, float* kernel_ms, float* loop_ms,
                    int* final_buf) {
   cudaStream_t s = h->stream;
   CommBase* comm = as_comm(comm_v);
   const int vb = h->vbytes;
-  if (x0 != buf0) CK(cudaMemcpyAsync(buf0, x0, (size_t)n_full * vb, cudaMemcpyDeviceToDevice, s));
+  if (x0 != buf0) device_copy(buf0, x0, (size_t)n_full * vb, s);
   const int64_t row_offset = comm ? (int64_t)comm->rank * chunk : 0;
   if (comm && (comm->rank + 1) * chunk > n_full) fail(SPMV_ERR_INVALID_ARG, "power_iterate: world·chunk > n_full");
   // S_0 = ||z_0||² over this rank's rows, then summed over ranks

@@ -107,12 +107,18 @@ __global__ void __launch_bounds__(kStatThreads) k_row_stats(const RP* __restrict
   }
 }
 
+// Order-statistic ranks, passed by value (no host->device copy that could
+// queue behind another stream's bulk upload on the copy engine).
+struct SelectTargets {
+  long long v[4];
+};
+
 // One block of 1024 threads. out[t] = the targets[t]-th smallest row length
 // (0-based, targets[t] < rows), t < 3; out[3] = mode (smallest most frequent).
 __global__ void __launch_bounds__(1024) k_select(const unsigned* __restrict__ hist,
                                                  const long long* __restrict__ big,
                                                  const unsigned long long* __restrict__ nbig_p,
-                                                 const long long* __restrict__ targets,
+                                                 const SelectTargets targets,
                                                  const StatPartial* __restrict__ part, int nparts,
                                                  long long* __restrict__ out) {
   __shared__ long long s_chunk[kChunks + 1];
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(1024) k_select(const unsigned* __restrict__ hi
   __syncthreads();
   const long long small_total = s_chunk[kChunks];
   for (int q = 0; q < 3; ++q) {
-    long long r = targets[q];
+    long long r = targets.v[q];
     if (r < 0) {
       if (t == 0) out[q] = -1;
       continue;
@@ -229,7 +235,6 @@ void features_typed(spmv_matrix* h) {
   const int64_t big_cap = h->nnz / kBins + 1;
   long long* big = sc.get<long long>(big_cap);
   unsigned long long* nbig = sc.get<unsigned long long>(1);
-  long long* d_targets = sc.get<long long>(4);
   long long* d_out = sc.get<long long>(4);
 
   // Order-statistic ranks: median lo/hi, and the HYB rule's rank (R12):
@@ -245,17 +250,17 @@ void features_typed(spmv_matrix* h) {
   CK(cudaEventRecord(e0, s));
   CK(cudaMemsetAsync(hist, 0, kBins * sizeof(unsigned), s));
   CK(cudaMemsetAsync(nbig, 0, sizeof(unsigned long long), s));
-  CK(cudaMemcpyAsync(d_targets, targets, sizeof(targets), cudaMemcpyHostToDevice, s));
   LAUNCH(k_row_stats<RP>, grid, kStatThreads, 0, s, static_cast<const RP*>(h->row_ptr), h->col, n, part,
          hist, big, nbig);
+  SelectTargets tg;
+  for (int i = 0; i < 4; ++i) tg.v[i] = targets[i];
   LAUNCH(k_select, 1, 1024, 0, s, (const unsigned*)hist, (const long long*)big,
-         (const unsigned long long*)nbig, (const long long*)d_targets, (const StatPartial*)part, (int)grid, d_out);
+         (const unsigned long long*)nbig, tg, (const StatPartial*)part, (int)grid, d_out);
   std::vector<StatPartial> hp(grid);
   long long res[4];
-  CK(cudaMemcpyAsync(hp.data(), part, grid * sizeof(StatPartial), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(res, d_out, sizeof(res), cudaMemcpyDeviceToHost, s));
   CK(cudaEventRecord(e1, s));
-  CK(cudaStreamSynchronize(s));
+  d2h_sync(hp.data(), part, grid * sizeof(StatPartial), s);
+  d2h_sync(res, d_out, sizeof(res), s);
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);

@@ -179,6 +179,8 @@ bool nvml_available();
 // Make sure the power-step partial buffers hold >= nblocks entries.
 void ensure_pi_scratch(spmv_matrix* h, size_t nblocks);
 void* ensure_seg_scratch(spmv_matrix* h, size_t bytes);
+// device->host copy of a small result through pinned memory; synchronises s
+void d2h_sync(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t s);
 void* ensure_fixup_scratch(spmv_matrix* h, size_t bytes);
 
 // Resolve a launch variant to the defaults of its kernel.

@@ -162,8 +162,7 @@ unsigned run_check(spmv_matrix* h, const int32_t* R, const int32_t* Cc, const V*
            h->cols, rp, d_flags, gaps, ngaps, cap);
   LAUNCH(k_fill_gaps<RP>, kNumSMs * 4, 256, 0, s, rp, (const Gap*)gaps, (const unsigned long long*)ngaps, cap);
   unsigned flags = 0;
-  CK(cudaMemcpyAsync(&flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  d2h_sync(&flags, d_flags, sizeof(unsigned), s);
   return flags;
 }
 
@@ -189,9 +188,17 @@ void ingest_typed(spmv_matrix* h, const int32_t* row_idx, const int32_t* col_idx
   bool copy_mode;
   if (where == SPMV_MEM_HOST) {
     r_tmp = sc.get<int32_t>(nnz);
-    CK(cudaMemcpyAsync(r_tmp, row_idx, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(h->col, col_idx, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(hval, vals, nnz * sizeof(V), cudaMemcpyHostToDevice, s));
+    // 64 MB pieces: another stream's copies (e.g. the next handle's vector
+    // upload) interleave instead of queueing behind a whole-matrix upload
+    auto upload = [&](void* dst, const void* src, size_t bytes) {
+      constexpr size_t kPiece = (size_t)64 << 20;
+      for (size_t off = 0; off < bytes; off += kPiece)
+        CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off,
+                           std::min(kPiece, bytes - off), cudaMemcpyHostToDevice, s));
+    };
+    upload(r_tmp, row_idx, nnz * sizeof(int32_t));
+    upload(h->col, col_idx, nnz * sizeof(int32_t));
+    upload(hval, vals, nnz * sizeof(V));
     R = r_tmp;
     Cc = h->col;
     Vsrc = hval;
