@@ -40,12 +40,6 @@ void* dalloc(size_t bytes, cudaStream_t s) {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      // Handles on different streams must not serialise through the pool: a
-      // block freed on stream A is reused on stream B only once A's free has
-      // completed (opportunistic), never by making B wait on A's work.
-      const char* dep = std::getenv("SPMV_POOL_INTERNAL_DEPS");
-      int no = (dep && dep[0] == '1') ? 1 : 0;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
     }
     g_pool_ready[dev] = true;
   }
