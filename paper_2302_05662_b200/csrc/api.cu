@@ -763,6 +763,7 @@ static void destroy_handle(spmv_matrix* h) {
   for (int f = 0; f < SPMV_NUM_FORMATS; ++f) free_format(h, f);
   dfree(h->seg_scratch, h->stream);
   dfree(h->fix_scratch, h->stream);
+  dfree(h->merge_coords, h->stream);
   dfree(h->pi_partials, h->stream);
   dfree(h->pi_counter, h->stream);  // stream-ordered frees: no host synchronisation
   for (auto& evs : h->lat_ev)

@@ -84,6 +84,11 @@ struct spmv_matrix {
   size_t seg_scratch_bytes = 0;
   void* fix_scratch = nullptr;
   size_t fix_scratch_bytes = 0;
+  // merge-path partition (chunk start coordinates) cached per items-per-thread:
+  // the CSR arrays never change after create, so it is computed once
+  int64_t* merge_coords = nullptr;
+  int64_t merge_coords_n = 0;
+  int merge_coords_ipt = 0;
   double* pi_partials = nullptr;
   unsigned* pi_counter = nullptr;
   size_t pi_partials_n = 0;

@@ -84,14 +84,17 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
   const int64_t items = 32LL * ipt;
   const int64_t nchunks = (total + items - 1) / items;
   if (nchunks <= 0) return;
-  // chunk records + partition coordinates share the grow-only scratch
-  const size_t rec_bytes = ((size_t)nchunks * sizeof(ChunkRec) + 255) / 256 * 256;
-  char* scratch = static_cast<char*>(ensure_seg_scratch(h, rec_bytes + (size_t)(nchunks + 1) * 2 * sizeof(int64_t)));
-  p.recs = reinterpret_cast<ChunkRec*>(scratch);
-  int64_t* coords = reinterpret_cast<int64_t*>(scratch + rec_bytes);
-  p.coords = coords;
+  p.recs = static_cast<ChunkRec*>(ensure_seg_scratch(h, (size_t)nchunks * sizeof(ChunkRec)));
+  if (!h->merge_coords || h->merge_coords_ipt != ipt || h->merge_coords_n != nchunks) {
+    dfree(h->merge_coords, h->stream);
+    h->merge_coords = nullptr;
+    h->merge_coords = static_cast<int64_t*>(dalloc((size_t)(nchunks + 1) * 2 * sizeof(int64_t), h->stream));
+    kern::merge_partition(h->row_ptr, h->rp64, h->rows, h->nnz, items, nchunks, h->merge_coords, h->stream);
+    h->merge_coords_ipt = ipt;
+    h->merge_coords_n = nchunks;
+  }
+  p.coords = h->merge_coords;
   p.nchunks = nchunks;
-  kern::merge_partition(h->row_ptr, h->rp64, h->rows, h->nnz, items, nchunks, coords, h->stream);
   // mode 1 (power step): alpha from device, beta = 0; the norms are computed
   // afterwards by run_norms because boundary rows finish in the fixup.
   const int64_t grid = (nchunks * 32 + L.block - 1) / L.block;
