@@ -22,7 +22,11 @@
  *  - On any error, `*out` handles stay NULL and nothing leaks; the handle's
  *    spmv_last_error() holds the detail (incl. CUDA error text).
  *  - Calls on one handle must be externally serialised; distinct handles are
- *    independent.
+ *    independent and may be driven from different host threads on different
+ *    streams at the same time (tests/test_gpu_concurrent.py). Host uploads in
+ *    spmv_create go in 64 MB pieces, and small results are read back through
+ *    a per-thread pinned buffer, so one handle's work does not wait for
+ *    another handle's copies.
  */
 #ifndef SPMV_H
 #define SPMV_H
