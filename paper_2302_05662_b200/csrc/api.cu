@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <new>
 #include <sstream>
@@ -27,7 +28,11 @@ thread_local int g_sm_reserve = 0;
 namespace {
 std::mutex g_mu;
 bool g_pool_ready[64] = {};
-std::unordered_map<const void*, int> g_carveout;
+// launch attributes per (device, function): carveout in effect (-1 = driver
+// default) and the dynamic shared memory opted in
+std::recursive_mutex g_attr_mu;
+std::map<std::pair<int, const void*>, int> g_carveout;
+std::map<std::pair<int, const void*>, size_t> g_dyn_smem;
 thread_local std::string g_err;
 }  // namespace
 
@@ -86,19 +91,19 @@ void dfree(void* p, cudaStream_t s) {
 int64_t persistent_grid(const void* func, int block, int64_t needed_blocks, size_t dyn_smem) {
   static std::unordered_map<uint64_t, int> occ;
   static int sms = 0;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
   int per_sm;
+  // the carveout in effect for func on this device changes the
+  // shared-memory-limited occupancy (lock order: g_attr_mu, then g_mu)
+  std::lock_guard<std::recursive_mutex> alk(g_attr_mu);
+  auto cv = g_carveout.find({dev, func});
+  const uint64_t carve = cv == g_carveout.end() || cv->second < 0 ? 127 : (uint64_t)cv->second;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    if (sms == 0) {
-      int dev = 0;
-      CK(cudaGetDevice(&dev));
-      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    // the carveout set on func changes the shared-memory-limited occupancy
-    auto cv = g_carveout.find(func);
-    const uint64_t carve = cv == g_carveout.end() ? 127 : (uint64_t)cv->second;
+    if (sms == 0) CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const uint64_t key = (uint64_t)(uintptr_t)func ^ ((uint64_t)block << 48) ^ ((uint64_t)dyn_smem << 20) ^
-                         (carve << 56);
+                         (carve << 56) ^ ((uint64_t)dev << 40);
     auto it = occ.find(key);
     if (it == occ.end()) {
       int nb = 0;
@@ -111,22 +116,26 @@ int64_t persistent_grid(const void* func, int block, int64_t needed_blocks, size
   return needed_blocks < cap ? needed_blocks : cap;
 }
 
-void set_max_dynamic_smem(const void* func, size_t bytes) {
-  static std::unordered_map<const void*, size_t> done;
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto it = done.find(func);
-  if (it != done.end() && it->second >= bytes) return;
-  CK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  done[func] = bytes;
-}
-
-void set_carveout(const void* func, int pct) {
-  if (pct < 0) return;
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto it = g_carveout.find(func);
-  if (it != g_carveout.end() && it->second == pct) return;
-  CK(cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-  g_carveout[func] = pct;
+LaunchAttrs::LaunchAttrs(const void* fn, int pct, size_t dyn_smem) : lk_(g_attr_mu) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const std::pair<int, const void*> key{dev, fn};
+  if (dyn_smem > 0) {
+    auto it = g_dyn_smem.find(key);
+    if (it == g_dyn_smem.end() || it->second < dyn_smem) {
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
+      g_dyn_smem[key] = dyn_smem;
+    }
+  }
+  const int want = pct < 0 ? -1 : pct;
+  auto it = g_carveout.find(key);
+  const int have = it == g_carveout.end() ? -1 : it->second;
+  if (have != want) {
+    // -1 is cudaSharedmemCarveoutDefault: restores the driver's choice
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            want < 0 ? (int)cudaSharedmemCarveoutDefault : want));
+    g_carveout[key] = want;
+  }
 }
 
 void ensure_pi_scratch(spmv_matrix* h, size_t nblocks) {
@@ -550,6 +559,7 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
       case SPMV_FMT_COO: build_coo(h); break;
     }
   };
+  std::vector<int> built_here;  // candidates this call converted (the caller's own builds are kept)
   auto try_build = [&](int fmt, const char* why) {
     bool was = built(h, fmt);
     try {
@@ -577,6 +587,7 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
     if (!was) {  // warm conversion latency: rebuild once the kernels are loaded
       free_format(h, fmt);
       do_build(fmt);
+      built_here.push_back(fmt);
     }
     auto m = measure(fmt, h->launch[fmt]);
     cands.push_back({fmt, 0, m.first, format_latency(h, fmt), why, Measured{}, m.second});
@@ -649,8 +660,8 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
      << (chosen == SPMV_FMT_CSR && chosen_alg == SPMV_CSR_STREAM ? "-stream" : "") << "\"}";
   log_append(h, os.str());
   // release candidates that were built here and not chosen
-  for (const Cand& c : cands)
-    if (c.fmt != chosen && c.fmt != SPMV_FMT_CSR) free_format(h, c.fmt);
+  for (int fmt : built_here)
+    if (fmt != chosen) free_format(h, fmt);
   h->active = chosen;
   if (chosen == SPMV_FMT_CSR) h->csr_alg = chosen_alg;
   if (tune_each) {  // the chosen end state keeps its tuned launch

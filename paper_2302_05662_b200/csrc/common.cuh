@@ -93,64 +93,73 @@ constexpr int kNumSMs = 148;
 
 // ---------------------------------------------------------------- device helpers
 
+// L2 cache policies (createpolicy; both fold into the load's uniform
+// descriptor, so they cost no instruction in the loop).
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // Streaming loads of the matrix arrays: read once per SpMV, so do not allocate
 // in L1 and mark evict-first in L2 (x stays resident instead).
-__device__ __forceinline__ int ld_stream(const int* p) {
-  int r;
-  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
-  return r;
-}
+#define SPMV_LD_STREAM(T, SUF, CONS)                                                                   \
+  __device__ __forceinline__ T ld_stream(const T* p) {                                                  \
+    T r;                                                                                                \
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint." SUF " %0, [%1], %2;" : "=" CONS(r) : "l"(p),     \
+        "l"(l2_evict_first()));                                                                         \
+    return r;                                                                                           \
+  }
+SPMV_LD_STREAM(int, "b32", "r")
+SPMV_LD_STREAM(float, "f32", "f")
+SPMV_LD_STREAM(double, "f64", "d")
+#undef SPMV_LD_STREAM
 __device__ __forceinline__ int2 ld_stream(const int2* p) {
   int2 r;
-  asm("ld.global.nc.L1::no_allocate.v2.b32 {%0,%1}, [%2];"
-               : "=r"(r.x), "=r"(r.y) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.b32 {%0,%1}, [%2], %3;"
+      : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(l2_evict_first()));
   return r;
 }
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
-  asm("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ float ld_stream(const float* p) {
-  float r;
-  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ double ld_stream(const double* p) {
-  double r;
-  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(l2_evict_first()));
   return r;
 }
 __device__ __forceinline__ float2 ld_stream(const float2* p) {
   float2 r;
-  asm("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];"
-               : "=f"(r.x), "=f"(r.y) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+      : "=f"(r.x), "=f"(r.y) : "l"(p), "l"(l2_evict_first()));
   return r;
 }
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   float4 r;
-  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(l2_evict_first()));
   return r;
 }
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
   double2 r;
-  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
-               : "=d"(r.x), "=d"(r.y) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+      : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(l2_evict_first()));
   return r;
 }
 
 // Gathers of x: read-only path, keep in L1, evict-last in L2 (x is reused by
-// every row that touches the column).
+// every row that touches the column; the matrix stream is evicted first).
 __device__ __forceinline__ double ld_x(const double* p) {
   double r;
-  asm("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(l2_evict_last()));
   return r;
 }
 __device__ __forceinline__ float ld_x(const float* p) {
   float r;
-  asm("ld.global.nc.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(l2_evict_last()));
   return r;
 }
 

@@ -2,6 +2,7 @@
 // by the translation units of libspmv.so.
 #pragma once
 #include <functional>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
@@ -194,9 +195,18 @@ spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t&
 // minus g_sm_reserve SMs' worth of residency (left free for concurrent NCCL kernels).
 extern thread_local int g_sm_reserve;
 int64_t persistent_grid(const void* func, int block, int64_t needed_blocks, size_t dyn_smem = 0);
-// Opt in to `bytes` of dynamic shared memory for func (cached).
-void set_max_dynamic_smem(const void* func, size_t bytes);
-// Carveout attribute (cached per function pointer).
-void set_carveout(const void* func, int pct);
+// Function attributes of one launch, applied on the CURRENT device (CUDA
+// function attributes are per device): the preferred shared-memory carveout
+// (pct < 0 = driver default, restored if an earlier launch changed it) and
+// the dynamic shared-memory opt-in. The object holds the process-wide
+// launch-attribute lock until it is destroyed, so the attributes cannot be
+// changed by another thread between the set and the launch: construct it
+// right before computing the grid and keep it in scope through the launch.
+class LaunchAttrs {
+ public:
+  LaunchAttrs(const void* fn, int carveout_pct, size_t dyn_smem = 0);
+ private:
+  std::unique_lock<std::recursive_mutex> lk_;
+};
 
 }  // namespace spmv

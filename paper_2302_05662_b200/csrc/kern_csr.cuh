@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(B + 32) __maxnreg__(regcap(B + 32, R)) k_csr_s
           // lane-dependent rotation. Other lengths (the stencil's 27) keep
           // k-aligned lanes, so the gathers of a step stay on adjacent x.
           int rot = (len & 7) == 0 && len > 0 ? lane : 0;
-          if (rot >= len) rot %= len;
+          if (len > 0 && rot >= len) rot %= len;
           for (int k = 0; k < len; k += U) {
             int c[U];
             T v[U];

@@ -23,7 +23,7 @@ template <int N>
 __device__ __forceinline__ void load_d16(const int16_t* p, int (&d)[N]) {
   if constexpr (N == 1) {
     unsigned short v;
-    asm("ld.global.nc.L1::no_allocate.b16 %0, [%1];" : "=h"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(l2_evict_first()));
     d[0] = (int)(int16_t)v;
   } else {
     constexpr int W = N / 2;  // 32-bit words

@@ -14,7 +14,7 @@ void launch_bell(spmv_matrix* h, kern::BellParams& p, const spmv_launch_t& L) {
     case 4: fn = (const void*)kern::bell_fn<T, 4>(bi, ri); break;
     default: fail(SPMV_ERR_UNSUPPORTED, "BELL block dimension must be 2, 3 or 4");
   }
-  set_carveout(fn, L.carveout_pct);
+  const LaunchAttrs attrs(fn, L.carveout_pct);
   const int64_t grid = persistent_grid(fn, L.block, (p.nbr + L.block - 1) / L.block);
   if (grid <= 0) return;
   if (p.e.mode == 1) {

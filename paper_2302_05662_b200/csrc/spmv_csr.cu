@@ -29,8 +29,7 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     if (smem > 227 * 1024 - 1024) fail(SPMV_ERR_UNSUPPORTED, "CSR-stream block × entries exceeds shared memory");
     if (((uintptr_t)h->col | (uintptr_t)h->val) & 15)
       fail(SPMV_ERR_UNSUPPORTED, "CSR-stream: col/val must be 16-byte aligned for the bulk copies");
-    set_carveout(fn, L.carveout_pct);
-    set_max_dynamic_smem(fn, smem);
+    const LaunchAttrs attrs(fn, L.carveout_pct, smem);
     const int threads = L.block + 32;  // B consumer threads + one TMA producer warp
     const int64_t grid = persistent_grid(fn, threads, (h->rows + L.block - 1) / L.block, smem);
     if (grid <= 0) return;
@@ -55,7 +54,7 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
       case 32: fn = (const void*)kern::csr_vector_fn<T, RP, 32>(bi, ri); break;
       default: fail(SPMV_ERR_INVALID_ARG, "CSR-vector lanes per row must be 1,2,4,8,16 or 32");
     }
-    set_carveout(fn, L.carveout_pct);
+    const LaunchAttrs attrs(fn, L.carveout_pct);
     const int ur = lanes >= 16 ? 4 : (lanes >= 4 ? 2 : 1);
     const int64_t groups = (h->rows + ur - 1) / ur;
     const int64_t grid = persistent_grid(fn, L.block, (groups * lanes + L.block - 1) / L.block);
@@ -77,9 +76,8 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     case 16: fn = (const void*)kern::csr_merge_fn<T, RP, 16>(bi, ri); break;
     default: fail(SPMV_ERR_INVALID_ARG, "merge-path items per thread must be 4, 8 or 16");
   }
-  set_carveout(fn, L.carveout_pct);
   const size_t smem = kern::merge_smem_bytes<T>(L.block, ipt);
-  set_max_dynamic_smem(fn, smem);
+  const LaunchAttrs attrs(fn, L.carveout_pct, smem);
   const int64_t total = h->rows + h->nnz;
   const int64_t items = 32LL * ipt;
   const int64_t nchunks = (total + items - 1) / items;

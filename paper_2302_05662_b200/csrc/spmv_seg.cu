@@ -116,7 +116,7 @@ void coo_launch(spmv_matrix* h, const int32_t* row, const int32_t* col, const vo
     case 8: fn = (const void*)kern::coo_fn<T, 8>(bi, ri); break;
     default: fail(SPMV_ERR_INVALID_ARG, "COO entries per lane must be 2, 4 or 8");
   }
-  set_carveout(fn, L.carveout_pct);
+  const LaunchAttrs attrs(fn, L.carveout_pct);
   const int64_t nchunks = (nnz + 32LL * W - 1) / (32LL * W);
   kern::CooParams p{};
   p.row = row;

@@ -23,7 +23,7 @@ void launch_sliced(spmv_matrix* h, kern::SlicedParams& p, int C, const spmv_laun
     default: fail(SPMV_ERR_UNSUPPORTED, "slice height C must be 32, 64, 128 or 256");
   }
 #undef SL_PICK
-  set_carveout(fn, L.carveout_pct);
+  const LaunchAttrs attrs(fn, L.carveout_pct);
   const int64_t warps_per_block = L.block / 32;
   const int64_t grid = persistent_grid(fn, L.block, (p.nslices + warps_per_block - 1) / warps_per_block);
   if (grid <= 0) return;
