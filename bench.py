@@ -6,26 +6,45 @@ one synthetic matrix, as the paper's run-time mode applies it to an
 iterative solver:
   a1/a2 spmv_create   device COO -> validated canonical COO + CSR
   a3    spmv_features device Table 2 features
-  a6/a7 the tuner/selector's decision for this workload (format + launch),
-        measured once before timing with spmv_tune and replayed per step
-  a4    spmv_convert  CSR -> chosen format
-  a5/a8 E power-iteration steps (spmv_power_step: one SpMV kernel with the
-        fused norm epilogue; NCCL all-gather/all-reduce when N > 1)
+  a7    select        the run-time mode's own decision for THIS matrix:
+                      spmv_tune(FORMAT | PREDICT | DECIDE_ONLY) — learned
+                      format class, overhead estimates, t_CSR timed on a
+                      row sample, gate (o + p of P:1288)
+  a4    spmv_convert  CSR -> the selected format
+  a5/a8 E power-iteration steps (one SpMV kernel with the fused norm
+        epilogue per step; the distributed plan with NCCL when N > 1)
   spmv_destroy.
+The compile-time mode (a6: launch sweep) and the fully measured run-time
+mode (a7 with every candidate timed) run once before the timed region, as the
+paper's offline training does; the per-step select phase reuses their launch
+variant when it picks the same format.
 value = useful GFLOP/s = 2·nnz·E·K / (max-over-ranks device time of K steps).
 
+Default workload: c5 (27-point stencil 512^3, 3.61e9 nnz, fp64) — the
+largest BASELINE.json config that fits one B200 and the anchor of the
+8-GPU target. At N = 1 the line also carries `per_config` (c2, c3, c4: the
+tuned kernel's µs, GB/s and fraction of the measured HBM peak; for c3/c4 the
+fraction of the measured x-gather ceiling) and `cpu_baseline` (the oracle,
+1 thread and all host cores, on a bounded slab of the same matrix, in a
+subprocess).
+
 `--impl reference` times the CPU oracle (oracle/, the only reference this
-tier has) on a bounded sample of the same workload.
+tier has) on a bounded sample of the same workload, on all host cores.
+`--virtual` (with --gpus W) runs W in-process ranks on one GPU through the
+exact N > 1 branch (partition, slab remap, distributed plan) with the
+in-process communicator group instead of NCCL — an execution check of the
+multi-GPU path on a one-GPU box, not a scaling number.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
-import tempfile
+import threading
 import time
 
 import numpy as np
@@ -36,17 +55,22 @@ sys.path.insert(0, ROOT)
 METRIC = "SpMV GFLOP/s & HBM GB/s vs 8 TB/s per format at 1/2/4/8 B200; MFLOPS/W"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--iters", type=int, default=100, help="power-iteration steps per step (E)")
-    ap.add_argument("--format", default="auto", help="auto (spmv_tune) or COO/CSR/CSR-vector/CSR-merge/CSR-stream/ELL/HYB/SELL/BELL")
+    ap.add_argument("--format", default="auto",
+                    help="auto (spmv_tune) or COO/CSR/CSR-vector/CSR-merge/CSR-stream/ELL/HYB/SELL/BELL")
+    ap.add_argument("--select", default="predict", choices=["predict", "replay"],
+                    help="per-step run-time selection: predict (timed select phase) or replay the offline choice")
     ap.add_argument("--no-tune-launch", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--per-config", default="c2,c3,c4", help="N=1 extra configs measured after the headline "
+                                                                "('none' to skip)")
     ap.add_argument("--launch", default="", help="block,maxreg,carveout,knob (skips the launch sweep)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-serial", action="store_true", help="e2e one step at a time (default at N=1: two in flight)")
@@ -55,7 +79,11 @@ def parse():
     ap.add_argument("--plan", default="overlap,halo",
                     help="N>1 schedule: comma list of overlap (interior SpMV overlaps the exchange) and halo "
                          "(exchange only referenced remote entries); 'none' = split + all-gather, serialised")
-    return ap.parse_args()
+    ap.add_argument("--virtual", action="store_true",
+                    help="--gpus W ranks as W threads on ONE GPU (in-process communicator; execution check)")
+    ap.add_argument("--energy-window", type=float, default=1.0, help="minimum NVML energy window in seconds")
+    ap.add_argument("--cpu-leg", action="store_true", help=argparse.SUPPRESS)  # internal: oracle subprocess
+    return ap.parse_args(argv)
 
 
 # ----------------------------------------------------------------------------- clocks / energy
@@ -69,7 +97,6 @@ class ClockSampler:
                "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
     def __init__(self, index=0, period_s=0.25):
-        import threading
         self.samples = []
         self.stop_ev = threading.Event()
         try:
@@ -114,6 +141,9 @@ class ClockSampler:
 
 
 class Energy:
+    """NVML total-energy counter (mJ) and a 10 ms power sampler (the paper's
+    mean of power samples), read over a window of >= 1 s."""
+
     def __init__(self, index=0):
         self.h = None
         try:
@@ -123,6 +153,9 @@ class Energy:
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
         except Exception:
             self.h = None
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
 
     def read_j(self):
         if self.h is None:
@@ -131,6 +164,29 @@ class Energy:
             return self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h) / 1000.0
         except Exception:
             return None
+
+    def start_sampler(self, period_s=0.01):
+        if self.h is None:
+            return
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                except Exception:
+                    pass
+                self._stop.wait(period_s)
+        self.samples = []
+        self._stop.clear()
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop_sampler(self):
+        if self._t is None:
+            return None
+        self._stop.set()
+        self._t.join(timeout=2)
+        return statistics.mean(self.samples) if self.samples else None
 
 
 def measured_peaks():
@@ -141,83 +197,223 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def host_info():
+    info = {"nproc": os.cpu_count(), "machine": platform.machine()}
+    try:
+        txt = open("/proc/cpuinfo").read()
+        models = [ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("model name")]
+        info["cpu_model"] = models[0] if models else None
+        phys = {ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("physical id")}
+        info["sockets"] = len(phys) or 1
+    except Exception:
+        pass
+    return info
+
+
 # ----------------------------------------------------------------------------- CPU oracle arm
 
-CPU_SAMPLE = {"c1": ("lap2d", 64), "c2": ("stencil27", 64), "c3": ("rmat", 16), "c4": ("uniform", 1 << 18),
-              "c5": ("stencil27", 64)}
+# Bounded samples of each workload (SURVEY §8(d) "CPU baseline"): c5 and c2
+# use a slab of interior z-planes of the SAME stencil (rows numbered from the
+# slab start, global columns); the others a scaled-down instance.
+CPU_SAMPLE = {"c1": ("lap2d", 64, 0), "c2": ("stencil27", 128, 16), "c3": ("rmat", 18, 0),
+              "c4": ("uniform", 1 << 20, 0), "c5": ("stencil27", 512, 8)}
+REF_SAMPLE = {"c1": ("lap2d", 64, 0), "c2": ("stencil27", 128, 8), "c3": ("rmat", 16, 0),
+              "c4": ("uniform", 1 << 18, 0), "c5": ("stencil27", 512, 1)}
 
 
-def oracle_pipeline(cfg, iters, seconds_cap=None):
-    """The oracle (as it stands) on a bounded sample of the workload:
-    canonicalize -> CSR -> features -> format build -> E power steps.
-    Returns (flops, seconds, description)."""
-    import oracle
+def oracle_sample(cfg, table):
+    """(COO, x, description) of the bounded sample of `cfg` (host numpy)."""
     import spmv_inputs as si
-    kind, size = CPU_SAMPLE[cfg]
-    if kind == "lap2d":
+    kind, size, planes = table[cfg]
+    if kind == "stencil27" and planes:
+        N = size
+        z0 = N // 2 - planes // 2
+        r0, r1 = z0 * N * N, (z0 + planes) * N * N
+        coo = si.stencil(si.STENCIL27, N, r0, r1, random_values=True)
+        x = si.vector(coo.cols)
+        desc = f"stencil27({N}) rows [{r0}, {r1}) = {planes} interior z-planes"
+    elif kind == "lap2d":
         coo = si.lap2d(size, random_values=True)
-    elif kind == "stencil27":
-        coo = si.stencil27(size, random_values=True)
+        x = si.vector(coo.cols)
+        desc = f"lap2d({size})"
     elif kind == "rmat":
         coo = si.rmat(size, dtype=np.float64)
+        x = si.vector(coo.cols)
+        desc = f"rmat(scale {size}, ef 16)"
     else:
         coo = si.uniform_k(size, 32)
-    x = si.vector(coo.cols)
+        x = si.vector(coo.cols)
+        desc = f"uniform_k({size}, 32)"
+    return coo, x, desc + f" n={coo.rows} nnz={coo.nnz}"
+
+
+def oracle_pipeline(coo, x, iters, all_cores, power_reps=None):
+    """The oracle as it stands: canonicalize (O1) -> CSR (O2) -> features (O3)
+    -> ELL build (O4) -> E power steps (O11). With power_reps, only that many
+    power steps are run and the E-step time is their mean × E (stated)."""
+    import oracle
+    t = {}
     t0 = time.perf_counter()
     st, R, C, V = oracle.canonicalize(coo.rows, coo.cols, coo.row, coo.col, coo.val)
+    t["canonicalize"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
     rp = oracle.csr(coo.rows, R)
-    _, f = oracle.features(coo.rows, coo.cols, rp, C)
-    if kind in ("stencil27", "lap2d", "uniform"):
-        oracle.sell(coo.rows, rp, C, V, 64, 1)
-    z = x / np.linalg.norm(x)
-    for k in range(iters):
-        y, z, lam, s = oracle.power_step(coo.rows, rp, C, V, z)
-    t = time.perf_counter() - t0
-    desc = (f"oracle (1 thread, fp64, naive C) on {kind}({size}) n={coo.rows} nnz={coo.nnz}: canonicalize+CSR+"
-            f"features+SELL build+{iters} power steps")
-    return 2.0 * coo.nnz * iters, t, desc
+    t["csr"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.features(coo.rows, coo.cols, rp, C)
+    t["features"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.ell(coo.rows, rp, C, V)
+    t["ell_build"] = time.perf_counter() - t0
+    z = x[: coo.cols] / np.linalg.norm(x[: coo.cols])
+    zf = np.zeros(coo.cols)
+    n_run = iters if power_reps is None else min(iters, power_reps)
+    t0 = time.perf_counter()
+    zz = z.copy()
+    for k in range(n_run):
+        y, xn, lam, s = oracle.power_step(coo.rows, rp, C, V, zz, all_cores=all_cores)
+        zf[: coo.rows] = xn  # square sample slabs: the next iterate is the slab's rows
+        zz = zf if coo.rows < coo.cols else xn
+    tp = (time.perf_counter() - t0) / max(n_run, 1)
+    t["power_step"] = tp
+    total = t["canonicalize"] + t["csr"] + t["features"] + t["ell_build"] + iters * tp
+    return 2.0 * coo.nnz * iters, total, t, n_run, rp, C, V
+
+
+def cpu_leg(args):
+    """Subprocess entry: the oracle on a bounded slab of the workload, once
+    single-threaded and once on all host cores (per-row order unchanged, so y
+    is identical). Prints one JSON object."""
+    import oracle
+    coo, x, desc = oracle_sample(args.config, CPU_SAMPLE)
+    E = args.iters
+    res = {"sample": desc, "host": host_info(), "threads_all": oracle.omp_threads()}
+    fl, tot1, t1, n1, rp, C, V = oracle_pipeline(coo, x, E, all_cores=False, power_reps=3)
+    res["one_thread"] = {"gflops_path": round(fl / tot1 / 1e9, 4), "seconds": {k: round(v, 4) for k, v in t1.items()},
+                         "power_steps_run": n1}
+    # SpMV alone (the kernel metric), best of 3
+    xs = x[: coo.cols]
+    s1 = min(_timed(lambda: oracle.spmv_csr(coo.rows, rp, C, V, xs)) for _ in range(3))
+    sA = min(_timed(lambda: oracle.spmv_csr(coo.rows, rp, C, V, xs, all_cores=True)) for _ in range(3))
+    flA, totA, tA, nA, *_ = oracle_pipeline(coo, x, E, all_cores=True, power_reps=10)
+    res["all_cores"] = {"gflops_path": round(flA / totA / 1e9, 4),
+                        "seconds": {k: round(v, 4) for k, v in tA.items()}, "power_steps_run": nA}
+    res["spmv_gflops_1thread"] = round(2 * coo.nnz / s1 / 1e9, 4)
+    res["spmv_gflops_all_cores"] = round(2 * coo.nnz / sA / 1e9, 4)
+    res["spmv_gbps_all_cores"] = round((12 * coo.nnz + 8 * (coo.rows + 1) + 16 * coo.rows) / sA / 1e9, 3)
+    res["nnz"] = coo.nnz
+    print(json.dumps(res), flush=True)
+
+
+def _timed(fn):
+    t0 = time.perf_counter()
+    fn()
+    return time.perf_counter() - t0
+
+
+def run_cpu_baseline(args):
+    """cpu_baseline for the GPU line: run cpu_leg in a subprocess (the GPU
+    process never loads the oracle library)."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-leg", "--config", args.config, "--iters",
+           str(args.iters)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as ex:  # report, never fall back
+        return {"value": None, "unit": "GFLOP/s", "kind": "oracle", "error": repr(ex)[:200]}
+    a = d["all_cores"]
+    return {"value": a["gflops_path"], "unit": "GFLOP/s", "cores": d["threads_all"], "kind": "oracle",
+            "sample": (f"{d['sample']}: canonicalize+CSR+features+ELL build+{args.iters} power steps on all "
+                       f"{d['threads_all']} host threads (OpenMP over rows; power-step time = mean of "
+                       f"{a['power_steps_run']} measured steps x {args.iters})"),
+            "one_thread": {"value": d["one_thread"]["gflops_path"], "cores": 1,
+                           "seconds": d["one_thread"]["seconds"]},
+            "all_cores_seconds": a["seconds"],
+            "spmv_gflops_1thread": d["spmv_gflops_1thread"], "spmv_gflops_all_cores": d["spmv_gflops_all_cores"],
+            "spmv_gbps_all_cores": d["spmv_gbps_all_cores"], "host": d["host"]}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    iters = args.iters
-    times = []
-    flops = 0.0
-    desc = ""
+    import oracle
+    coo, x, desc = oracle_sample(args.config, REF_SAMPLE)
+    times, flops = [], 0.0
     for i in range(args.warmup + args.steps):
-        fl, t, desc = oracle_pipeline(args.config, iters)
+        t0 = time.perf_counter()
+        fl, _, _, _, *_ = oracle_pipeline(coo, x, args.iters, all_cores=True)
+        t = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(t)
             flops = fl
     tot = sum(times)
     val = flops * len(times) / tot / 1e9
+    thr = oracle.omp_threads()
+    sample = (f"oracle (fp64 naive C, SpMV over rows on {thr} OpenMP threads) on {desc}: canonicalize+CSR+features+"
+              f"ELL build+{args.iters} power steps per step")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1000 * tot / len(times), 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "power_iterations_per_step": iters, "sample": CPU_SAMPLE[args.config]},
-        "cpu_baseline": {"value": round(val, 4), "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": desc},
+        "config": {"workload": args.config, "power_iterations_per_step": args.iters, "sample": desc},
+        "cpu_baseline": {"value": round(val, 4), "unit": "GFLOP/s", "cores": thr, "kind": "oracle", "sample": sample,
+                         "host": host_info()},
         "e2e": {"value": round(val, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
-# ----------------------------------------------------------------------------- GPU arm
+# ----------------------------------------------------------------------------- rank context
 
-def setup_dist(args):
-    import torch
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
+class Ctx:
+    """One rank's view of the job: real (one process per GPU, NCCL) or virtual
+    (W threads on one GPU, in-process communicator group)."""
+
+    def __init__(self, rank, world, local, comm=None, virtual=None):
+        self.rank, self.world, self.local = rank, world, local
+        self.comm = comm          # native communicator pointer (None at world 1)
+        self.virtual = virtual    # shared VirtualGroup or None
+
+    def barrier(self):
+        import torch
+        torch.cuda.current_stream().synchronize()
+        if self.virtual is not None:
+            self.virtual.barrier.wait()
+        elif self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def reduce(self, v, op):
+        """max / sum of a host float over ranks."""
+        if self.world == 1:
+            return v
+        if self.virtual is not None:
+            return self.virtual.reduce(self.rank, v, op)
+        import torch
         import torch.distributed as dist
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    return world, rank, local
+        t = torch.tensor([float(v)], dtype=torch.float64, device=f"cuda:{self.local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return t.item()
 
+
+class VirtualGroup:
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [0.0] * world
+
+    def reduce(self, rank, v, op):
+        self.barrier.wait()
+        self.slots[rank] = float(v)
+        self.barrier.wait()
+        out = max(self.slots) if op == "max" else sum(self.slots)
+        self.barrier.wait()
+        return out
+
+
+# ----------------------------------------------------------------------------- GPU arm helpers
 
 def gen_slab(cfg, bounds, rank, layout):
     """Row slab [b_r, b_{r+1}) of the config on this device, columns remapped
@@ -243,6 +439,7 @@ def gen_slab(cfg, bounds, rank, layout):
             hi = int(torch.searchsorted(rr, torch.tensor([b], device=rr.device)).item())
             coo = si.COO(b - a, n, (full.row[lo:hi] - a).contiguous(), full.col[lo:hi].contiguous(),
                          full.val[lo:hi].contiguous())
+            del full, rr
     if layout.world > 1:
         P.spmv_dist_remap_columns(coo.col, layout.bounds)
     coo.cols = layout.padded_n if layout.world > 1 else n
@@ -281,31 +478,173 @@ def summarize_decisions(log):
     return out
 
 
-def stored_bytes_power(info_bytes, rows, cols, vb):
-    # format arrays (padding included) + x read once + y written
-    return info_bytes + cols * vb + rows * vb
+def fmt_label(P, fmt, params):
+    """Exact kernel label (the key of profiles/ncu_traffic_<cfg>.json)."""
+    name = P.FORMAT_NAMES[fmt]
+    if fmt == P.FMT_CSR:
+        name += {P.CSR_MERGE: "-merge", P.CSR_STREAM: "-stream", P.CSR_SCALAR: "-scalar"}.get(
+            params.get("csr_alg", 0), "-vector")
+    if fmt in (P.FMT_ELL, P.FMT_SELL) and params.get("index16", 0) == 1:
+        name += "-16"
+    if fmt == P.FMT_BELL:
+        name += f"-{params.get('bell_b', 2)}"
+    return name
 
 
-def run_ours(args):
+def normalise_params(P, fmt, params):
+    if fmt == P.FMT_SELL:
+        return dict(sell_C=params.get("sell_C", 0), sell_sigma=params.get("sell_sigma", 0),
+                    index16=params.get("index16", -1))
+    if fmt == P.FMT_ELL:
+        return dict(index16=params.get("index16", -1))
+    if fmt == P.FMT_BELL:
+        return dict(bell_b=params.get("bell_b", 0))
+    if fmt == P.FMT_HYB:
+        return dict(hyb_K=params.get("hyb_K", -1))
+    if fmt == P.FMT_CSR:
+        return dict(csr_alg=params.get("csr_alg", 0), csr_T=params.get("csr_T", 0))
+    return {}
+
+
+def report_params(P, rep):
+    return dict(csr_alg=rep.params.csr_alg, csr_T=rep.params.csr_T, sell_C=rep.params.sell_C,
+                sell_sigma=rep.params.sell_sigma, hyb_K=rep.params.hyb_K, bell_b=rep.params.bell_b,
+                index16=rep.params.index16)
+
+
+def ncu_traffic(cfg, label):
+    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg}.json")
+    if not os.path.exists(prof):
+        return None, None
+    try:
+        pj = json.load(open(prof))
+        rec = pj.get(label)
+        if isinstance(rec, dict):
+            return rec.get("dram_bytes_per_launch"), rec
+    except Exception:
+        pass
+    return None, None
+
+
+def time_plain(P, h, fmt, x, y, min_ms=200.0):
+    """Median of 5 batches of back-to-back plain SpMVs (alpha=1, beta=0) with
+    CUDA events on the current stream; each batch >= min_ms/5."""
+    import torch
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        P.spmv_run(h, 1.0, x, 0.0, y, fmt=fmt)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    P.spmv_run(h, 1.0, x, 0.0, y, fmt=fmt)
+    e1.record(s)
+    torch.cuda.synchronize()
+    one = max(e0.elapsed_time(e1), 1e-3)
+    reps = max(5, min(2000, int(min_ms / 5 / one)))
+    ts = []
+    for _ in range(5):
+        e0.record(s)
+        for _ in range(reps):
+            P.spmv_run(h, 1.0, x, 0.0, y, fmt=fmt)
+        e1.record(s)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / reps)
+    return statistics.median(ts) * 1e-3, reps
+
+
+def per_config_leg(args, P, si, peak):
+    """c2/c3/c4 at N = 1: measured run-time + compile-time modes (spmv_tune
+    FORMAT|LAUNCH), the chosen kernel timed as a plain SpMV; c3/c4 also
+    against the measured x-gather ceiling of their own column stream."""
+    import torch
+    out = {}
+    gc = None
+    for cfg in [c for c in args.per_config.split(",") if c and c != "none"]:
+        t_cfg = time.perf_counter()
+        try:
+            coo = si.config_device(cfg)
+            dt = coo.val.dtype
+            vb = coo.val.element_size()
+            x = si.vector_device(coo.cols, dtype=dt)
+            y = torch.empty(coo.rows, dtype=dt, device="cuda")
+            h = P.spmv_create(coo.rows, coo.cols, coo.row, coo.col, coo.val)
+            rec = {"nnz": int(coo.nnz), "n": int(coo.rows), "dtype": "f32" if vb == 4 else "f64"}
+            if cfg in ("c3", "c4"):
+                try:
+                    sys.path.insert(0, os.path.join(ROOT, "tools"))
+                    import gather_ceiling as gcm
+                    gc = gcm.measure(coo.col, coo.nnz, x, coo.cols, vb, reps=10)
+                except Exception as ex:
+                    gc = {"error": repr(ex)[:160]}
+            del coo
+            torch.cuda.empty_cache()
+            P.spmv_features(h)
+            rep = P.spmv_tune(h, P.TUNE_FORMAT | P.TUNE_LAUNCH, expected_iterations=args.iters)
+            fmt = rep.format
+            params = report_params(P, rep)
+            info = P.spmv_format_info(h, fmt)
+            label = fmt_label(P, fmt, dict(params, index16=1 if info.get("index_bytes") == 2 else 0))
+            t, reps = time_plain(P, h, fmt, x, y)
+            alg = info["stored_bytes"] + x.numel() * vb + y.numel() * vb
+            rec.update({"format": label, "launch": list(P.spmv_get_launch(h, fmt)), "kernel_us": round(t * 1e6, 2),
+                        "alg_bytes": int(alg), "GBps": round(alg / t / 1e9, 1),
+                        "frac_measured_peak": round(alg / t / 1e9 / peak, 4), "frac_8TBs": round(alg / t / 8e12, 4),
+                        "GFLOPs": round(2 * rec["nnz"] / t / 1e9, 1), "reps": reps,
+                        "candidates": summarize_decisions(P.spmv_decision_log(h)).get("candidates")})
+            tr, _ = ncu_traffic(cfg, label)
+            rec["traffic"] = tr
+            if gc is not None and cfg in ("c3", "c4"):
+                rec["gather_ceiling"] = gc
+                if gc.get("ceiling_us"):
+                    rec["frac_gather_ceiling"] = round(gc["ceiling_us"] / (t * 1e6), 4)
+                gc = None
+            P.spmv_destroy(h)
+            del x, y
+        except Exception as ex:  # report, never fall back
+            rec = {"error": repr(ex)[:200]}
+        rec["leg_seconds"] = round(time.perf_counter() - t_cfg, 1)
+        out[cfg] = rec
+        P.lib().spmv_trim_pool(0)
+        torch.cuda.empty_cache()
+    return out
+
+
+# ----------------------------------------------------------------------------- one rank
+
+def run_rank(args, ctx: Ctx, shared: dict):
     import torch
     import paper_2302_05662_b200 as P
-    from paper_2302_05662_b200.dist import Layout, NativeComm, PowerIteration, native_power_iteration
+    from paper_2302_05662_b200.dist import Layout, PowerIteration, native_power_iteration
     import spmv_inputs as si
 
-    world, rank, local = setup_dist(args)
+    rank, world, local = ctx.rank, ctx.world, ctx.local
+    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    my_stream = torch.cuda.Stream(device=dev) if ctx.virtual is not None else torch.cuda.current_stream()
+    sctx = torch.cuda.stream(my_stream)
+    sctx.__enter__()
+    stream = torch.cuda.current_stream()
     cfgd = si.CONFIGS[args.config]
     dtype = "f32" if cfgd["dtype"] == "f32" else "f64"
     tdt = torch.float32 if dtype == "f32" else torch.float64
     vb = 4 if dtype == "f32" else 8
     E = args.iters
 
-    lengths = row_lengths(args.config)
+    if ctx.virtual is not None:  # one partition for all virtual ranks (computed by rank 0)
+        if rank == 0:
+            shared["lengths"] = row_lengths(args.config)
+        ctx.virtual.barrier.wait()
+        lengths = shared["lengths"]
+    else:
+        lengths = row_lengths(args.config)
     bounds = P.spmv_dist_partition_lengths(lengths, world)
     layout = Layout.from_bounds(bounds)
+    if ctx.virtual is not None:
+        ctx.virtual.barrier.wait()
+        if rank == 0:
+            shared.pop("lengths", None)
+    del lengths
     coo, n_global = gen_slab(args.config, bounds, rank, layout)
     nnz_local = coo.nnz
-    del lengths
     torch.cuda.empty_cache()
 
     # x0 (global, padded layout), generated on device
@@ -319,17 +658,15 @@ def run_ours(args):
         x0.copy_(x0g)
     del x0g
 
-    # ---- a6/a7 decision, measured once before timing (replayed every step)
+    # ---- offline: compile-time mode (launch sweep) + measured run-time mode
+    t_off = time.perf_counter()
     h = P.spmv_create(coo.rows, coo.cols, coo.row, coo.col, coo.val)
     P.spmv_features(h)
     if args.format == "auto":
         flags = P.TUNE_FORMAT | (0 if args.no_tune_launch else P.TUNE_LAUNCH)
         rep = P.spmv_tune(h, flags, expected_iterations=E)
         fmt = rep.format
-        params = dict(csr_alg=rep.params.csr_alg, csr_T=rep.params.csr_T, sell_C=rep.params.sell_C,
-                      sell_sigma=rep.params.sell_sigma, hyb_K=rep.params.hyb_K, bell_b=rep.params.bell_b,
-                      index16=rep.params.index16)
-        launch = P.spmv_get_launch(h, fmt)
+        params = report_params(P, rep)
         decision = P.spmv_decision_log(h)
     else:
         csr_algs = {"CSR-vector": P.CSR_VECTOR, "CSR-merge": P.CSR_MERGE, "CSR-stream": P.CSR_STREAM}
@@ -342,30 +679,14 @@ def run_ours(args):
             P.spmv_set_launch(h, fmt, *[int(v) for v in args.launch.split(",")])
         elif not args.no_tune_launch:
             P.spmv_tune(h, P.TUNE_LAUNCH, expected_iterations=E)
-        launch = P.spmv_get_launch(h, fmt)
         decision = P.spmv_decision_log(h)
+    params = normalise_params(P, fmt, params)
+    launch = tuple(P.spmv_get_launch(h, fmt))
     P.spmv_destroy(h)
-    if fmt != P.FMT_CSR:
-        params = {k: v for k, v in params.items() if k != "csr_alg" or fmt == P.FMT_CSR}
-    if fmt == P.FMT_SELL:
-        params = dict(sell_C=params.get("sell_C", 0), sell_sigma=params.get("sell_sigma", 0),
-                      index16=params.get("index16", 0))
-    elif fmt == P.FMT_ELL:
-        params = dict(index16=params.get("index16", 0))
-    elif fmt == P.FMT_BELL:
-        params = dict(bell_b=params.get("bell_b", 0))
-    elif fmt == P.FMT_HYB:
-        params = dict(hyb_K=params.get("hyb_K", -1))
-    elif fmt == P.FMT_CSR:
-        params = dict(csr_alg=params.get("csr_alg", 0), csr_T=params.get("csr_T", 0))
-    else:
-        params = {}
-    fmt_label = P.FORMAT_NAMES[fmt] + ({P.CSR_MERGE: "-merge", P.CSR_STREAM: "-stream", P.CSR_VECTOR: "-vector"}
-                                       .get(params.get("csr_alg", 0), "") if fmt == P.FMT_CSR else "")
+    offline_s = time.perf_counter() - t_off
+    offline = {"format": fmt, "params": params, "launch": launch}
 
-    stream = torch.cuda.current_stream()
-    state = {"kms": []}
-    comm = NativeComm(rank, world, local) if world > 1 else None
+    comm = ctx.comm
     bufs = {
         "cur": torch.zeros(layout.padded_n if world > 1 else n_global, dtype=tdt, device=dev),
         "nxt": torch.zeros(layout.padded_n if world > 1 else n_global, dtype=tdt, device=dev),
@@ -375,141 +696,132 @@ def run_ours(args):
     plan_flags = 0
     for f in (args.plan or "").split(","):
         plan_flags |= {"overlap": P.PLAN_OVERLAP, "halo": P.PLAN_HALO}.get(f.strip(), 0)
+    state = {"kms": [], "time_kernels": False, "phase_events": None, "selected": None}
 
-    def power(h, x_start, bufs=bufs):
+    class _C:  # native_power_iteration expects an object with .comm
+        def __init__(self, c):
+            self.comm = c
+
+    def power(h, x_start, bufs=bufs, fmt_run=None):
         # N = 1: one event pair around the E back-to-back SpMV launches (no
         # events between kernels); N > 1: the distributed plan (interior/halo
         # split, overlap, halo exchange) with events around each interior kernel.
-        timing = state.get("time_kernels", False)
+        timing = state["time_kernels"]
         if world > 1:
-            plan = P.spmv_dist_plan_create(h, comm.comm, layout.chunk, plan_flags)
+            plan = P.spmv_dist_plan_create(h, comm, layout.chunk, plan_flags)
             if state.get("want_plan_info"):
                 state["plan_info"] = P.spmv_dist_plan_info(plan)
                 part0 = P.spmv_dist_plan_part(plan, 0)
-                state["part0_info"] = P.spmv_format_info(part0, fmt) if part0 is not None else None
+                state["part0_info"] = P.spmv_format_info(part0, fmt_run) if part0 is not None else None
             fb, _, ims = P.spmv_dist_plan_iterate(plan, x_start, bufs["cur"], bufs["nxt"], E, bufs["sums"],
                                                   time_interior=timing)
             P.spmv_dist_plan_destroy(plan)
             if ims:
                 state["kms"].extend(ims)
             return (bufs["cur"] if fb == 0 else bufs["nxt"]), bufs["sums"]
-        res = native_power_iteration(h, layout, rank, x_start, bufs, E, comm,
-                                     time_kernels=timing and world > 1, time_loop=timing and world == 1)
-        z, sums, kms = res[:3]
+        res = native_power_iteration(h, layout, rank, x_start, bufs, E, None,
+                                     time_kernels=False, time_loop=timing)
+        z, sums = res[0], res[1]
         lms = res[3] if len(res) > 3 else None
-        if kms:
-            state["kms"].extend(kms)
         if lms is not None and timing:
             state["kms"].extend([lms / E] * E)
         return z, sums
 
-    phases = {} if os.environ.get("BENCH_PHASES") else None
+    ev_names = ["create", "features", "select", "convert", "power", "destroy"]
 
-    def mark(name):
-        if phases is not None:
-            torch.cuda.synchronize()
-            phases.setdefault(name, []).append(time.perf_counter())
-
-    ev_names = ["create", "features", "convert", "power", "destroy"]
-
-    def ev_mark(i):
+    def ev_mark():
         # CUDA events at phase boundaries on the stream (no synchronisation)
-        if state.get("phase_events") is not None:
+        if state["phase_events"] is not None:
             e = torch.cuda.Event(enable_timing=True)
             e.record(stream)
             state["phase_events"][-1].append(e)
 
-    def one_step(coo_in, want_info=False):
-        if state.get("phase_events") is not None:
-            state["phase_events"].append([])
-        mark("0_start")
-        ev_mark(0)
-        h = P.spmv_create(coo_in.rows, coo_in.cols, coo_in.row, coo_in.col, coo_in.val)
-        state["h"] = h
-        mark("1_create")
-        ev_mark(1)
-        P.spmv_features(h)
-        mark("2_features")
-        ev_mark(2)
-        P.spmv_convert(h, fmt, **params)
-        P.spmv_set_launch(h, fmt, *launch)
-        info = P.spmv_format_info(h, fmt) if want_info else None  # (reads sizes back: not in the timed loop)
-        state["want_plan_info"] = want_info
-        mark("3_convert")
-        ev_mark(3)
-        power(h, x0)
-        mark("4_power")
-        ev_mark(4)
-        P.spmv_destroy(h)
-        state["h"] = None
-        mark("5_destroy")
-        ev_mark(5)
-        return info
+    def select(h):
+        """a7 run-time mode for this matrix: (format, params, launch)."""
+        if args.select == "replay" or args.format != "auto":
+            return offline["format"], offline["params"], offline["launch"]
+        r = P.spmv_tune(h, P.TUNE_FORMAT | P.TUNE_PREDICT | P.TUNE_DECIDE_ONLY, expected_iterations=E)
+        f = r.format if r.converted else P.FMT_CSR
+        if f == offline["format"]:
+            return f, offline["params"], offline["launch"]
+        p = normalise_params(P, f, report_params(P, r) if r.converted else {"csr_alg": P.CSR_VECTOR})
+        return f, p, (0, 0, -1, 0)
 
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-        torch.cuda.synchronize()
+    def one_step(coo_in, want_info=False):
+        if state["phase_events"] is not None:
+            state["phase_events"].append([])
+        ev_mark()
+        h = P.spmv_create(coo_in.rows, coo_in.cols, coo_in.row, coo_in.col, coo_in.val)
+        ev_mark()
+        P.spmv_features(h)
+        ev_mark()
+        f, p, lch = select(h)
+        ev_mark()
+        P.spmv_convert(h, f, **p)
+        P.spmv_set_launch(h, f, *lch)
+        state["selected"] = (f, p, lch)
+        info = P.spmv_format_info(h, f) if want_info else None  # (reads sizes back: not in the timed loop)
+        state["want_plan_info"] = want_info
+        ev_mark()
+        power(h, x0, fmt_run=f)
+        ev_mark()
+        P.spmv_destroy(h)
+        ev_mark()
+        return info
 
     info = None
     for w in range(args.warmup):
         info = one_step(coo, want_info=(w == args.warmup - 1)) or info
     if info is None:
         info = one_step(coo, want_info=True)
-    barrier()
+    ctx.barrier()
 
-    clocks = ClockSampler(local) if not os.environ.get("BENCH_NO_CLOCKS") else None
+    clocks = ClockSampler(local) if (rank == 0 or ctx.virtual is None) and not os.environ.get("BENCH_NO_CLOCKS") \
+        else None
     energy = Energy(local)
     state["time_kernels"] = not os.environ.get("BENCH_NO_KEVENTS")
     state["kms"] = []
     state["phase_events"] = []
     l0 = P.launch_count()
+    energy.start_sampler()
     e_j0 = energy.read_j()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
-    barrier()
-    state["host_t0"] = time.perf_counter()
+    ctx.barrier()
+    host_t0 = time.perf_counter()
     t_start.record(stream)
     for _ in range(args.steps):
         one_step(coo)
     t_end.record(stream)
-    barrier()
-    e_j1 = energy.read_j()
+    ctx.barrier()
     launches = P.launch_count() - l0
     clk = clocks.stop() if clocks else None
     state["time_kernels"] = False
     ms = t_start.elapsed_time(t_end)
-    host_s = time.perf_counter() - state.get("host_t0", time.perf_counter())
-    if phases is not None and rank == 0:
-        keys = sorted(phases)
-        n = min(len(phases[k]) for k in keys)
-        rep = {}
-        for a, b in zip(keys[:-1], keys[1:]):
-            d = [phases[b][i] - phases[a][i] for i in range(n)]
-            rep[b] = {"first_ms": round(d[0] * 1e3, 3), "last_ms": round(d[-1] * 1e3, 3),
-                      "median_ms": round(statistics.median(d) * 1e3, 3)}
-        print("PHASES", json.dumps(rep), file=sys.stderr, flush=True)
+    host_s = time.perf_counter() - host_t0
+    # energy over >= energy_window seconds (P:884): extend with untimed steps if needed
+    extra = 0
+    while time.perf_counter() - host_t0 < args.energy_window and extra < 1000:
+        one_step(coo)
+        extra += 1
+    ctx.barrier()
+    e_j1 = energy.read_j()
+    w_mean = energy.stop_sampler()
+    window_s = time.perf_counter() - host_t0
+    lam_main = PowerIteration.lambdas(bufs["sums"])  # every step restarts from x0: the same λ_1..λ_E
     kernel_ms = list(state["kms"])
     phase_ms = {}
-    pe = state.pop("phase_events", None) or []
+    pe = state["phase_events"] or []
     state["phase_events"] = None
     for i, name in enumerate(ev_names):
-        vals = [st[i].elapsed_time(st[i + 1]) for st in pe if len(st) > i + 1]
+        vals = [st[i].elapsed_time(st[i + 1]) for st in pe[: args.steps] if len(st) > i + 1]
         if vals:
             phase_ms[name] = round(statistics.median(vals), 4)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        import torch.distributed as dist
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-        nnz_t = torch.tensor([nnz_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(nnz_t)
-        nnz_total = nnz_t.item()
-    else:
-        nnz_total = nnz_local
-    ms_max = ms_t.item()
+    ms_max = ctx.reduce(ms, "max")
+    nnz_total = ctx.reduce(float(nnz_local), "sum")
     flops = 2.0 * nnz_total * E * args.steps
     value = flops / (ms_max * 1e-3) / 1e9
+    sel_f, sel_p, sel_l = state["selected"]
 
     # ---- roofline of the dominant kernel (the SpMV of the chosen format)
     rows_local = coo.rows
@@ -518,62 +830,43 @@ def run_ours(args):
         p0rows = state["plan_info"]["part_rows"][0]
         alg_bytes = state["part0_info"]["stored_bytes"] + rows_local * vb + p0rows * vb
     else:
-        alg_bytes = stored_bytes_power(info["stored_bytes"], rows_local, n_global, vb)
+        alg_bytes = info["stored_bytes"] + n_global * vb + rows_local * vb
     k_avg_ms = statistics.mean(kernel_ms) if kernel_ms else float("nan")
     achieved = alg_bytes / (k_avg_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
-    if os.path.exists(prof):
-        try:
-            pj = json.load(open(prof))
-            key = fmt_label if fmt == P.FMT_CSR else P.FORMAT_NAMES[fmt]
-            if pj.get("format") == key:  # legacy single-format layout
-                traffic = pj.get("dram_bytes_per_launch")
-            elif isinstance(pj.get(key), dict):
-                traffic = pj[key].get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    label = fmt_label(P, sel_f, dict(sel_p, index16=1 if info.get("index_bytes") == 2 else 0))
+    traffic, trec = ncu_traffic(args.config, label)
     kernel_share = sum(kernel_ms) / ms if ms > 0 else None
 
-    # ---- e2e: same metric through the C ABI with HOST buffers (rank 0 .. all ranks)
+    # ---- e2e: same metric through the C ABI with HOST buffers
     e2e = None
+    lam = None
     try:
         if args.no_e2e:
             raise RuntimeError("e2e skipped (--no-e2e)")
+        if ctx.virtual is not None:
+            raise RuntimeError("e2e not run with --virtual (ranks share one GPU and one host link)")
         host_row = coo.row.cpu().pin_memory()
         host_col = coo.col.cpu().pin_memory()
         host_val = coo.val.cpu().pin_memory()
         host_x0 = x0.cpu().pin_memory()
-        # N = 1: two steps in flight on two streams (one host thread each, the
-        # C calls release the GIL), so step k+1's host->device copy overlaps
-        # step k's kernels; every step still copies its own inputs in and its
-        # result out. N > 1: one step at a time (the ranks' collectives are
-        # issued in step order on one communicator).
         free_b, _ = torch.cuda.mem_get_info(dev)
         step_b = 3 * coo.nnz * (8 + vb)  # COO + format + scratch, per step in flight (upper estimate)
         depth = 2 if world == 1 and not args.e2e_serial and 2 * step_b < 0.8 * free_b else 1
-        lanes = []
-        for i in range(depth):
-            lanes.append({
-                "stream": torch.cuda.Stream(device=dev),
-                "bufs": bufs if i == 0 else {k: torch.zeros_like(v) for k, v in bufs.items()},
-                "y_host": torch.empty(layout.padded_n if world > 1 else n_global, dtype=tdt).pin_memory(),
-                "s_host": torch.empty(E + 1, 2, dtype=torch.float64).pin_memory()})
-        y_host, s_host = lanes[0]["y_host"], lanes[0]["s_host"]
 
-        import threading
+        def make_lane(i):
+            return {"stream": torch.cuda.Stream(device=dev),
+                    "bufs": bufs if i == 0 else {k: torch.zeros_like(v) for k, v in bufs.items()},
+                    "y_host": torch.empty(layout.padded_n if world > 1 else n_global, dtype=tdt).pin_memory(),
+                    "s_host": torch.empty(E + 1, 2, dtype=torch.float64).pin_memory()}
+        lanes = [make_lane(i) for i in range(depth)]
         ingest_lock = threading.Lock()
 
         def e2e_step(lane):
             torch.cuda.set_device(dev)
             st = lane["stream"]
             with torch.cuda.stream(st):
-                # one ingest at a time: the host link is the shared resource, so
-                # the lanes settle into copy(k+1) || kernels(k) instead of both
-                # copying, then both computing, in lockstep; one FIFO per
-                # copy engine (the x upload is queued with the matrix, not behind
-                # the other lane's next matrix upload)
+                # one ingest at a time: the host link is the shared resource
                 xdev = torch.empty_like(x0)
                 with ingest_lock:
                     h = P.spmv_create(coo.rows, coo.cols, host_row.numpy(), host_col.numpy(), host_val.numpy(),
@@ -581,78 +874,88 @@ def run_ours(args):
                     xdev.copy_(host_x0, non_blocking=True)
                 try:
                     P.spmv_features(h)
-                    P.spmv_convert(h, fmt, **params)
-                    P.spmv_set_launch(h, fmt, *launch)
-                    z, sums = power(h, xdev, lane["bufs"])
+                    f, p, lch = select(h)
+                    P.spmv_convert(h, f, **p)
+                    P.spmv_set_launch(h, f, *lch)
+                    z, sums = power(h, xdev, lane["bufs"], fmt_run=f)
                     lane["y_host"].copy_(z, non_blocking=True)
                     lane["s_host"].copy_(sums, non_blocking=True)
                     st.synchronize()
                 finally:
                     P.spmv_destroy(h)
 
-        def run_lane(i, count):
-            for _ in range(count):
-                e2e_step(lanes[i])
-
         from concurrent.futures import ThreadPoolExecutor
-        pool = ThreadPoolExecutor(max_workers=depth)  # the same host threads warm up and run
 
-        def run_all(total):
-            counts = [total // depth + (1 if i < total % depth else 0) for i in range(depth)]
-            for f in [pool.submit(run_lane, i, counts[i]) for i in range(depth)]:
+        def run_all(pool, nl, total):
+            counts = [total // nl + (1 if i < total % nl else 0) for i in range(nl)]
+            for f in [pool.submit(lambda i=i: [e2e_step(lanes[i]) for _ in range(counts[i])]) for i in range(nl)]:
                 f.result()
 
-        run_all(max(2 * depth, args.warmup))
-        torch.cuda.synchronize()
-        barrier()
-        t0 = time.perf_counter()
-        run_all(args.steps)
-        torch.cuda.synchronize()
-        barrier()
-        t_e2e = time.perf_counter() - t0
-        pool.shutdown()
-        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-        if world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(flops / tt.item() / 1e9, 3), "unit": "GFLOP/s",
+        def timed_e2e(nl, steps):
+            pool = ThreadPoolExecutor(max_workers=nl)  # the same host threads warm up and run
+            run_all(pool, nl, max(2 * nl, args.warmup))
+            torch.cuda.synchronize()
+            ctx.barrier()
+            t0 = time.perf_counter()
+            run_all(pool, nl, steps)
+            torch.cuda.synchronize()
+            ctx.barrier()
+            t = time.perf_counter() - t0
+            pool.shutdown()
+            return ctx.reduce(t, "max")
+
+        t_e2e = timed_e2e(depth, args.steps)
+        e2e = {"value": round(flops / t_e2e / 1e9, 3), "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(coo.nnz * (8 + vb) + x0.numel() * vb),
-               "d2h_bytes_per_step": int(y_host.numel() * vb + s_host.numel() * 8),
+               "d2h_bytes_per_step": int(lanes[0]["y_host"].numel() * vb + lanes[0]["s_host"].numel() * 8),
                "steps_in_flight": depth}
-        lam = PowerIteration.lambdas(s_host)
+        if depth > 1:  # the serial figure too (one step at a time), comparable across configs/rounds
+            t_ser = timed_e2e(1, max(2, args.steps // 2))
+            e2e["serial_value"] = round(2.0 * nnz_total * E * max(2, args.steps // 2) / t_ser / 1e9, 3)
+        else:
+            e2e["serial_value"] = e2e["value"]
+        lam = PowerIteration.lambdas(lanes[0]["s_host"])
     except Exception as ex:  # report, never fall back
         e2e = {"value": None, "unit": "GFLOP/s", "error": repr(ex)[:200]}
-        lam = None
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        fl, t, desc = oracle_pipeline(args.config, E)
-        cpu = {"value": round(fl / t / 1e9, 4), "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": desc}
 
     mflops_w = None
+    energy_rec = None
     if e_j0 is not None and e_j1 is not None and e_j1 > e_j0:
-        joules = (e_j1 - e_j0)
-        mflops_w = flops / 1e6 / joules / (world if world > 1 else 1)
+        joules = ctx.reduce(e_j1 - e_j0, "sum") if ctx.virtual is None else (e_j1 - e_j0)
+        flops_win = 2.0 * nnz_total * E * (args.steps + extra)
+        mflops_w = flops_win / 1e6 / joules
+        energy_rec = {"window_s": round(window_s, 3), "joules": round(joules, 2),
+                      "avg_w_counter": round(joules / window_s / (world if ctx.virtual is None else 1), 1),
+                      "avg_w_samples": round(w_mean, 1) if w_mean else None,
+                      "untimed_extra_steps": extra, "source": "NVML total-energy counter delta; 10 ms power samples"}
 
     if rank == 0:
+        plan = None
+        if world > 1 and state.get("plan_info"):
+            plan = {"flags": args.plan, **{k: state["plan_info"][k] for k in
+                                           ("h0", "h1", "part_rows", "halo", "recv_bytes_per_step")}}
         out = {
-            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s",
+            "n_gpus": 1 if ctx.virtual is not None else world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype,
-            "data": "synthetic",
+            "higher_is_better": True,
+            "scaling": "none (virtual ranks share one GPU)" if ctx.virtual is not None else "strong",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": {"workload": args.config, "desc": cfgd["desc"], "n": n_global, "nnz": int(nnz_total),
-                       "power_iterations_per_step": E, "format": fmt_label, "format_params": params,
-                       "launch": {"block": launch[0], "maxreg": launch[1], "carveout_pct": launch[2],
-                                  "knob": launch[3]},
+                       "power_iterations_per_step": E, "format": label, "format_params": sel_p,
+                       "launch": {"block": sel_l[0], "maxreg": sel_l[1], "carveout_pct": sel_l[2],
+                                  "knob": sel_l[3]},
+                       "select": args.select if args.format == "auto" else "fixed --format",
+                       "offline_choice": fmt_label(P, offline["format"], offline["params"]),
+                       "offline_tune_s": round(offline_s, 1),
                        "partition": "row, nnz-balanced" if world > 1 else "none",
-                       "plan": ({"flags": args.plan, **{k: state["plan_info"][k] for k in
-                                 ("h0", "h1", "part_rows", "halo", "recv_bytes_per_step")}}
-                                if world > 1 and state.get("plan_info") else None),
+                       "virtual_ranks": world if ctx.virtual is not None else None,
+                       "plan": plan,
                        "l2": "inputs larger than L2 (matrix arrays > 126 MB; x stays L2-resident by design)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": f"{fmt_label} SpMV (power-step epilogue)" + (
-                             "" if world == 1 else ", interior rows"),
+                         "traffic_source": (f"profiles/ncu_traffic_{args.config}.json[{label}]" if traffic else None),
+                         "kernel": f"{label} SpMV (power-step epilogue)" + ("" if world == 1 else ", interior rows"),
                          "kernel_timing": ("CUDA events around the E back-to-back SpMV launches of each step / E "
                                            "(includes launch gaps)") if world == 1 else
                                           "CUDA events around each interior SpMV (overlapping the exchange)",
@@ -662,24 +965,90 @@ def run_ours(args):
             "hbm_gbs": round(achieved, 1),
             "step_phases_ms": phase_ms,
             "mflops_per_w": round(mflops_w, 1) if mflops_w else None,
-            "cpu_baseline": cpu,
+            "energy": energy_rec,
+            "cpu_baseline": None,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "host_ms_per_step": round(host_s * 1e3 / args.steps, 3),
             "clocks": clk,
             "lambda_last": float(lam[-1]) if lam is not None and len(lam) else None,
+            "lambdas": [float(v) for v in lam_main[:8]] + ([float(lam_main[-1])] if len(lam_main) > 8 else []),
             "tuner": summarize_decisions(decision),
         }
-        print(json.dumps(out), flush=True)
-    if comm is not None:
-        comm.close()
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+        if trec:
+            out["roofline"]["x_reread_factor"] = trec.get("x_reread_factor")
+        shared["out"] = out
+    # release the big buffers before the per-config leg
+    del coo, bufs, x0
+    torch.cuda.empty_cache()
+    sctx.__exit__(None, None, None)
+
+
+def run_ours(args):
+    import torch
+    import paper_2302_05662_b200 as P
+    import spmv_inputs as si
+    shared = {}
+    if args.virtual:
+        W = args.gpus
+        torch.cuda.set_device(0)
+        comms = P.spmv_dist_local_group(W, [0] * W) if W > 1 else [None]
+        grp = VirtualGroup(W)
+        errs = []
+
+        def body(r):
+            try:
+                run_rank(args, Ctx(r, W, 0, comm=comms[r], virtual=grp), shared)
+            except BaseException as ex:  # noqa: BLE001 — surfaced below
+                errs.append(ex)
+                grp.barrier.abort()
+                raise
+        ths = [threading.Thread(target=body, args=(r,)) for r in range(W)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        for c in comms:
+            if c is not None:
+                P.spmv_dist_destroy(c)
+        if errs:
+            raise errs[0]
+        world, rank = W, 0
+    else:
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        comm = None
+        if world > 1:
+            import torch.distributed as dist
+            from paper_2302_05662_b200.dist import NativeComm
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # the communicator's init log (nranks) stays visible
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            comm = NativeComm(rank, world, local)
+        run_rank(args, Ctx(rank, world, local, comm=comm.comm if comm else None), shared)
+        if comm is not None:
+            comm.close()
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if rank != 0:
+        return
+    out = shared["out"]
+    peak, _ = measured_peaks()
+    if world == 1 and not args.virtual:
+        if args.per_config and args.per_config != "none":
+            out["per_config"] = per_config_leg(args, P, si, peak)
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = run_cpu_baseline(args)
+    print(json.dumps(out), flush=True)
 
 
 def main():
     args = parse()
+    if args.cpu_leg:
+        cpu_leg(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return

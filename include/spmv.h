@@ -145,9 +145,18 @@ typedef struct {
  * candidate: features -> decision-tree class (best format) -> predicted speed
  * ratio vs CSR-vector and predicted conversion latency -> convert iff
  * expected_iterations·(t_csr − ratio·t_csr) > f_latency + c_latency_pred.
- * Only t_csr is measured. Latency objective only (SPMV_ERR_UNSUPPORTED with
- * another objective): the models are trained on latency. */
+ * Only t_csr is measured: the default CSR-vector kernel timed on a row
+ * prefix of about 2^25 entries (the whole matrix when nnz <= 2^26), scaled to
+ * nnz. Latency objective only (SPMV_ERR_UNSUPPORTED with another objective):
+ * the models are trained on latency. */
 #define SPMV_TUNE_PREDICT 4u
+/* With SPMV_TUNE_FORMAT | SPMV_TUNE_PREDICT only: decide, do not convert.
+ * The report carries the verdict (format, params, converted = 1 iff the gate
+ * accepts the conversion; format = SPMV_FMT_CSR otherwise) and the handle's
+ * active format is left unchanged, so the caller converts with spmv_convert
+ * (the bench times selection and conversion as separate phases).
+ * SPMV_ERR_INVALID_ARG without PREDICT or together with SPMV_TUNE_LAUNCH. */
+#define SPMV_TUNE_DECIDE_ONLY 8u
 
 typedef struct {
   int32_t format;                /* chosen spmv_format_t (active after the call) */

@@ -35,7 +35,7 @@ def build(force: bool = False) -> str:
         return LIB_PATH
     tmp = LIB_PATH + ".tmp"
     subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-std=c11", "-fno-fast-math",
-                           "-ffp-contract=off", SRC, "-o", tmp, "-lm"])
+                           "-ffp-contract=off", "-fopenmp", SRC, "-o", tmp, "-lm", "-lgomp"])
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
@@ -86,6 +86,9 @@ def lib():
         L.oracle_power_step.argtypes = [i64, vp, vp, vp, vp, vp, vp,
                                         ctypes.POINTER(d), ctypes.POINTER(d)]
         L.oracle_partition.argtypes = [i64, vp, i64, vp]
+        L.oracle_spmv_csr_omp.argtypes = L.oracle_spmv_csr.argtypes
+        L.oracle_power_step_omp.argtypes = L.oracle_power_step.argtypes
+        L.oracle_omp_threads.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -196,14 +199,21 @@ def bell(rows, row_ptr, col, val, bh=2, bw=2):
 
 # --------------------------------------------------------------------------- O8–O12
 
-def spmv_csr(rows, row_ptr, col, val, x, alpha=1.0, beta=0.0, y_in=None):
-    """O8: (y, abs_sum) in fp64; abs_sum_i = Σ|a_ik x_k|."""
+def spmv_csr(rows, row_ptr, col, val, x, alpha=1.0, beta=0.0, y_in=None, all_cores=False):
+    """O8: (y, abs_sum) in fp64; abs_sum_i = Σ|a_ik x_k|. `all_cores` runs the
+    same per-row loop under OpenMP (timing leg; bitwise the same y)."""
     rp, col, val, x = _c(row_ptr, np.int64), _c(col, np.int32), _c(val, np.float64), _c(x, np.float64)
     y = np.empty(rows, np.float64)
     a = np.empty(rows, np.float64)
     yin = _c(y_in, np.float64) if (y_in is not None and beta != 0.0) else None
-    lib().oracle_spmv_csr(rows, _p(rp), _p(col), _p(val), _p(x), alpha, beta, _p(yin), _p(y), _p(a))
+    fn = lib().oracle_spmv_csr_omp if all_cores else lib().oracle_spmv_csr
+    fn(rows, _p(rp), _p(col), _p(val), _p(x), alpha, beta, _p(yin), _p(y), _p(a))
     return y, a
+
+
+def omp_threads() -> int:
+    """Threads the all-core leg uses (OMP_NUM_THREADS or the host's cores)."""
+    return int(lib().oracle_omp_threads())
 
 
 def dense_spmv(rows, cols, r, c, v, x):
@@ -214,12 +224,12 @@ def dense_spmv(rows, cols, r, c, v, x):
     return y
 
 
-def power_step(rows, row_ptr, col, val, x):
+def power_step(rows, row_ptr, col, val, x, all_cores=False):
     """O11: (y, x_next, lambda, s)."""
     rp, col, val, x = _c(row_ptr, np.int64), _c(col, np.int32), _c(val, np.float64), _c(x, np.float64)
     y, xn = np.empty(rows, np.float64), np.empty(rows, np.float64)
     lam, s = ctypes.c_double(), ctypes.c_double()
-    lib().oracle_power_step(rows, _p(rp), _p(col), _p(val), _p(x), _p(y), _p(xn),
+    (lib().oracle_power_step_omp if all_cores else lib().oracle_power_step)(rows, _p(rp), _p(col), _p(val), _p(x), _p(y), _p(xn),
                             ctypes.byref(lam), ctypes.byref(s))
     return y, xn, lam.value, s.value
 

@@ -18,6 +18,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define EXPORT __attribute__((visibility("default")))
 
@@ -407,25 +410,49 @@ EXPORT void oracle_bell(int64_t rows, const int64_t* row_ptr, const int32_t* col
  * Laplacian on x = (grid row)² gives −2 on interior rows, Dirichlet
  * eigenvectors, Appendix D.
  * ------------------------------------------------------------------------- */
+static void spmv_row(int64_t i, const int64_t* row_ptr, const int32_t* col, const double* val,
+                     const double* x, double alpha, double beta, const double* y_in, double* y_out,
+                     double* abs_out) {
+  double sum = 0.0, comp = 0.0, a = 0.0;
+  if (alpha != 0.0) {
+    for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+      double t = val[k] * x[col[k]];
+      double s = sum + t;
+      if (fabs(sum) >= fabs(t)) comp += (sum - s) + t;
+      else comp += (t - s) + sum;
+      sum = s;
+      a += fabs(t);
+    }
+  }
+  double acc = sum + comp;
+  y_out[i] = (beta == 0.0) ? alpha * acc : alpha * acc + beta * y_in[i];
+  if (abs_out) abs_out[i] = a;
+}
+
 EXPORT void oracle_spmv_csr(int64_t rows, const int64_t* row_ptr, const int32_t* col,
                             const double* val, const double* x, double alpha, double beta,
                             const double* y_in, double* y_out, double* abs_out) {
-  for (int64_t i = 0; i < rows; ++i) {
-    double sum = 0.0, comp = 0.0, a = 0.0;
-    if (alpha != 0.0) {
-      for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
-        double t = val[k] * x[col[k]];
-        double s = sum + t;
-        if (fabs(sum) >= fabs(t)) comp += (sum - s) + t;
-        else comp += (t - s) + sum;
-        sum = s;
-        a += fabs(t);
-      }
-    }
-    double acc = sum + comp;
-    y_out[i] = (beta == 0.0) ? alpha * acc : alpha * acc + beta * y_in[i];
-    if (abs_out) abs_out[i] = a;
-  }
+  for (int64_t i = 0; i < rows; ++i) spmv_row(i, row_ptr, col, val, x, alpha, beta, y_in, y_out, abs_out);
+}
+
+/* The same O8 loop over all host cores (SURVEY §8(d) "CPU baseline": the CSR
+ * naive loop once single-threaded and once with an OpenMP parallel-for over
+ * rows, schedule(static)). Each row is still summed by one thread in column
+ * order, so y is bitwise identical to oracle_spmv_csr (pinned by
+ * test_omp_leg_bitwise). Timing only: the parity tests use the 1-thread loop. */
+EXPORT void oracle_spmv_csr_omp(int64_t rows, const int64_t* row_ptr, const int32_t* col,
+                                const double* val, const double* x, double alpha, double beta,
+                                const double* y_in, double* y_out, double* abs_out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < rows; ++i) spmv_row(i, row_ptr, col, val, x, alpha, beta, y_in, y_out, abs_out);
+}
+
+EXPORT int oracle_omp_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
 }
 
 /* ---------------------------------------------------------------------------
@@ -463,15 +490,29 @@ static double neumaier_dot(int64_t n, const double* a, const double* b) {
   return sum + comp;
 }
 
-EXPORT void oracle_power_step(int64_t rows, const int64_t* row_ptr, const int32_t* col,
-                              const double* val, const double* x, double* y, double* x_next,
-                              double* lambda, double* s_out) {
-  oracle_spmv_csr(rows, row_ptr, col, val, x, 1.0, 0.0, NULL, y, NULL);
+static void power_step(int omp, int64_t rows, const int64_t* row_ptr, const int32_t* col,
+                       const double* val, const double* x, double* y, double* x_next,
+                       double* lambda, double* s_out) {
+  if (omp) oracle_spmv_csr_omp(rows, row_ptr, col, val, x, 1.0, 0.0, NULL, y, NULL);
+  else oracle_spmv_csr(rows, row_ptr, col, val, x, 1.0, 0.0, NULL, y, NULL);
   double s = neumaier_dot(rows, y, y);
   *lambda = neumaier_dot(rows, x, y);
   *s_out = s;
   double r = sqrt(s);
   for (int64_t i = 0; i < rows; ++i) x_next[i] = y[i] / r;
+}
+
+EXPORT void oracle_power_step(int64_t rows, const int64_t* row_ptr, const int32_t* col,
+                              const double* val, const double* x, double* y, double* x_next,
+                              double* lambda, double* s_out) {
+  power_step(0, rows, row_ptr, col, val, x, y, x_next, lambda, s_out);
+}
+
+/* O11 with the all-core O8 loop (timing leg; the sums stay serial). */
+EXPORT void oracle_power_step_omp(int64_t rows, const int64_t* row_ptr, const int32_t* col,
+                                  const double* val, const double* x, double* y, double* x_next,
+                                  double* lambda, double* s_out) {
+  power_step(1, rows, row_ptr, col, val, x, y, x_next, lambda, s_out);
 }
 
 /* ---------------------------------------------------------------------------

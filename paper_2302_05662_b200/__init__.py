@@ -30,6 +30,7 @@ FORMAT_NAMES = {v: k for k, v in FORMATS.items()}
 CSR_AUTO, CSR_SCALAR, CSR_VECTOR, CSR_MERGE, CSR_STREAM = 0, 1, 2, 3, 4
 TUNE_LAUNCH, TUNE_FORMAT, TUNE_ALL = 1, 2, 3
 TUNE_PREDICT = 4  # with TUNE_FORMAT: learned selector + overhead estimators instead of measuring candidates
+TUNE_DECIDE_ONLY = 8  # with TUNE_FORMAT | TUNE_PREDICT: report the verdict, leave the handle unconverted
 SELECTOR_CLASSES = ["CSR-vector", "CSR-merge", "ELL", "SELL", "HYB", "COO", "BELL-2", "BELL-3", "CSR-stream"]
 OBJECTIVES = {"latency": 0, "energy": 1, "power": 2, "efficiency": 3}   # OR-ed into flags as value << 4
 (ARR_CSR_ROW_PTR, ARR_CSR_COL, ARR_CSR_VAL, ARR_COO_ROW, ARR_ELL_COL, ARR_ELL_VAL, ARR_SELL_PERM,

@@ -695,7 +695,49 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
 
 // Run-time mode with the learned models (SPMV_TUNE_PREDICT):
 // features -> predicted format -> estimated overhead -> gate.
-static void tune_predict(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tune_report_t* rep) {
+// t_CSR for the run-time mode: the default CSR-vector kernel timed on a row
+// prefix holding about kPredictSampleNnz entries (the whole matrix when it is
+// smaller), scaled to the full nnz. The kernel's time is linear in the
+// entries it streams, and a per-matrix selection must not cost a sizeable
+// share of the SpMVs it is choosing for (c5: 3.6e9 entries, 13 ms per CSR
+// SpMV, twelve timed launches otherwise).
+constexpr int64_t kPredictSampleNnz = 1LL << 25;
+static double predict_t_csr(spmv_matrix* h, TuneScratch& ts, int64_t* sample_nnz) {
+  const spmv_launch_t L = resolve_launch(h, SPMV_FMT_CSR, spmv_launch_t{0, 0, -1, 0});
+  if (h->nnz <= 2 * kPredictSampleNnz || h->rows < 2) {
+    *sample_nnz = h->nnz;
+    return time_variant(h, SPMV_FMT_CSR, L, ts.x, ts.y);
+  }
+  int64_t R = (int64_t)((double)h->rows * (double)kPredictSampleNnz / (double)h->nnz);
+  R = std::max<int64_t>(1, std::min(R, h->rows));
+  int64_t nnzR = 0;
+  if (h->rp64) {
+    d2h_sync(&nnzR, static_cast<const int64_t*>(h->row_ptr) + R, sizeof(int64_t), h->stream);
+  } else {
+    int32_t v = 0;
+    d2h_sync(&v, static_cast<const int32_t*>(h->row_ptr) + R, sizeof(int32_t), h->stream);
+    nnzR = v;
+  }
+  if (nnzR <= 0) {
+    *sample_nnz = h->nnz;
+    return time_variant(h, SPMV_FMT_CSR, L, ts.x, ts.y);
+  }
+  const int64_t rows0 = h->rows;
+  h->rows = R;  // CSR-vector reads rows [0, R) only
+  double t;
+  try {
+    t = time_variant(h, SPMV_FMT_CSR, L, ts.x, ts.y);
+  } catch (...) {
+    h->rows = rows0;
+    throw;
+  }
+  h->rows = rows0;
+  *sample_nnz = nnzR;
+  return t * (double)h->nnz / (double)nnzR;
+}
+
+static void tune_predict(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tune_report_t* rep,
+                         bool decide_only) {
   if (!h->have_features) compute_features(h);
   const spmv_features_t& f = h->feat;
   double x[kSelectorFeatures];
@@ -706,8 +748,14 @@ static void tune_predict(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tu
   selector_class_format(cls, &fmt, &q);
   const int orig_alg = h->csr_alg;
   h->csr_alg = SPMV_CSR_VECTOR;
-  const double t_csr =
-      time_variant(h, SPMV_FMT_CSR, resolve_launch(h, SPMV_FMT_CSR, spmv_launch_t{0, 0, -1, 0}), ts.x, ts.y);
+  int64_t sample_nnz = 0;
+  double t_csr;
+  try {
+    t_csr = predict_t_csr(h, ts, &sample_nnz);
+  } catch (...) {
+    h->csr_alg = orig_alg;
+    throw;
+  }
   h->csr_alg = orig_alg;
   const double ratio = selector_speed_ratio(cls, x);
   const double t_pred = t_csr * ratio;
@@ -720,9 +768,26 @@ static void tune_predict(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tu
   os << "{\"kind\":\"format_predict\",\"x\":[";
   for (int i = 0; i < kSelectorFeatures; ++i) os << x[i] << (i + 1 < kSelectorFeatures ? "," : "");
   os << "],\"class\":\"" << selector_class_name(cls) << "\",\"speed_ratio\":" << ratio << ",\"t_csr_s\":" << t_csr
-     << ",\"t_pred_s\":" << t_pred << ",\"gate\":{\"expected_iterations\":" << iters << ",\"gain_s\":" << gain
+     << ",\"t_csr_sample_nnz\":" << sample_nnz << ",\"t_pred_s\":" << t_pred << ",\"gate\":{\"expected_iterations\":" << iters << ",\"gain_s\":" << gain
      << ",\"f_latency_s\":" << h->f_latency << ",\"c_latency_pred_s\":" << c_pred << ",\"overhead\":" << overhead
      << ",\"convert\":" << (convert ? "true" : "false") << "}";
+  if (convert && decide_only) {
+    // SPMV_TUNE_DECIDE_ONLY: report the verdict, leave the handle as it is
+    os << ",\"decide_only\":true,\"chosen\":\"" << selector_class_name(cls) << "\"}";
+    log_append(h, os.str());
+    if (rep) {
+      rep->format = fmt;
+      rep->params = q;
+      rep->t_csr_s = t_csr;
+      rep->t_best_s = t_pred;
+      rep->f_latency_s = h->f_latency;
+      rep->c_latency_s = c_pred;
+      rep->expected_iterations = iters;
+      rep->converted = 1;
+      rep->n_candidates = 1;
+    }
+    return;
+  }
   if (convert) {
     try {
       switch (fmt) {
@@ -743,14 +808,14 @@ static void tune_predict(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tu
       os << ",\"build_failed\":\"" << e.msg << "\"";
     }
   }
-  if (!convert) {
+  if (!convert && !decide_only) {
     h->active = SPMV_FMT_CSR;
     h->csr_alg = SPMV_CSR_VECTOR;
   }
   os << ",\"chosen\":\"" << (convert ? selector_class_name(cls) : "CSR-vector") << "\"}";
   log_append(h, os.str());
   if (rep) {
-    rep->format = h->active;
+    rep->format = convert || !decide_only ? h->active : SPMV_FMT_CSR;
     rep->t_csr_s = t_csr;
     rep->t_best_s = convert ? t_pred : t_csr;
     rep->f_latency_s = h->f_latency;
@@ -831,6 +896,7 @@ extern "C" {
 spmv_status_t spmv_create(spmv_handle_t* out, int64_t rows, int64_t cols, int64_t nnz, const int32_t* row_idx,
                           const int32_t* col_idx, const void* vals, spmv_dtype_t dtype, spmv_mem_t where,
                           int device, void* cuda_stream) {
+  const NvtxRange nvtx_range("spmv_create");
   if (!out) return SPMV_ERR_INVALID_ARG;
   *out = nullptr;
   if (rows < 0 || cols < 0 || nnz < 0) return SPMV_ERR_INVALID_ARG;
@@ -863,6 +929,7 @@ spmv_status_t spmv_create(spmv_handle_t* out, int64_t rows, int64_t cols, int64_
 }
 
 spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format_params_t* p) {
+  const NvtxRange nvtx_range("spmv_convert");
   if (!h) return SPMV_ERR_INVALID_ARG;
   if (fmt < 0 || fmt >= SPMV_NUM_FORMATS) return SPMV_ERR_INVALID_ARG;
   API_TRY
@@ -945,6 +1012,7 @@ spmv_status_t spmv_get_format(spmv_handle_t h, spmv_format_t* fmt) {
 }
 
 spmv_status_t spmv_features(spmv_handle_t h, spmv_features_t* out) {
+  const NvtxRange nvtx_range("spmv_features");
   if (!h || !out) return SPMV_ERR_INVALID_ARG;
   API_TRY
   DeviceGuard g(h->device);
@@ -997,13 +1065,16 @@ spmv_status_t spmv_get_launch(spmv_handle_t h, spmv_format_t fmt, spmv_launch_t*
 }
 
 spmv_status_t spmv_tune(spmv_handle_t h, uint32_t flags, int64_t expected_iterations, spmv_tune_report_t* out) {
+  const NvtxRange nvtx_range("spmv_tune");
   const uint32_t what = flags & SPMV_TUNE_ALL;
   const int obj = (int)((flags & SPMV_TUNE_OBJ_MASK) >> 4);
-  if (!h || (flags & ~(SPMV_TUNE_ALL | SPMV_TUNE_OBJ_MASK | SPMV_TUNE_PREDICT)) || what == 0 ||
-      expected_iterations < 0)
+  if (!h || (flags & ~(SPMV_TUNE_ALL | SPMV_TUNE_OBJ_MASK | SPMV_TUNE_PREDICT | SPMV_TUNE_DECIDE_ONLY)) ||
+      what == 0 || expected_iterations < 0)
     return SPMV_ERR_INVALID_ARG;
   const bool predict = (flags & SPMV_TUNE_PREDICT) != 0;
+  const bool decide_only = (flags & SPMV_TUNE_DECIDE_ONLY) != 0;
   if (predict && !(what & SPMV_TUNE_FORMAT)) return SPMV_ERR_INVALID_ARG;
+  if (decide_only && (!predict || (what & SPMV_TUNE_LAUNCH))) return SPMV_ERR_INVALID_ARG;
   if (predict && obj != 0) return SPMV_ERR_UNSUPPORTED;
   if (h->rows == 0 || h->nnz == 0) return SPMV_ERR_INVALID_ARG;
   API_TRY
@@ -1016,13 +1087,15 @@ spmv_status_t spmv_tune(spmv_handle_t h, uint32_t flags, int64_t expected_iterat
   rep.energy_j = rep.power_w = rep.mflops_per_w = std::nan("");
   TuneScratch ts(h);
   if (what & SPMV_TUNE_FORMAT) {
-    if (predict) tune_predict(h, expected_iterations, ts, &rep);
+    if (predict) tune_predict(h, expected_iterations, ts, &rep, decide_only);
     else tune_format(h, expected_iterations, ts, &rep, obj, (what & SPMV_TUNE_LAUNCH) != 0);
   }
   // after a measured format selection with LAUNCH the chosen launch is already tuned
   if ((what & SPMV_TUNE_LAUNCH) && (predict || !(what & SPMV_TUNE_FORMAT))) tune_launch(h, h->active, ts, &rep, obj);
-  rep.format = h->active;
-  rep.launch = resolve_launch(h, h->active, h->launch[h->active]);
+  if (!decide_only) {
+    rep.format = h->active;
+    rep.launch = resolve_launch(h, h->active, h->launch[h->active]);
+  }
   CK(cudaStreamSynchronize(h->stream));
   if (out) *out = rep;
   API_CATCH(h)
@@ -1064,6 +1137,7 @@ spmv_status_t spmv_norm2(spmv_handle_t h, const void* x, int64_t n, double* sums
 spmv_status_t spmv_power_iterate(spmv_handle_t h, const void* x0, void* buf0, void* buf1, int64_t n_full,
                                  int64_t steps, double* sums, void* comm, int64_t chunk, void* chunk_buf,
                                  float* kernel_ms, float* loop_ms, int* final_buf) {
+  const NvtxRange nvtx_range("spmv_power_iterate");
   if (!h || !x0 || !buf0 || !buf1 || !sums || steps < 0 || n_full < h->rows || buf0 == buf1) return SPMV_ERR_INVALID_ARG;
   if (comm && (!chunk_buf || chunk < h->rows)) return SPMV_ERR_INVALID_ARG;
   if (!built(h, h->active)) return SPMV_ERR_NOT_CONVERTED;
@@ -1075,6 +1149,7 @@ spmv_status_t spmv_power_iterate(spmv_handle_t h, const void* x0, void* buf0, vo
 
 spmv_status_t spmv_dist_plan_create(spmv_dist_plan_t* out, spmv_handle_t h, void* comm, int64_t chunk,
                                     uint32_t flags) {
+  const NvtxRange nvtx_range("spmv_dist_plan_create");
   if (!out) return SPMV_ERR_INVALID_ARG;
   *out = nullptr;
   if (!h || (comm && chunk < 1) || (flags & ~(SPMV_PLAN_OVERLAP | SPMV_PLAN_HALO))) return SPMV_ERR_INVALID_ARG;
@@ -1099,6 +1174,7 @@ spmv_status_t spmv_dist_plan_part(spmv_dist_plan_t plan, int part, spmv_handle_t
 
 spmv_status_t spmv_dist_plan_iterate(spmv_dist_plan_t plan, const void* x0, void* buf0, void* buf1, int64_t steps,
                                      double* sums, float* loop_ms, float* interior_ms, int* final_buf) {
+  const NvtxRange nvtx_range("spmv_dist_plan_iterate");
   if (!plan || !x0 || !buf0 || !buf1 || !sums || steps < 0 || buf0 == buf1) return SPMV_ERR_INVALID_ARG;
   API_TRY
   DeviceGuard g(plan_device(plan));
@@ -1122,6 +1198,7 @@ spmv_status_t spmv_dist_local_group(int world, const int* devices, void** comms)
 }
 
 spmv_status_t spmv_create_row_slice(spmv_handle_t* out, spmv_handle_t h, int64_t row_begin, int64_t row_end) {
+  const NvtxRange nvtx_range("spmv_create_row_slice");
   if (!out) return SPMV_ERR_INVALID_ARG;
   *out = nullptr;
   if (!h || row_begin < 0 || row_end < row_begin || row_end > h->rows) return SPMV_ERR_INVALID_ARG;
@@ -1249,6 +1326,7 @@ spmv_status_t spmv_set_stream(spmv_handle_t h, void* s) {
 }
 
 spmv_status_t spmv_destroy(spmv_handle_t h) {
+  const NvtxRange nvtx_range("spmv_destroy");
   if (!h) return SPMV_OK;
   destroy_handle(h);
   return SPMV_OK;

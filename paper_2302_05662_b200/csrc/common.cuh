@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/spmv.h"
 
 namespace spmv {
@@ -16,6 +18,17 @@ namespace spmv {
 struct SpmvError {
   spmv_status_t status;
   std::string msg;
+};
+
+// NVTX range for the duration of a scope (host-side phases: create, features,
+// convert, tune, the plan's exchange) so an nsys timeline shows the pipeline
+// and the overlap of the interior SpMV with the exchange. Header-only NVTX3:
+// a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 [[noreturn]] inline void fail(spmv_status_t s, const std::string& m) { throw SpmvError{s, m}; }

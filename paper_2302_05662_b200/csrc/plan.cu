@@ -297,6 +297,7 @@ bool build_halo_lists(spmv_dist_plan* P) {
 }
 
 void exchange_step(spmv_dist_plan* P, void* x) {
+  const NvtxRange nvtx_range("plan_exchange");
   cudaStream_t cs = P->cs;
   char* xb = static_cast<char*>(x);
   const int vb = P->vb;

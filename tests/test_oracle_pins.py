@@ -438,6 +438,26 @@ def test_parity_check_rule():
     assert not ok
 
 
+def test_omp_leg_bitwise():
+    """The all-core timing leg (SURVEY §8(d) CPU baseline) sums each row on one
+    thread in the same order: y, Σ|a·x| and the power step are bitwise the
+    1-thread oracle's, and the closed form A·1 = row sums still holds."""
+    coo = si.stencil27(24, random_values=True)
+    rp, C, V = build(coo)
+    x = si.vector(coo.cols)
+    y1, a1 = oracle.spmv_csr(coo.rows, rp, C, V, x, 2.5, -0.5, x[: coo.rows])
+    y2, a2 = oracle.spmv_csr(coo.rows, rp, C, V, x, 2.5, -0.5, x[: coo.rows], all_cores=True)
+    assert np.array_equal(y1.view(np.int64), y2.view(np.int64)) and np.array_equal(a1, a2)
+    p1 = oracle.power_step(coo.rows, rp, C, V, x / np.linalg.norm(x))
+    p2 = oracle.power_step(coo.rows, rp, C, V, x / np.linalg.norm(x), all_cores=True)
+    assert np.array_equal(p1[0], p2[0]) and np.array_equal(p1[1], p2[1]) and p1[2:] == p2[2:]
+    lap = si.stencil27(24)
+    rp, C, V = build(lap)
+    y, _ = oracle.spmv_csr(lap.rows, rp, C, V, np.ones(lap.cols), all_cores=True)
+    assert (y == 27 - np.diff(rp)).all()
+    assert oracle.omp_threads() >= 1
+
+
 def test_power_step_closed_forms():
     N = 64
     coo = si.lap2d(N)
