@@ -16,6 +16,8 @@
 #include <vector>
 
 #include "dist.cuh"
+#include "kern_coo_decl.cuh"
+#include "kern_csr_decl.cuh"
 #include "kern_sliced_decl.cuh"
 #include "selector.cuh"
 #include "spmv_common.cuh"
@@ -375,7 +377,8 @@ static void log_append(spmv_matrix* h, const std::string& rec) {
 static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
   switch (fmt) {
     case SPMV_FMT_CSR:
-      if (h->csr_alg == SPMV_CSR_MERGE) return {4, 8, 16};
+      if (h->csr_alg == SPMV_CSR_MERGE)  // per-warp merge walk, or row-interleaved tiles of block·IPT items
+        return {4, 8, 16, kern::kMergeTile | 4, kern::kMergeTile | 8, kern::kMergeTile | 16};
       if (h->csr_alg == SPMV_CSR_STREAM) return {16, 32, 64};
       {
         int t = csr_default_lanes(h);
@@ -387,8 +390,9 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
     case SPMV_FMT_ELL:  // rows per warp × batch loop (kern::kSlicedCarry)
       return {32, 64, 128, 32 | kern::kSlicedCarry, 64 | kern::kSlicedCarry, 128 | kern::kSlicedCarry};
     case SPMV_FMT_SELL: return {(int)h->sell_C, (int)h->sell_C | kern::kSlicedCarry};
-    case SPMV_FMT_COO: return {2, 4, 8};
-    case SPMV_FMT_HYB: return {2, 4, 8};
+    case SPMV_FMT_COO:  // warp chunks of 32·W entries, or row-interleaved tiles of block·EPT entries
+    case SPMV_FMT_HYB:
+      return {2, 4, 8, kern::kCooTile | 4, kern::kCooTile | 8, kern::kCooTile | 16};
     case SPMV_FMT_BELL: return {(int)h->bell_b};
   }
   return {0};

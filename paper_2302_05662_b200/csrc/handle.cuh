@@ -89,7 +89,7 @@ struct spmv_matrix {
   // the CSR arrays never change after create, so it is computed once
   int64_t* merge_coords = nullptr;
   int64_t merge_coords_n = 0;
-  int merge_coords_ipt = 0;
+  int merge_coords_ipt = 0;  // merge items per chunk the cached coordinates were computed for
   double* pi_partials = nullptr;
   unsigned* pi_counter = nullptr;
   size_t pi_partials_n = 0;

@@ -5,5 +5,8 @@ namespace kern {
 template CooFn coo_fn<float, 2>(int, int);
 template CooFn coo_fn<float, 4>(int, int);
 template CooFn coo_fn<float, 8>(int, int);
+template CooFn coo_tile_fn<float, 4>(int, int);
+template CooFn coo_tile_fn<float, 8>(int, int);
+template CooFn coo_tile_fn<float, 16>(int, int);
 }  // namespace kern
 }  // namespace spmv

@@ -414,6 +414,121 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_merge(const
   }
 }
 
+// Merge-path CSR on row-interleaved tiles. A block owns the merge-path chunk
+// of B·IPT items [(x0, y0), (x1, y1)) from the partition pre-pass, so one
+// 150K-entry row and thousands of empty rows cost the same per item (the
+// load balance of merge-path). The block stages the chunk's entries
+// (col, val of [y0, y1), coalesced) and the starts of its rows x0 .. x1
+// (clamped to the chunk) in shared memory, then walks the rows thread per
+// row: at step k the lanes of a warp gather the k-th entry of 32 consecutive
+// rows (adjacent x on banded matrices) instead of staging products and
+// walking the merge path per lane (k_csr_merge above), and rows longer than
+// kLong entries are summed by a warp. Empty rows are written here too. Row
+// x0, if it began before y0, leaves its partial in rec.head; row x1, if it
+// has entries here and continues past y1, in rec.tail; k_seg_fixup finishes
+// both (deterministic). Same chunk-record semantics as k_csr_merge.
+template <int B, int R, class T, int IPT, class RP>
+__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_merge_tile(const CsrParams p) {
+  constexpr int ITEMS = B * IPT;
+  constexpr int NW = B / 32;
+  constexpr int kLong = 64;
+  constexpr int U = 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* s_val = reinterpret_cast<T*>(smem_raw);
+  int32_t* s_col = reinterpret_cast<int32_t*>(smem_raw + (size_t)ITEMS * sizeof(T));
+  int32_t* s_rs = s_col + ITEMS;  // row starts relative to y0, clamped to [0, nnzc]
+  __shared__ int s_nlong;
+  __shared__ int s_long[ITEMS / kLong + 1];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t chunk = blockIdx.x;
+  const RP* __restrict__ rp = static_cast<const RP*>(p.rp);
+  const T* __restrict__ val = static_cast<const T*>(p.val);
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  T* __restrict__ y = static_cast<T*>(p.y);
+  const int64_t x0 = p.coords[2 * chunk], y0 = p.coords[2 * chunk + 1];
+  const int64_t x1 = p.coords[2 * chunk + 2], y1 = p.coords[2 * chunk + 3];
+  const int nnzc = (int)(y1 - y0);
+  const bool cont_in = x0 < p.rows && y0 > (int64_t)rp[x0];
+  const bool cont_out = x1 < p.rows && y1 > (int64_t)rp[x1];
+  // rows x0 .. x1-1 end in this chunk; row x1 is here iff it has entries here
+  const int nseg = (int)(x1 - x0) + (cont_out ? 1 : 0);
+  for (int i = t; i < nnzc; i += B) {
+    s_col[i] = ld_stream(p.col + y0 + i);
+    s_val[i] = ld_stream(val + y0 + i);
+  }
+  for (int j = t; j <= nseg; j += B) {
+    const int64_t r = x0 + j;
+    int64_t v = r <= p.rows ? (int64_t)rp[r] : (int64_t)y1;
+    v = v < y0 ? y0 : (v > y1 ? y1 : v);
+    s_rs[j] = (int)(v - y0);
+  }
+  if (t == 0) s_nlong = 0;
+  __syncthreads();
+  const double alpha = epi_alpha(p.e);
+  auto finish = [&](int j, double acc) {
+    const int64_t row = x0 + j;
+    const bool first = j == 0 && cont_in, last = j == nseg - 1 && cont_out;
+    if (first || last) {
+      ChunkRec& rec = p.recs[chunk];
+      if (first) rec.head = acc;
+      if (last) rec.tail = acc;
+    } else {
+      y[row] = epi_value<T>(p.e, alpha, acc, y, row);
+    }
+  };
+  for (int j = t; j < nseg; j += B) {
+    const int a = s_rs[j], len = s_rs[j + 1] - a;
+    if (len > kLong) {
+      s_long[atomicAdd(&s_nlong, 1)] = j;
+      continue;
+    }
+    int rot = (len & 7) == 0 && len > 0 ? lane : 0;
+    if (len > 0 && rot >= len) rot %= len;
+    double acc = 0.0;
+    for (int k = 0; k < len; k += U) {
+      int c[U];
+      T v[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        int i = k + q + rot;
+        i = i >= len ? i - len : i;
+        const bool ok = k + q < len;
+        c[q] = ok ? s_col[a + i] : 0;
+        v[q] = ok ? s_val[a + i] : T(0);
+      }
+      T xv[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) xv[q] = k + q < len ? ld_x(x + c[q]) : T(0);
+#pragma unroll
+      for (int q = 0; q < U; ++q) acc = fma((double)v[q], (double)xv[q], acc);
+    }
+    finish(j, acc);
+  }
+  __syncthreads();
+  const int nlong = s_nlong;
+  for (int q = w; q < nlong; q += NW) {
+    const int j = s_long[q];
+    const int a = s_rs[j], b = s_rs[j + 1];
+    double acc = 0.0;
+    for (int k = a + lane; k < b; k += 32) acc = fma((double)s_val[k], (double)ld_x(x + s_col[k]), acc);
+    acc = warp_sum(acc);
+    if (lane == 0) finish(j, acc);
+  }
+  if (t == 0) {
+    ChunkRec& rec = p.recs[chunk];
+    rec.first_row = (int32_t)x0;
+    rec.cont_in = cont_in;
+    rec.last_row = (int32_t)(cont_out ? x1 : (x1 - 1 > x0 ? x1 - 1 : x0));
+    rec.cont_out = cont_out;
+  }
+}
+
+template <int B, int R, class T, int I, class RP>
+constexpr CsrFn merge_tile_ptr() {
+  if constexpr (merge_tile_smem<T>(B, I) > 200 * 1024) return nullptr;
+  else return &k_csr_merge_tile<B, R, T, I, RP>;
+}
+
 template <class RP>
 __global__ void k_merge_partition(const RP* __restrict__ rp, int64_t rows, int64_t nnz, int64_t items,
                                   int64_t nchunks, int64_t* __restrict__ coords) {
@@ -456,6 +571,16 @@ CsrFn csr_stream_fn(int bi, int ri) {
 }
 #undef CSRS_TAB
 #undef CSRS_ROW
+
+#define CSRMT_ROW(B, I) {merge_tile_ptr<B, 32, T, I, RP>(), merge_tile_ptr<B, 64, T, I, RP>(), \
+                         merge_tile_ptr<B, 128, T, I, RP>(), merge_tile_ptr<B, 255, T, I, RP>()}
+template <class T, class RP, int I>
+CsrFn csr_merge_tile_fn(int bi, int ri) {
+  static const CsrFn tab[5][4] = {CSRMT_ROW(64, I), CSRMT_ROW(128, I), CSRMT_ROW(256, I), CSRMT_ROW(512, I),
+                                  CSRMT_ROW(1024, I)};
+  return tab[bi][ri];
+}
+#undef CSRMT_ROW
 
 #define CSRM_ROW(B, I) {&k_csr_merge<B, 32, T, I, RP>, &k_csr_merge<B, 64, T, I, RP>, \
                         &k_csr_merge<B, 128, T, I, RP>, &k_csr_merge<B, 255, T, I, RP>}

@@ -55,6 +55,16 @@ template <class T>
 constexpr size_t merge_smem_bytes(int block, int ipt) {
   return (size_t)(block / 32) * merge_warp_smem(ipt);
 }
+// Merge-path tiles (k_csr_merge_tile): launch knob kMergeTile | IPT; a block
+// owns block·IPT merge items (row ends + entries).
+constexpr int kMergeTile = 0x100;
+template <class T, class RP, int IPT>
+CsrFn csr_merge_tile_fn(int bi, int ri);
+template <class T>
+constexpr size_t merge_tile_smem(int block, int ipt) {
+  // col + value of up to block·IPT entries, then up to block·IPT + 2 row starts
+  return (size_t)block * ipt * (4 + sizeof(T)) + ((size_t)block * ipt + 2) * 4 + 16;
+}
 // Merge-path partition pre-pass: coords[2c], coords[2c+1] = start of chunk c.
 void merge_partition(const void* rp, bool rp64, int64_t rows, int64_t nnz, int64_t items_per_chunk,
                      int64_t nchunks, int64_t* coords, cudaStream_t s);

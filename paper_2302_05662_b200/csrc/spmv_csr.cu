@@ -68,34 +68,40 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
     return;
   }
-  const int ipt = L.knob;
+  const bool tile = (L.knob & kern::kMergeTile) != 0;
+  const int ipt = L.knob & 0xff;
   const void* fn;
   switch (ipt) {
-    case 4: fn = (const void*)kern::csr_merge_fn<T, RP, 4>(bi, ri); break;
-    case 8: fn = (const void*)kern::csr_merge_fn<T, RP, 8>(bi, ri); break;
-    case 16: fn = (const void*)kern::csr_merge_fn<T, RP, 16>(bi, ri); break;
-    default: fail(SPMV_ERR_INVALID_ARG, "merge-path items per thread must be 4, 8 or 16");
+    case 4: fn = tile ? (const void*)kern::csr_merge_tile_fn<T, RP, 4>(bi, ri)
+                      : (const void*)kern::csr_merge_fn<T, RP, 4>(bi, ri); break;
+    case 8: fn = tile ? (const void*)kern::csr_merge_tile_fn<T, RP, 8>(bi, ri)
+                      : (const void*)kern::csr_merge_fn<T, RP, 8>(bi, ri); break;
+    case 16: fn = tile ? (const void*)kern::csr_merge_tile_fn<T, RP, 16>(bi, ri)
+                       : (const void*)kern::csr_merge_fn<T, RP, 16>(bi, ri); break;
+    default: fail(SPMV_ERR_INVALID_ARG, "merge-path items per thread must be 4, 8 or 16 (or kMergeTile | 4, 8, 16)");
   }
-  const size_t smem = kern::merge_smem_bytes<T>(L.block, ipt);
+  if (!fn) fail(SPMV_ERR_UNSUPPORTED, "merge-path tile: block × items per thread exceeds shared memory");
+  const size_t smem = tile ? kern::merge_tile_smem<T>(L.block, ipt) : kern::merge_smem_bytes<T>(L.block, ipt);
   const LaunchAttrs attrs(fn, L.carveout_pct, smem);
   const int64_t total = h->rows + h->nnz;
-  const int64_t items = 32LL * ipt;
+  const int64_t items = tile ? (int64_t)L.block * ipt : 32LL * ipt;
   const int64_t nchunks = (total + items - 1) / items;
   if (nchunks <= 0) return;
   p.recs = static_cast<ChunkRec*>(ensure_seg_scratch(h, (size_t)nchunks * sizeof(ChunkRec)));
-  if (!h->merge_coords || h->merge_coords_ipt != ipt || h->merge_coords_n != nchunks) {
+  // chunk coordinates depend only on the CSR arrays and the items per chunk
+  if (!h->merge_coords || h->merge_coords_ipt != items || h->merge_coords_n != nchunks) {
     dfree(h->merge_coords, h->stream);
     h->merge_coords = nullptr;
     h->merge_coords = static_cast<int64_t*>(dalloc((size_t)(nchunks + 1) * 2 * sizeof(int64_t), h->stream));
     kern::merge_partition(h->row_ptr, h->rp64, h->rows, h->nnz, items, nchunks, h->merge_coords, h->stream);
-    h->merge_coords_ipt = ipt;
+    h->merge_coords_ipt = items;
     h->merge_coords_n = nchunks;
   }
   p.coords = h->merge_coords;
   p.nchunks = nchunks;
   // mode 1 (power step): alpha from device, beta = 0; the norms are computed
   // afterwards by run_norms because boundary rows finish in the fixup.
-  const int64_t grid = (nchunks * 32 + L.block - 1) / L.block;
+  const int64_t grid = tile ? nchunks : (nchunks * 32 + L.block - 1) / L.block;
   void* args[] = {&p};
   launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, smem, h->stream);
   run_seg_fixup(h, p.recs, nchunks, e, y);

@@ -110,14 +110,32 @@ void coo_launch(spmv_matrix* h, const int32_t* row, const int32_t* col, const vo
   const int W = L.knob;
   const int bi = block_index(L.block), ri = reg_index(L.maxreg);
   const void* fn;
-  switch (W) {
-    case 2: fn = (const void*)kern::coo_fn<T, 2>(bi, ri); break;
-    case 4: fn = (const void*)kern::coo_fn<T, 4>(bi, ri); break;
-    case 8: fn = (const void*)kern::coo_fn<T, 8>(bi, ri); break;
-    default: fail(SPMV_ERR_INVALID_ARG, "COO entries per lane must be 2, 4 or 8");
+  const bool tile = (W & kern::kCooTile) != 0;
+  const int ept = W & 0xff;
+  size_t smem = 0;
+  int64_t per_chunk = 32LL * W;
+  if (tile) {
+    switch (ept) {
+      case 4: fn = (const void*)kern::coo_tile_fn<T, 4>(bi, ri); break;
+      case 8: fn = (const void*)kern::coo_tile_fn<T, 8>(bi, ri); break;
+      case 16: fn = (const void*)kern::coo_tile_fn<T, 16>(bi, ri); break;
+      default: fail(SPMV_ERR_INVALID_ARG, "COO tile entries per thread must be 4, 8 or 16");
+    }
+    if (!fn) fail(SPMV_ERR_UNSUPPORTED, "COO tile: block × entries per thread exceeds shared memory");
+    if (((uintptr_t)row | (uintptr_t)col | (uintptr_t)val) & 15)
+      fail(SPMV_ERR_UNSUPPORTED, "COO tile: row/col/val must be 16-byte aligned for vector staging");
+    smem = kern::coo_tile_smem<T>(L.block, ept);
+    per_chunk = (int64_t)L.block * ept;
+  } else {
+    switch (W) {
+      case 2: fn = (const void*)kern::coo_fn<T, 2>(bi, ri); break;
+      case 4: fn = (const void*)kern::coo_fn<T, 4>(bi, ri); break;
+      case 8: fn = (const void*)kern::coo_fn<T, 8>(bi, ri); break;
+      default: fail(SPMV_ERR_INVALID_ARG, "COO entries per lane must be 2, 4 or 8 (or kCooTile | 4, 8, 16)");
+    }
   }
-  const LaunchAttrs attrs(fn, L.carveout_pct);
-  const int64_t nchunks = (nnz + 32LL * W - 1) / (32LL * W);
+  const LaunchAttrs attrs(fn, L.carveout_pct, smem);
+  const int64_t nchunks = (nnz + per_chunk - 1) / per_chunk;
   kern::CooParams p{};
   p.row = row;
   p.col = col;
@@ -127,9 +145,9 @@ void coo_launch(spmv_matrix* h, const int32_t* row, const int32_t* col, const vo
   p.y = y;
   p.e = e;
   p.recs = static_cast<ChunkRec*>(ensure_seg_scratch(h, (size_t)nchunks * sizeof(ChunkRec)));
-  const int64_t grid = (nchunks * 32 + L.block - 1) / L.block;
+  const int64_t grid = tile ? nchunks : (nchunks * 32 + L.block - 1) / L.block;
   void* args[] = {&p};
-  launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
+  launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, smem, h->stream);
   run_seg_fixup(h, p.recs, nchunks, e, y);
 }
 
