@@ -526,6 +526,31 @@ def ncu_traffic(cfg, label):
     return None, None
 
 
+# The compile-time mode's launch sweep (a6: 80 block × reg cap × carveout
+# points × knobs, each timed over >= 6 ms) costs minutes on c5's 7 ms SpMV.
+# On matrices above this size it runs on a contiguous slab of rows from the
+# middle of the matrix holding about this many entries (same format and
+# parameters): the kernels are persistent grid-stride loops whose best
+# variant depends on the row structure, not on the row count, once the
+# slab fills every SM many times over.
+LAUNCH_SAMPLE_NNZ = 1 << 28
+
+
+def tune_launch_on_slab(P, h, fmt, params, E):
+    feats = P.spmv_features(h)
+    rows = int(feats["n_rows"])
+    take = max(1, min(rows, int(rows * LAUNCH_SAMPLE_NNZ / max(1, int(feats["nnz"])))))
+    r0 = (rows - take) // 2
+    sl = P.spmv_create_row_slice(h, r0, r0 + take)
+    try:
+        P.spmv_convert(sl, fmt, **normalise_params(P, fmt, params))
+        P.spmv_tune(sl, P.TUNE_LAUNCH, expected_iterations=E)
+        return {"launch": tuple(P.spmv_get_launch(sl, fmt)), "rows": (r0, r0 + take),
+                "log": [dict(r, slab_rows=[r0, r0 + take]) for r in P.spmv_decision_log(sl)]}
+    finally:
+        P.spmv_destroy(sl)
+
+
 def time_plain(P, h, fmt, x, y, min_ms=200.0):
     """Median of 5 batches of back-to-back plain SpMVs (alpha=1, beta=0) with
     CUDA events on the current stream; each batch >= min_ms/5."""
@@ -663,11 +688,15 @@ def run_rank(args, ctx: Ctx, shared: dict):
     h = P.spmv_create(coo.rows, coo.cols, coo.row, coo.col, coo.val)
     P.spmv_features(h)
     if args.format == "auto":
-        flags = P.TUNE_FORMAT | (0 if args.no_tune_launch else P.TUNE_LAUNCH)
+        big = coo.nnz > LAUNCH_SAMPLE_NNZ
+        flags = P.TUNE_FORMAT | (0 if (args.no_tune_launch or big) else P.TUNE_LAUNCH)
         rep = P.spmv_tune(h, flags, expected_iterations=E)
         fmt = rep.format
         params = report_params(P, rep)
         decision = P.spmv_decision_log(h)
+        if big and not args.no_tune_launch:
+            launch_slab = tune_launch_on_slab(P, h, fmt, params, E)
+            decision = decision + launch_slab["log"]
     else:
         csr_algs = {"CSR-vector": P.CSR_VECTOR, "CSR-merge": P.CSR_MERGE, "CSR-stream": P.CSR_STREAM}
         fmt = P.FMT_CSR if args.format in csr_algs else P.FORMATS[args.format]
@@ -682,6 +711,8 @@ def run_rank(args, ctx: Ctx, shared: dict):
         decision = P.spmv_decision_log(h)
     params = normalise_params(P, fmt, params)
     launch = tuple(P.spmv_get_launch(h, fmt))
+    if args.format == "auto" and coo.nnz > LAUNCH_SAMPLE_NNZ and not args.no_tune_launch:
+        launch = tuple(launch_slab["launch"])
     P.spmv_destroy(h)
     offline_s = time.perf_counter() - t_off
     offline = {"format": fmt, "params": params, "launch": launch}
