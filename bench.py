@@ -484,8 +484,8 @@ def fmt_label(P, fmt, params):
     if fmt == P.FMT_CSR:
         name += {P.CSR_MERGE: "-merge", P.CSR_STREAM: "-stream", P.CSR_SCALAR: "-scalar"}.get(
             params.get("csr_alg", 0), "-vector")
-    if fmt in (P.FMT_ELL, P.FMT_SELL) and params.get("index16", 0) == 1:
-        name += "-16"
+    if fmt in (P.FMT_ELL, P.FMT_SELL) and params.get("index16", 0) in (1, 2):
+        name += "-16" if params["index16"] == 1 else "-8"
     if fmt == P.FMT_BELL:
         name += f"-{params.get('bell_b', 2)}"
     return name
@@ -607,7 +607,7 @@ def per_config_leg(args, P, si, peak):
             fmt = rep.format
             params = report_params(P, rep)
             info = P.spmv_format_info(h, fmt)
-            label = fmt_label(P, fmt, dict(params, index16=1 if info.get("index_bytes") == 2 else 0))
+            label = fmt_label(P, fmt, dict(params, index16={2: 1, 1: 2}.get(info.get("index_bytes"), 0)))
             t, reps = time_plain(P, h, fmt, x, y)
             alg = info["stored_bytes"] + x.numel() * vb + y.numel() * vb
             rec.update({"format": label, "launch": list(P.spmv_get_launch(h, fmt)), "kernel_us": round(t * 1e6, 2),
@@ -865,7 +865,7 @@ def run_rank(args, ctx: Ctx, shared: dict):
     k_avg_ms = statistics.mean(kernel_ms) if kernel_ms else float("nan")
     achieved = alg_bytes / (k_avg_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
-    label = fmt_label(P, sel_f, dict(sel_p, index16=1 if info.get("index_bytes") == 2 else 0))
+    label = fmt_label(P, sel_f, dict(sel_p, index16={2: 1, 1: 2}.get(info.get("index_bytes"), 0)))
     traffic, trec = ncu_traffic(args.config, label)
     kernel_share = sum(kernel_ms) / ms if ms > 0 else None
 

@@ -98,7 +98,11 @@ typedef struct {
   int32_t bell_b;     /* BELL square block dimension in {2,3,4}; 0 = 2 (the paper's 2×2) */
   int32_t index16;    /* ELL/SELL column storage: 0 = int32 columns (default); 1 = 16-bit offsets
                          d = col − row (10 instead of 12 B per fp64 slot; SPMV_ERR_UNSUPPORTED unless
-                         every |col − row| <= 32767); -1 = 16-bit when they fit, else int32 */
+                         every |col − row| <= 32767); 2 = 8-bit codes of d into a per-matrix
+                         dictionary of its distinct offsets (9 B per fp64 slot + a 1 KB table;
+                         SPMV_ERR_UNSUPPORTED unless the matrix has at most 255 distinct col − row,
+                         as banded / stencil matrices do: 27 for the 27-point stencil); -1 = the
+                         narrowest that fits: 8-bit, then 16-bit, else int32 */
 } spmv_format_params_t;
 
 /* Table 2 features + the north star's max and bandwidth.
@@ -193,7 +197,7 @@ typedef struct {
   int64_t n_empty_rows;  /* COO: rows without entries */
   int64_t stored_bytes;  /* bytes of the format's arrays (padding included) */
   int64_t block;         /* BELL block dimension b (K = blocks per block row, n_pad = padded block rows) */
-  int64_t index_bytes;   /* bytes per stored column index (2 with ELL/SELL index16, else 4; 0 = CSR/COO arrays) */
+  int64_t index_bytes;   /* bytes per stored column index (1 / 2 with ELL/SELL index16 = 2 / 1, else 4; 0 = CSR/COO arrays) */
 } spmv_format_info_t;
 
 typedef enum {
@@ -216,7 +220,10 @@ typedef enum {
   SPMV_ARR_BELL_COL = 16,     /* int32 [K·n_pad]: block column of slot (I, k) at k·n_pad + I, pad −1 */
   SPMV_ARR_BELL_VAL = 17,     /* value [K·b·b·n_pad]: entry (r, c) of slot (I, k) at (k·b·b + r·b + c)·n_pad + I */
   SPMV_ARR_ELL_COL16 = 18,    /* int16 [K·n_pad] when index16: d = col − row, pad −32768 (ELL_COL is then absent) */
-  SPMV_ARR_SELL_COL16 = 19    /* int16 [slots] when index16: d = col − row of the slot's (permuted) row, pad −32768 */
+  SPMV_ARR_SELL_COL16 = 19,   /* int16 [slots] when index16: d = col − row of the slot's (permuted) row, pad −32768 */
+  SPMV_ARR_ELL_COL8 = 20,     /* uint8 [K·n_pad] when index16 = 2: code of d = col − row, pad 255 */
+  SPMV_ARR_SELL_COL8 = 21,    /* uint8 [slots] when index16 = 2: code of d for the slot's (permuted) row, pad 255 */
+  SPMV_ARR_DICT8_TAB = 22     /* int32 [256]: the offset d of each 8-bit code (after an index16 = 2 build) */
 } spmv_array_t;
 
 /* ---------------------------------------------------------------- core API */

@@ -36,7 +36,7 @@ OBJECTIVES = {"latency": 0, "energy": 1, "power": 2, "efficiency": 3}   # OR-ed 
 (ARR_CSR_ROW_PTR, ARR_CSR_COL, ARR_CSR_VAL, ARR_COO_ROW, ARR_ELL_COL, ARR_ELL_VAL, ARR_SELL_PERM,
  ARR_SELL_SLICE_PTR, ARR_SELL_COL, ARR_SELL_VAL, ARR_HYB_ELL_COL, ARR_HYB_ELL_VAL, ARR_HYB_TAIL_ROW,
  ARR_HYB_TAIL_COL, ARR_HYB_TAIL_VAL, ARR_COO_EMPTY_ROWS, ARR_BELL_COL, ARR_BELL_VAL, ARR_ELL_COL16,
- ARR_SELL_COL16) = range(20)
+ ARR_SELL_COL16, ARR_ELL_COL8, ARR_SELL_COL8, ARR_DICT8_TAB) = range(23)
 
 
 class SpmvError(RuntimeError):

@@ -363,6 +363,13 @@ static double objective_value(int obj, const Measured& m) {
   }
 }
 
+// Column encoding of a built ELL/SELL layout: 0 int32, 1 16-bit offsets, 2 8-bit dictionary codes.
+static int index_encoding(const spmv_matrix* h, int fmt) {
+  if (fmt == SPMV_FMT_ELL) return h->ell_col8 ? 2 : (h->ell_col16 ? 1 : 0);
+  if (fmt == SPMV_FMT_SELL) return h->sell_col8 ? 2 : (h->sell_col16 ? 1 : 0);
+  return 0;
+}
+
 static const char* fmt_name(int f) {
   static const char* n[] = {"COO", "CSR", "ELL", "HYB", "SELL", "BELL"};
   return (f >= 0 && f < 6) ? n[f] : "?";
@@ -693,7 +700,7 @@ static void tune_format(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tun
     rep->params.sell_sigma = (int32_t)h->sell_sigma;
     rep->params.hyb_K = h->hyb_K;
     rep->params.bell_b = (int32_t)h->bell_b;
-    rep->params.index16 = (h->active == SPMV_FMT_ELL && h->ell_col16) || (h->active == SPMV_FMT_SELL && h->sell_col16);
+    rep->params.index16 = index_encoding(h, h->active);
   }
 }
 
@@ -833,7 +840,7 @@ static void tune_predict(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tu
     rep->params.sell_sigma = (int32_t)h->sell_sigma;
     rep->params.hyb_K = h->hyb_K;
     rep->params.bell_b = (int32_t)h->bell_b;
-    rep->params.index16 = (h->active == SPMV_FMT_ELL && h->ell_col16) || (h->active == SPMV_FMT_SELL && h->sell_col16);
+    rep->params.index16 = index_encoding(h, h->active);
   }
 }
 
@@ -844,6 +851,8 @@ static void destroy_handle(spmv_matrix* h) {
   dfree(h->seg_scratch, h->stream);
   dfree(h->fix_scratch, h->stream);
   dfree(h->merge_coords, h->stream);
+  dfree(h->dict8_map, h->stream);
+  dfree(h->dict8_tab, h->stream);
   dfree(h->pi_partials, h->stream);
   dfree(h->pi_counter, h->stream);  // stream-ordered frees: no host synchronisation
   for (auto& evs : h->lat_ev)
@@ -955,10 +964,10 @@ spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format
       if (!h->coo_built) build_coo(h);
       break;
     case SPMV_FMT_ELL: {
-      if (q.index16 < -1 || q.index16 > 1) fail(SPMV_ERR_INVALID_ARG, "index16 must be -1, 0 or 1");
+      if (q.index16 < -1 || q.index16 > 2) fail(SPMV_ERR_INVALID_ARG, "index16 must be -1, 0, 1 or 2");
       if (!h->have_features) compute_features(h);
-      const int want = q.index16 == -1 ? (offsets16_fit(h) ? 1 : 0) : q.index16;
-      if (h->ell_built && (want == 1) == (h->ell_col16 != nullptr)) break;
+      const int want = q.index16 == -1 ? resolve_index_auto(h) : q.index16;
+      if (h->ell_built && want == index_encoding(h, SPMV_FMT_ELL)) break;
       if (h->ell_built) free_format(h, SPMV_FMT_ELL);
       build_ell(h, want);
       break;
@@ -968,10 +977,10 @@ spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format
       int64_t sigma = q.sell_sigma ? q.sell_sigma : 1;
       if (C != 32 && C != 64 && C != 128 && C != 256) fail(SPMV_ERR_UNSUPPORTED, "SELL C must be 32, 64, 128 or 256");
       if (sigma < 1 || (sigma != 1 && sigma % C != 0)) fail(SPMV_ERR_INVALID_ARG, "SELL sigma must be 1 or a multiple of C");
-      if (q.index16 < -1 || q.index16 > 1) fail(SPMV_ERR_INVALID_ARG, "index16 must be -1, 0 or 1");
+      if (q.index16 < -1 || q.index16 > 2) fail(SPMV_ERR_INVALID_ARG, "index16 must be -1, 0, 1 or 2");
       if (!h->have_features) compute_features(h);
-      const int want = q.index16 == -1 ? (offsets16_fit(h) ? 1 : 0) : q.index16;
-      if (!h->sell_built || h->sell_C != C || h->sell_sigma != sigma || (want == 1) != (h->sell_col16 != nullptr)) {
+      const int want = q.index16 == -1 ? resolve_index_auto(h) : q.index16;
+      if (!h->sell_built || h->sell_C != C || h->sell_sigma != sigma || want != index_encoding(h, SPMV_FMT_SELL)) {
         if (h->sell_built) free_format(h, SPMV_FMT_SELL);
         build_sell(h, C, sigma, want);
       }
@@ -1261,7 +1270,7 @@ spmv_status_t spmv_format_info(spmv_handle_t h, spmv_format_t fmt, spmv_format_i
   }
   o->stored_bytes = o->present ? format_stored_bytes(h, fmt) : 0;
   if (o->present && (fmt == SPMV_FMT_ELL || fmt == SPMV_FMT_SELL || fmt == SPMV_FMT_HYB || fmt == SPMV_FMT_BELL))
-    o->index_bytes = (fmt == SPMV_FMT_ELL && h->ell_col16) || (fmt == SPMV_FMT_SELL && h->sell_col16) ? 2 : 4;
+    o->index_bytes = index_encoding(h, fmt) == 2 ? 1 : (index_encoding(h, fmt) == 1 ? 2 : 4);
   return SPMV_OK;
 }
 
@@ -1284,6 +1293,13 @@ spmv_status_t spmv_copy_array(spmv_handle_t h, spmv_array_t which, void* dst, in
       src = h->sell_col16;
       bytes = (need ? sell_slots(h) : 0) * 2;
       break;
+    case SPMV_ARR_ELL_COL8: need = h->ell_built && h->ell_col8; src = h->ell_col8; bytes = h->ell_K * h->ell_npad; break;
+    case SPMV_ARR_SELL_COL8:
+      need = h->sell_built && h->sell_col8;
+      src = h->sell_col8;
+      bytes = need ? sell_slots(h) : 0;
+      break;
+    case SPMV_ARR_DICT8_TAB: need = h->dict8_tab != nullptr; src = h->dict8_tab; bytes = 256 * 4; break;
     case SPMV_ARR_ELL_VAL: need = h->ell_built; src = h->ell_val; bytes = h->ell_K * h->ell_npad * vb; break;
     case SPMV_ARR_SELL_PERM: need = h->sell_built; src = h->sell_perm; bytes = h->rows * 4; break;
     case SPMV_ARR_SELL_SLICE_PTR: need = h->sell_built; src = h->sell_sp; bytes = (h->sell_ns + 1) * 8; break;

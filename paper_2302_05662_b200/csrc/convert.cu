@@ -17,22 +17,49 @@ namespace spmv {
 namespace {
 
 // ---------------------------------------------------------------- ELL
-// Column index as stored: int32 column (pad -1) or a 16-bit offset from
-// origin + row (pad -32768), see spmv_matrix::col_origin.
+// Column index as stored: int32 column (pad -1), a 16-bit offset from
+// origin + row (pad -32768), see spmv_matrix::col_origin, or the 8-bit code
+// of that offset in the handle's dictionary (pad 255; map[d + m] = code).
+struct Dict8View {
+  const uint8_t* map = nullptr;
+  int64_t m = 0;
+};
 template <class IDX>
-__device__ __forceinline__ IDX enc_col(int32_t c, int64_t row, int64_t origin) {
-  if constexpr (sizeof(IDX) == 2) return (IDX)((int64_t)c - origin - row);
+__device__ __forceinline__ IDX enc_col(int32_t c, int64_t row, int64_t origin, Dict8View dv) {
+  if constexpr (sizeof(IDX) == 1) return dv.map[(int64_t)c - origin - row + dv.m];
+  else if constexpr (sizeof(IDX) == 2) return (IDX)((int64_t)c - origin - row);
   else return (IDX)c;
 }
 template <class IDX>
 __device__ __forceinline__ IDX pad_col() {
-  return sizeof(IDX) == 2 ? (IDX)-32768 : (IDX)-1;
+  return sizeof(IDX) == 1 ? (IDX)255 : (sizeof(IDX) == 2 ? (IDX)-32768 : (IDX)-1);
+}
+
+// Offset dictionary: flag every offset d = col − origin − row that occurs
+// (thread per row), scan the flags into codes, then map[d + m] = code and
+// tab[code] = d for the first 255 codes.
+template <class RP>
+__global__ void k_dict_flags(const RP* __restrict__ rp, const int32_t* __restrict__ col, int64_t rows,
+                             int64_t origin, int64_t m, int64_t* __restrict__ flags) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) flags[(int64_t)col[k] - origin - i + m] = 1;
+}
+__global__ void k_dict_build(const int64_t* __restrict__ flags, const int64_t* __restrict__ codes, int64_t bins,
+                             int64_t m, uint8_t* __restrict__ map, int32_t* __restrict__ tab) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < bins; b += stride) {
+    const int64_t c = codes[b];
+    const bool hit = flags[b] != 0 && c < 255;
+    map[b] = hit ? (uint8_t)c : (uint8_t)255;
+    if (hit) tab[c] = (int32_t)(b - m);
+  }
 }
 
 template <class RP, class V, class IDX>
 __global__ void k_ell_fill(const RP* __restrict__ rp, const int32_t* __restrict__ col,
                            const V* __restrict__ val, int64_t rows, int64_t K, int64_t n_pad,
-                           IDX* __restrict__ colE, V* __restrict__ valE, int64_t origin) {
+                           IDX* __restrict__ colE, V* __restrict__ valE, int64_t origin, Dict8View dv) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
     int64_t a = 0, L = 0;
@@ -44,7 +71,7 @@ __global__ void k_ell_fill(const RP* __restrict__ rp, const int32_t* __restrict_
     for (int64_t k = 0; k < K; ++k) {
       int64_t pos = k * n_pad + i;
       if (k < L) {
-        colE[pos] = enc_col<IDX>(col[a + k], i, origin);
+        colE[pos] = enc_col<IDX>(col[a + k], i, origin, dv);
         valE[pos] = val[a + k];
       } else {
         colE[pos] = pad_col<IDX>();
@@ -113,7 +140,7 @@ template <class RP, class V, class IDX>
 __global__ void k_sell_fill(const RP* __restrict__ rp, const int32_t* __restrict__ col,
                             const V* __restrict__ val, const int32_t* __restrict__ perm, int64_t rows,
                             int64_t C, int64_t ns, const int64_t* __restrict__ sp,
-                            IDX* __restrict__ colS, V* __restrict__ valS, int64_t origin) {
+                            IDX* __restrict__ colS, V* __restrict__ valS, int64_t origin, Dict8View dv) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t total = ns * C;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
@@ -128,7 +155,7 @@ __global__ void k_sell_fill(const RP* __restrict__ rp, const int32_t* __restrict
     for (int64_t k = 0; k < w; ++k) {
       const int64_t pos = base + k * C + j;
       if (k < L) {
-        colS[pos] = enc_col<IDX>(col[a + k], i, origin);
+        colS[pos] = enc_col<IDX>(col[a + k], i, origin, dv);
         valS[pos] = val[a + k];
       } else {
         colS[pos] = pad_col<IDX>();
@@ -315,34 +342,44 @@ void lat_end(spmv_matrix* h, int fmt) {
 }
 
 template <class RP, class V>
-void ell_typed(spmv_matrix* h, bool d16) {
+void ell_typed(spmv_matrix* h, int enc) {
   cudaStream_t s = h->stream;
   const int64_t K = h->feat.max_len, n_pad = (h->rows + 127) / 128 * 128;
-  guard_bytes((double)K * n_pad * ((d16 ? 2.0 : 4.0) + sizeof(V)), "ELL");
+  const double ib = enc == 2 ? 1.0 : (enc == 1 ? 2.0 : 4.0);
+  guard_bytes((double)K * n_pad * (ib + sizeof(V)), "ELL");
   Scratch sc(s);
-  int32_t* colE = d16 ? nullptr : sc.get<int32_t>(K * n_pad);
-  int16_t* colE16 = d16 ? sc.get<int16_t>(K * n_pad) : nullptr;
+  int32_t* colE = enc == 0 ? sc.get<int32_t>(K * n_pad) : nullptr;
+  int16_t* colE16 = enc == 1 ? sc.get<int16_t>(K * n_pad) : nullptr;
+  uint8_t* colE8 = enc == 2 ? sc.get<uint8_t>(K * n_pad) : nullptr;
   V* valE = sc.get<V>(K * n_pad);
+  const Dict8View dv{h->dict8_map, h->dict8_m};
+  const RP* rp = static_cast<const RP*>(h->row_ptr);
+  const V* val = static_cast<const V*>(h->val);
   lat_begin(h, SPMV_FMT_ELL);  // c_latency = device time of the conversion kernels (allocation excluded)
-  if (d16)
-    LAUNCH((k_ell_fill<RP, V, int16_t>), grid_for(n_pad, 256), 256, 0, s, static_cast<const RP*>(h->row_ptr),
-           h->col, static_cast<const V*>(h->val), h->rows, K, n_pad, colE16, valE, h->col_origin);
+  const unsigned g = grid_for(n_pad, 256);
+  if (enc == 2)
+    LAUNCH((k_ell_fill<RP, V, uint8_t>), g, 256, 0, s, rp, h->col, val, h->rows, K, n_pad, colE8, valE,
+           h->col_origin, dv);
+  else if (enc == 1)
+    LAUNCH((k_ell_fill<RP, V, int16_t>), g, 256, 0, s, rp, h->col, val, h->rows, K, n_pad, colE16, valE,
+           h->col_origin, dv);
   else
-    LAUNCH((k_ell_fill<RP, V, int32_t>), grid_for(n_pad, 256), 256, 0, s, static_cast<const RP*>(h->row_ptr),
-           h->col, static_cast<const V*>(h->val), h->rows, K, n_pad, colE, valE, int64_t(0));
+    LAUNCH((k_ell_fill<RP, V, int32_t>), g, 256, 0, s, rp, h->col, val, h->rows, K, n_pad, colE, valE, int64_t(0),
+           dv);
   lat_end(h, SPMV_FMT_ELL);
-  for (void* p : {(void*)colE, (void*)colE16, (void*)valE})
+  for (void* p : {(void*)colE, (void*)colE16, (void*)colE8, (void*)valE})
     if (p) sc.keep(p);
   h->ell_K = K;
   h->ell_npad = n_pad;
   h->ell_col = colE;
   h->ell_col16 = colE16;
+  h->ell_col8 = colE8;
   h->ell_val = valE;
   h->ell_built = true;
 }
 
 template <class RP, class V>
-void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma, bool d16) {
+void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma, int enc) {
   cudaStream_t s = h->stream;
   const int64_t rows = h->rows, ns = (rows + C - 1) / C;
   Scratch sc(s);
@@ -364,12 +401,17 @@ void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma, bool d16) {
   int64_t* sp = sc.get<int64_t>(ns + 1);
   int32_t* colS = nullptr;
   int16_t* colS16 = nullptr;
+  uint8_t* colS8 = nullptr;
   V* valS = nullptr;
-  const double ib = d16 ? 2.0 : 4.0;
+  const double ib = enc == 2 ? 1.0 : (enc == 1 ? 2.0 : 4.0);
+  auto alloc_cols = [&](int64_t n) {
+    if (enc == 2) colS8 = sc.get<uint8_t>(n);
+    else if (enc == 1) colS16 = sc.get<int16_t>(n);
+    else colS = sc.get<int32_t>(n);
+  };
   if (use_ub) {
     guard_bytes((double)ub * (ib + sizeof(V)), "SELL");
-    if (d16) colS16 = sc.get<int16_t>(ub);
-    else colS = sc.get<int32_t>(ub);
+    alloc_cols(ub);
     valS = sc.get<V>(ub);
   }
   lat_begin(h, SPMV_FMT_SELL);  // c_latency = device time of the conversion kernels
@@ -387,22 +429,26 @@ void sell_typed(spmv_matrix* h, int64_t C, int64_t sigma, bool d16) {
   const int64_t slots = use_ub ? ub : read_i64(sp + ns, s);
   if (!use_ub) {
     guard_bytes((double)slots * (ib + sizeof(V)), "SELL");
-    if (d16) colS16 = sc.get<int16_t>(slots);
-    else colS = sc.get<int32_t>(slots);
+    alloc_cols(slots);
     valS = sc.get<V>(slots);
   }
-  if (d16)
-    LAUNCH((k_sell_fill<RP, V, int16_t>), grid_for(ns * C, 256), 256, 0, s, rp, h->col,
-           static_cast<const V*>(h->val), (const int32_t*)perm, rows, C, ns, (const int64_t*)sp, colS16, valS,
-           h->col_origin);
+  const Dict8View dv{h->dict8_map, h->dict8_m};
+  const unsigned g = grid_for(ns * C, 256);
+  const V* val = static_cast<const V*>(h->val);
+  if (enc == 2)
+    LAUNCH((k_sell_fill<RP, V, uint8_t>), g, 256, 0, s, rp, h->col, val, (const int32_t*)perm, rows, C, ns,
+           (const int64_t*)sp, colS8, valS, h->col_origin, dv);
+  else if (enc == 1)
+    LAUNCH((k_sell_fill<RP, V, int16_t>), g, 256, 0, s, rp, h->col, val, (const int32_t*)perm, rows, C, ns,
+           (const int64_t*)sp, colS16, valS, h->col_origin, dv);
   else
-    LAUNCH((k_sell_fill<RP, V, int32_t>), grid_for(ns * C, 256), 256, 0, s, rp, h->col,
-           static_cast<const V*>(h->val), (const int32_t*)perm, rows, C, ns, (const int64_t*)sp, colS, valS,
-           int64_t(0));
+    LAUNCH((k_sell_fill<RP, V, int32_t>), g, 256, 0, s, rp, h->col, val, (const int32_t*)perm, rows, C, ns,
+           (const int64_t*)sp, colS, valS, int64_t(0), dv);
   lat_end(h, SPMV_FMT_SELL);
-  for (void* p : {(void*)perm, (void*)sp, (void*)colS, (void*)colS16, (void*)valS})
+  for (void* p : {(void*)perm, (void*)sp, (void*)colS, (void*)colS16, (void*)colS8, (void*)valS})
     if (p) sc.keep(p);
   h->sell_col16 = colS16;
+  h->sell_col8 = colS8;
   h->sell_C = C;
   h->sell_sigma = sigma;
   h->sell_ns = ns;
@@ -428,7 +474,7 @@ void hyb_typed(spmv_matrix* h, int64_t K) {
   int64_t* toff = sc.get<int64_t>(rows + 1);
   lat_begin(h, SPMV_FMT_HYB);  // kernels + the tail-size read-back
   LAUNCH((k_ell_fill<RP, V, int32_t>), grid_for(n_pad, 256), 256, 0, s, rp, h->col, static_cast<const V*>(h->val),
-         rows, K, n_pad, colE, valE, int64_t(0));
+         rows, K, n_pad, colE, valE, int64_t(0), Dict8View{});
   LAUNCH(k_row_counts<RP>, grid_for(rows, 256), 256, 0, s, rp, rows, 1, K, cnt);
   exclusive_scan_i64(cnt, toff, rows, s);
   const int64_t tail = read_i64(toff + rows, s);
@@ -524,10 +570,11 @@ void dispatch(spmv_matrix* h, F&& f) {
 
 }  // namespace
 
-bool offsets16_fit(spmv_matrix* h) {
-  if (h->col_origin == 0 && h->have_features)  // bandwidth from the features (no device pass)
-    return h->feat.bw_lower <= 32767 && h->feat.bw_upper <= 32767;
-  if (h->rows == 0 || h->nnz == 0) return true;
+// Largest |col − col_origin − row| over the matrix (device pass unless the
+// features already hold the bandwidth).
+static int64_t max_offset(spmv_matrix* h) {
+  if (h->col_origin == 0 && h->have_features) return std::max(h->feat.bw_lower, h->feat.bw_upper);
+  if (h->rows == 0 || h->nnz == 0) return 0;
   Scratch sc(h->stream);
   unsigned long long* d = sc.get<unsigned long long>(1);
   CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long), h->stream));
@@ -540,34 +587,87 @@ bool offsets16_fit(spmv_matrix* h) {
            h->col_origin, d);
   unsigned long long m = 0;
   d2h_sync(&m, d, sizeof(m), h->stream);
-  return m <= 32767ull;
+  return (int64_t)m;
 }
 
-static bool resolve16(spmv_matrix* h, int index16, const char* what) {
-  if (index16 == 0) return false;
-  const bool fit = offsets16_fit(h);
-  if (index16 > 0 && !fit)
+bool offsets16_fit(spmv_matrix* h) { return max_offset(h) <= 32767; }
+
+// Offsets wider than this are not dictionary-coded (the flag array would
+// exceed 2^23 bins); such matrices are not banded anyway.
+constexpr int64_t kDictMaxOffset = 1LL << 22;
+
+int dict8_codes(spmv_matrix* h) {
+  if (h->dict8_count >= 0) return h->dict8_count;
+  const int64_t m = max_offset(h);
+  if (m > kDictMaxOffset) {
+    h->dict8_count = 256;
+    return h->dict8_count;
+  }
+  cudaStream_t s = h->stream;
+  const int64_t bins = 2 * m + 1;
+  Scratch sc(s);
+  int64_t* flags = sc.get<int64_t>(bins);
+  int64_t* codes = sc.get<int64_t>(bins + 1);
+  CK(cudaMemsetAsync(flags, 0, (size_t)bins * sizeof(int64_t), s));
+  const unsigned g = grid_for(h->rows, 256);
+  if (h->rows > 0) {
+    if (h->rp64)
+      LAUNCH(k_dict_flags<int64_t>, g, 256, 0, s, static_cast<const int64_t*>(h->row_ptr), h->col, h->rows,
+             h->col_origin, m, flags);
+    else
+      LAUNCH(k_dict_flags<int32_t>, g, 256, 0, s, static_cast<const int32_t*>(h->row_ptr), h->col, h->rows,
+             h->col_origin, m, flags);
+  }
+  exclusive_scan_i64(flags, codes, bins, s);
+  const int64_t count = read_i64(codes + bins, s);
+  h->dict8_count = (int)std::min<int64_t>(count, 256);
+  if (count <= 255) {
+    uint8_t* map = sc.get<uint8_t>(bins);
+    int32_t* tab = sc.get<int32_t>(256);
+    CK(cudaMemsetAsync(tab, 0, 256 * sizeof(int32_t), s));
+    LAUNCH(k_dict_build, grid_for(bins, 256), 256, 0, s, (const int64_t*)flags, (const int64_t*)codes, bins, m, map,
+           tab);
+    sc.keep(map);
+    sc.keep(tab);
+    h->dict8_map = map;
+    h->dict8_tab = tab;
+    h->dict8_m = m;
+  }
+  return h->dict8_count;
+}
+
+int resolve_index_auto(spmv_matrix* h) {
+  if (dict8_codes(h) <= 255) return 2;
+  return offsets16_fit(h) ? 1 : 0;
+}
+
+static int resolve_enc(spmv_matrix* h, int index16, const char* what) {
+  if (index16 == 0) return 0;
+  if (index16 < 0) return resolve_index_auto(h);
+  if (index16 == 1 && !offsets16_fit(h))
     fail(SPMV_ERR_UNSUPPORTED, std::string(what) + ": 16-bit column offsets need every |col - row| <= 32767");
-  return fit;
+  if (index16 == 2 && dict8_codes(h) > 255)
+    fail(SPMV_ERR_UNSUPPORTED, std::string(what) + ": 8-bit column codes need at most 255 distinct col - row offsets");
+  return index16;
 }
 
 void build_ell(spmv_matrix* h, int index16) {
   if (!h->have_features) compute_features(h);
-  const bool d16 = resolve16(h, index16, "ELL");
+  const int enc = resolve_enc(h, index16, "ELL");
   dispatch(h, [&](auto rpt, auto vt) {
     using RP = std::remove_pointer_t<decltype(rpt)>;
     using V = std::remove_pointer_t<decltype(vt)>;
-    ell_typed<RP, V>(h, d16);
+    ell_typed<RP, V>(h, enc);
   });
 }
 
 void build_sell(spmv_matrix* h, int64_t C, int64_t sigma, int index16) {
   if (!h->have_features) compute_features(h);
-  const bool d16 = resolve16(h, index16, "SELL");
+  const int enc = resolve_enc(h, index16, "SELL");
   dispatch(h, [&](auto rpt, auto vt) {
     using RP = std::remove_pointer_t<decltype(rpt)>;
     using V = std::remove_pointer_t<decltype(vt)>;
-    sell_typed<RP, V>(h, C, sigma, d16);
+    sell_typed<RP, V>(h, C, sigma, enc);
   });
 }
 
@@ -609,11 +709,11 @@ void free_format(spmv_matrix* h, int fmt) {
       h->coo_built = false;
       break;
     case SPMV_FMT_ELL:
-      F(h->ell_col); F(h->ell_col16); F(h->ell_val);
+      F(h->ell_col); F(h->ell_col16); F(h->ell_col8); F(h->ell_val);
       h->ell_built = false;
       break;
     case SPMV_FMT_SELL:
-      F(h->sell_perm); F(h->sell_sp); F(h->sell_col); F(h->sell_col16); F(h->sell_val);
+      F(h->sell_perm); F(h->sell_sp); F(h->sell_col); F(h->sell_col16); F(h->sell_col8); F(h->sell_val);
       h->sell_built = false;
       h->sell_slots_pending = false;
       break;
@@ -657,9 +757,11 @@ int64_t format_stored_bytes(spmv_matrix* h, int fmt) {
   switch (fmt) {
     case SPMV_FMT_CSR: return (h->rows + 1) * rpb + h->nnz * (4 + vb);
     case SPMV_FMT_COO: return h->nnz * (8 + vb) + h->coo_n_empty * 4;
-    case SPMV_FMT_ELL: return h->ell_K * h->ell_npad * ((h->ell_col16 ? 2 : 4) + vb);
+    case SPMV_FMT_ELL:
+      return h->ell_K * h->ell_npad * ((h->ell_col8 ? 1 : (h->ell_col16 ? 2 : 4)) + vb) + (h->ell_col8 ? 1024 : 0);
     case SPMV_FMT_SELL:
-      return sell_slots(h) * ((h->sell_col16 ? 2 : 4) + vb) + (h->sell_ns + 1) * 8 + (h->sell_perm ? h->rows * 4 : 0);
+      return sell_slots(h) * ((h->sell_col8 ? 1 : (h->sell_col16 ? 2 : 4)) + vb) + (h->sell_ns + 1) * 8 +
+             (h->sell_perm ? h->rows * 4 : 0) + (h->sell_col8 ? 1024 : 0);
     case SPMV_FMT_HYB: return h->hyb_K * h->hyb_npad * (4 + vb) + h->hyb_tail * (8 + vb);
     case SPMV_FMT_BELL: return h->bell_kb * h->bell_nbr_pad * (4 + h->bell_b * h->bell_b * vb);
   }

@@ -32,6 +32,7 @@ struct spmv_matrix {
   int32_t* ell_col = nullptr;
   void* ell_val = nullptr;
   int16_t* ell_col16 = nullptr;  // 16-bit column offsets (ell_col == nullptr then)
+  uint8_t* ell_col8 = nullptr;   // 8-bit dictionary codes (ell_col == nullptr then)
 
   // SELL-C-sigma.
   bool sell_built = false;
@@ -41,6 +42,15 @@ struct spmv_matrix {
   int32_t* sell_col = nullptr;
   void* sell_val = nullptr;
   int16_t* sell_col16 = nullptr;  // 16-bit column offsets (sell_col == nullptr then)
+  uint8_t* sell_col8 = nullptr;   // 8-bit dictionary codes (sell_col == nullptr then)
+  // 8-bit dictionary of the distinct offsets d = col − col_origin − row of
+  // the matrix (banded / stencil matrices have a few dozen: c5 has 27):
+  // column = col_origin + row + dict8_tab[code], pad code 255. Built once per
+  // handle (dict8_count = -1 until computed; > 255 = not encodable).
+  int dict8_count = -1;
+  int64_t dict8_m = 0;           // map covers d in [-m, m]
+  uint8_t* dict8_map = nullptr;  // [2m+1]: code of d + m
+  int32_t* dict8_tab = nullptr;  // [256]: d of each code
   // 16-bit ELL/SELL column offsets: column = col_origin + row + d, d in
   // [-32767, 32767], pad -32768 (row slices of the distributed plan set the
   // origin to their first global column position).
@@ -112,12 +122,18 @@ void compute_features(spmv_matrix* h);
 
 // convert.cu
 void build_coo(spmv_matrix* h);
-// index16: 0 = int32 columns, 1 = 16-bit offsets (SPMV_ERR_UNSUPPORTED if
-// they do not fit), -1 = 16-bit offsets when they fit.
+// index16 (column encoding): 0 = int32 columns, 1 = 16-bit offsets, 2 = 8-bit
+// codes into the offset dictionary (SPMV_ERR_UNSUPPORTED if the encoding does
+// not fit), -1 = the narrowest that fits (8-bit, then 16-bit, then int32).
 void build_ell(spmv_matrix* h, int index16 = 0);
 void build_sell(spmv_matrix* h, int64_t C, int64_t sigma, int index16 = 0);
 // True iff every column lies within ±32767 of col_origin + its row.
 bool offsets16_fit(spmv_matrix* h);
+// Distinct offsets d = col − col_origin − row (builds the dictionary once);
+// > 255 means the 8-bit encoding does not fit.
+int dict8_codes(spmv_matrix* h);
+// The encoding index16 = -1 resolves to on this handle (0, 1 or 2).
+int resolve_index_auto(spmv_matrix* h);
 void build_hyb(spmv_matrix* h, int64_t K);
 void build_bell(spmv_matrix* h, int64_t b);
 void free_format(spmv_matrix* h, int fmt);
@@ -145,7 +161,8 @@ void run_csr(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const sp
 void run_ell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);
 void run_ell_arrays(spmv_matrix* h, const int32_t* col, const void* val, int64_t K, int64_t n_pad,
                     const Epilogue& e, const void* x, void* y, const spmv_launch_t& L,
-                    const int16_t* col16 = nullptr);
+                    const int16_t* col16 = nullptr, const uint8_t* col8 = nullptr,
+                    const int32_t* tab8 = nullptr);
 // y <- beta·y over all rows (alpha == 0: A is not read).
 void run_scale(spmv_matrix* h, void* y, double beta);
 void run_sell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L);

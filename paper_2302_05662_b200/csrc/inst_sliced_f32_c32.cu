@@ -2,9 +2,9 @@
 #include "kern_sliced.cuh"
 namespace spmv {
 namespace kern {
-template SlicedFn sliced_fn<float, 32, false, false>(int, int);
-template SlicedFn sliced_fn<float, 32, false, true>(int, int);
-template SlicedFn sliced_fn<float, 32, true, false>(int, int);
-template SlicedFn sliced_fn<float, 32, true, true>(int, int);
+template SlicedFn sliced_fn<float, 32, 0, false>(int, int);
+template SlicedFn sliced_fn<float, 32, 0, true>(int, int);
+template SlicedFn sliced_fn<float, 32, 1, false>(int, int);
+template SlicedFn sliced_fn<float, 32, 1, true>(int, int);
 }  // namespace kern
 }  // namespace spmv

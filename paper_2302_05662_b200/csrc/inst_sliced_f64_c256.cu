@@ -2,9 +2,9 @@
 #include "kern_sliced.cuh"
 namespace spmv {
 namespace kern {
-template SlicedFn sliced_fn<double, 256, false, false>(int, int);
-template SlicedFn sliced_fn<double, 256, false, true>(int, int);
-template SlicedFn sliced_fn<double, 256, true, false>(int, int);
-template SlicedFn sliced_fn<double, 256, true, true>(int, int);
+template SlicedFn sliced_fn<double, 256, 0, false>(int, int);
+template SlicedFn sliced_fn<double, 256, 0, true>(int, int);
+template SlicedFn sliced_fn<double, 256, 1, false>(int, int);
+template SlicedFn sliced_fn<double, 256, 1, true>(int, int);
 }  // namespace kern
 }  // namespace spmv

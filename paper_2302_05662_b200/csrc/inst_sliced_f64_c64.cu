@@ -2,9 +2,9 @@
 #include "kern_sliced.cuh"
 namespace spmv {
 namespace kern {
-template SlicedFn sliced_fn<double, 64, false, false>(int, int);
-template SlicedFn sliced_fn<double, 64, false, true>(int, int);
-template SlicedFn sliced_fn<double, 64, true, false>(int, int);
-template SlicedFn sliced_fn<double, 64, true, true>(int, int);
+template SlicedFn sliced_fn<double, 64, 0, false>(int, int);
+template SlicedFn sliced_fn<double, 64, 0, true>(int, int);
+template SlicedFn sliced_fn<double, 64, 1, false>(int, int);
+template SlicedFn sliced_fn<double, 64, 1, true>(int, int);
 }  // namespace kern
 }  // namespace spmv

@@ -45,13 +45,45 @@ __device__ __forceinline__ void load_d16(const int16_t* p, int (&d)[N]) {
   }
 }
 
+// N 8-bit dictionary codes of one lane (N bytes, aligned): one load.
+template <int N>
+__device__ __forceinline__ void load_c8(const uint8_t* p, int (&d)[N]) {
+  if constexpr (N == 1) {
+    unsigned short v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(l2_evict_first()));
+    d[0] = (int)(v & 0xff);
+  } else if constexpr (N == 2) {
+    unsigned short v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(l2_evict_first()));
+    d[0] = (int)(v & 0xff);
+    d[1] = (int)(v >> 8);
+  } else if constexpr (N == 4) {
+    const unsigned v = (unsigned)ld_stream(reinterpret_cast<const int*>(p));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) d[i] = (int)((v >> (8 * i)) & 0xff);
+  } else {
+    const int2 v = ld_stream(reinterpret_cast<const int2*>(p));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      d[i] = (int)(((unsigned)v.x >> (8 * i)) & 0xff);
+      d[4 + i] = (int)(((unsigned)v.y >> (8 * i)) & 0xff);
+    }
+  }
+}
+
+// ENC selects the stored column encoding: 0 int32 columns (pad −1); 1 16-bit
+// offsets d = col − origin − row (pad −32768); 2 8-bit codes into the
+// matrix's offset dictionary (pad 255), decoded through a 256-entry table in
+// shared memory (a stencil's k-th slot holds the same code on most lanes:
+// the lookup is a broadcast). 12 / 10 / 9 bytes per fp64 slot.
 // CARRY selects the batch loop (a launch-tuner knob, SPMV_SLICED_CARRY):
 //  CARRY = 1: batch k+U is loaded under a branch after batch k's FMAs and
 //             carried in registers (fastest on stencils: c2 ELL-16 96 µs);
 //  CARRY = 0: the batch load is unconditional and predicated per k-step
 //             (fastest on scattered gathers: c4 ELL 539 vs 564 µs).
-template <int B, int R, class T, int C, bool D16, bool CARRY>
+template <int B, int R, class T, int C, int ENC, bool CARRY>
 __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const SlicedParams p) {
+  constexpr bool D16 = ENC == 1, D8 = ENC == 2, DOFF = ENC != 0;
   constexpr int RPL = C / 32;                                       // rows per lane
   constexpr int VW = (int)(16 / sizeof(T)) < RPL ? (int)(16 / sizeof(T)) : RPL;  // elems per vector load
   constexpr int NV = RPL / VW;
@@ -67,6 +99,11 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
   // (x, sums_prev) before reading them. No-ops without the launch attribute.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  __shared__ int s_tab[D8 ? 256 : 1];
+  if constexpr (D8) {
+    for (int i = threadIdx.x; i < 256; i += B) s_tab[i] = i < 255 ? p.tab8[i] : 0;
+    __syncthreads();
+  }
   const double alpha = epi_alpha(p.e);
   double yy = 0.0, xy = 0.0;
   // persistent: each warp walks slices warp0, warp0 + nwarps, ... so the
@@ -82,15 +119,16 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
       width = p.ell_K;
       stride = p.ell_stride;
     }
-    const int32_t* __restrict__ cp = D16 ? nullptr : p.col + base + lane * RPL;
+    const int32_t* __restrict__ cp = DOFF ? nullptr : p.col + base + lane * RPL;
     const int16_t* __restrict__ dp = D16 ? p.col16 + base + lane * RPL : nullptr;
+    const uint8_t* __restrict__ bp = D8 ? p.col8 + base + lane * RPL : nullptr;
     const T* __restrict__ vp = val + base + lane * RPL;
     double acc[RPL];
-    int64_t rowv[D16 ? RPL : 1];  // D16: column origin of each of the lane's rows
+    int64_t rowv[DOFF ? RPL : 1];  // 16/8-bit: column origin of each of the lane's rows
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       acc[r] = 0.0;
-      if constexpr (D16) {
+      if constexpr (DOFF) {
         const int64_t ri = slice * C + lane * RPL + r;
         rowv[r] = p.col_origin + (ri < p.rows ? (p.perm ? (int64_t)p.perm[ri] : ri) : 0);
       }
@@ -107,7 +145,7 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
           int tc[VW];
           if (ok) {
             load_vals<T, VW>(vp + (k + u) * stride + q * VW, tv);
-            if constexpr (!D16) load_cols<VW>(cp + (k + u) * stride + q * VW, tc);
+            if constexpr (!DOFF) load_cols<VW>(cp + (k + u) * stride + q * VW, tc);
           } else {
 #pragma unroll
             for (int w = 0; w < VW; ++w) {
@@ -118,7 +156,7 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
 #pragma unroll
           for (int w = 0; w < VW; ++w) {
             v[u][q * VW + w] = tv[w];
-            if constexpr (!D16) c[u][q * VW + w] = tc[w];
+            if constexpr (!DOFF) c[u][q * VW + w] = tc[w];
           }
         }
         if constexpr (D16) {
@@ -131,6 +169,17 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
           }
 #pragma unroll
           for (int r = 0; r < RPL; ++r) c[u][r] = dd[r] == -32768 ? -1 : (int)(rowv[r] + dd[r]);
+        }
+        if constexpr (D8) {
+          int dd[RPL];
+          if (ok) {
+            load_c8<RPL>(bp + (k + u) * stride, dd);
+          } else {
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) dd[r] = 255;
+          }
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) c[u][r] = dd[r] == 255 ? -1 : (int)(rowv[r] + s_tab[dd[r]]);
         }
       }
     };
@@ -183,9 +232,9 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
 }
 
 
-#define SL_ROW(B) {&k_sliced<B, 32, T, C, D16, CARRY>, &k_sliced<B, 64, T, C, D16, CARRY>, \
-                   &k_sliced<B, 128, T, C, D16, CARRY>, &k_sliced<B, 255, T, C, D16, CARRY>}
-template <class T, int C, bool D16, bool CARRY>
+#define SL_ROW(B) {&k_sliced<B, 32, T, C, ENC, CARRY>, &k_sliced<B, 64, T, C, ENC, CARRY>, \
+                   &k_sliced<B, 128, T, C, ENC, CARRY>, &k_sliced<B, 255, T, C, ENC, CARRY>}
+template <class T, int C, int ENC, bool CARRY>
 SlicedFn sliced_fn(int bi, int ri) {
   static const SlicedFn tab[5][4] = {SL_ROW(64), SL_ROW(128), SL_ROW(256), SL_ROW(512), SL_ROW(1024)};
   return tab[bi][ri];

@@ -8,13 +8,11 @@ template <class T>
 void launch_sliced(spmv_matrix* h, kern::SlicedParams& p, int C, const spmv_launch_t& L) {
   const int bi = block_index(L.block), ri = reg_index(L.maxreg);
   const void* fn;
-  const bool d16 = p.col16 != nullptr;
+  const int enc = p.col8 ? 2 : (p.col16 ? 1 : 0);
   const bool carry = (L.knob & kern::kSlicedCarry) != 0;
-#define SL_PICK(CC)                                                                                         \
-  fn = d16 ? (carry ? (const void*)kern::sliced_fn<T, CC, true, true>(bi, ri)                               \
-                    : (const void*)kern::sliced_fn<T, CC, true, false>(bi, ri))                             \
-           : (carry ? (const void*)kern::sliced_fn<T, CC, false, true>(bi, ri)                              \
-                    : (const void*)kern::sliced_fn<T, CC, false, false>(bi, ri))
+#define SL_ENC(CC, E) (carry ? (const void*)kern::sliced_fn<T, CC, E, true>(bi, ri) \
+                             : (const void*)kern::sliced_fn<T, CC, E, false>(bi, ri))
+#define SL_PICK(CC) fn = enc == 2 ? SL_ENC(CC, 2) : (enc == 1 ? SL_ENC(CC, 1) : SL_ENC(CC, 0))
   switch (C) {
     case 32: SL_PICK(32); break;
     case 64: SL_PICK(64); break;
@@ -23,6 +21,7 @@ void launch_sliced(spmv_matrix* h, kern::SlicedParams& p, int C, const spmv_laun
     default: fail(SPMV_ERR_UNSUPPORTED, "slice height C must be 32, 64, 128 or 256");
   }
 #undef SL_PICK
+#undef SL_ENC
   const LaunchAttrs attrs(fn, L.carveout_pct);
   const int64_t warps_per_block = L.block / 32;
   const int64_t grid = persistent_grid(fn, L.block, (p.nslices + warps_per_block - 1) / warps_per_block);
@@ -57,12 +56,15 @@ void launch_sliced(spmv_matrix* h, kern::SlicedParams& p, int C, const spmv_laun
 }  // namespace
 
 void run_ell_arrays(spmv_matrix* h, const int32_t* col, const void* val, int64_t K, int64_t n_pad,
-                    const Epilogue& e, const void* x, void* y, const spmv_launch_t& L, const int16_t* col16) {
+                    const Epilogue& e, const void* x, void* y, const spmv_launch_t& L, const int16_t* col16,
+                    const uint8_t* col8, const int32_t* tab8) {
   kern::SlicedParams p{};
   const int C = L.knob & 0xffff;
   if (C == 0 || n_pad % C != 0) fail(SPMV_ERR_UNSUPPORTED, "ELL rows-per-warp must divide n_pad (a multiple of 128)");
   p.col = col;
   p.col16 = col16;
+  p.col8 = col8;
+  p.tab8 = tab8;
   p.col_origin = h->col_origin;
   p.val = val;
   p.sp = nullptr;
@@ -79,13 +81,16 @@ void run_ell_arrays(spmv_matrix* h, const int32_t* col, const void* val, int64_t
 }
 
 void run_ell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L) {
-  run_ell_arrays(h, h->ell_col, h->ell_val, h->ell_K, h->ell_npad, e, x, y, L, h->ell_col16);
+  run_ell_arrays(h, h->ell_col, h->ell_val, h->ell_K, h->ell_npad, e, x, y, L, h->ell_col16, h->ell_col8,
+                 h->dict8_tab);
 }
 
 void run_sell(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const spmv_launch_t& L) {
   kern::SlicedParams p{};
   p.col = h->sell_col;
   p.col16 = h->sell_col16;
+  p.col8 = h->sell_col8;
+  p.tab8 = h->dict8_tab;
   p.col_origin = h->col_origin;
   p.val = h->sell_val;
   p.sp = h->sell_sp;

@@ -1,9 +1,12 @@
-"""GPU tests: 16-bit column offsets for ELL/SELL (index16) and the learned
-run-time mode (SPMV_TUNE_PREDICT).
+"""GPU tests: 16-bit column offsets (index16 = 1) and 8-bit dictionary codes
+(index16 = 2) for ELL/SELL, and the learned run-time mode (SPMV_TUNE_PREDICT,
+SURVEY §8(f) f3).
 
-index16 changes only how the column index is STORED (d = col − row, int16,
-pad −32768): decoded, the layouts must equal the oracle's ELL/SELL (O4/O5)
-bit for bit, and every SpMV must pass O9 exactly as the int32 layouts do."""
+index16 changes only how the column index is STORED (d = col − row as int16,
+pad −32768; or the 8-bit code of d in the matrix's dictionary of distinct
+offsets, pad 255): decoded, the layouts must equal the oracle's ELL/SELL
+(O4/O5) bit for bit, and every SpMV must pass O9 exactly as the int32
+layouts do."""
 import numpy as np
 import pytest
 
@@ -26,6 +29,17 @@ def fits16(coo):
     return int(np.abs(d).max()) <= 32767
 
 
+def n_offsets(coo):
+    """Distinct col − row offsets (the 8-bit dictionary fits iff <= 255)."""
+    if coo.row.shape[0] == 0:
+        return 0
+    return int(np.unique(coo.col.astype(np.int64) - coo.row.astype(np.int64)).shape[0])
+
+
+def auto_bytes(coo):
+    return 1 if n_offsets(coo) <= 255 else (2 if fits16(coo) else 4)
+
+
 def create(coo, dtype):
     r, c, v = to_device(coo, dtype)
     return P.spmv_create(coo.rows, coo.cols, r, c, v)
@@ -41,6 +55,74 @@ def fetch(h, which, n, np_dtype):
 def decode(d16, rows_of_slot):
     d = d16.astype(np.int64)
     return np.where(d == -32768, -1, rows_of_slot + d).astype(np.int32)
+
+
+def decode8(c8, tab, rows_of_slot):
+    c = c8.astype(np.int64)
+    return np.where(c == 255, -1, rows_of_slot + tab[np.minimum(c, 254)].astype(np.int64)).astype(np.int32)
+
+
+def sell_rows_of_slot(perm, sp, Cs, rows):
+    out = np.zeros(sp[-1], np.int64)
+    for s_ in range(len(sp) - 1):
+        w = (sp[s_ + 1] - sp[s_]) // Cs
+        for j in range(Cs):
+            q = s_ * Cs + j
+            rr = perm[q] if q < rows else 0
+            out[sp[s_] + np.arange(w) * Cs + j] = rr
+    return out
+
+
+@pytest.mark.parametrize("name", [n for n, c in corpus() if c.rows > 0 and n_offsets(c) <= 255])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_index8_layouts_decode_to_oracle(name, dtype):
+    """8-bit codes: the dictionary holds exactly the matrix's distinct offsets
+    (sorted), the codes decode to the oracle's ELL / SELL columns bit for bit,
+    values are the oracle's, and the SpMV passes O9 for every knob."""
+    coo = CASES[name]
+    h = create(coo, dtype)
+    try:
+        rp, R, C, V = oracle_csr(coo)
+        P.spmv_convert(h, P.FMT_ELL, index16=2)
+        K, n_pad, colE, valE = oracle.ell(coo.rows, rp, C, V)
+        info = P.spmv_format_info(h, P.FMT_ELL)
+        assert info["index_bytes"] == 1 and (info["K"], info["n_pad"]) == (K, n_pad)
+        tab = fetch(h, P.ARR_DICT8_TAB, 256, np.int32)
+        offs = np.unique(coo.col.astype(np.int64) - coo.row.astype(np.int64))
+        assert (tab[: len(offs)] == offs).all()
+        rows_of_slot = np.tile(np.arange(n_pad, dtype=np.int64), K)
+        assert (decode8(fetch(h, P.ARR_ELL_COL8, K * n_pad, np.uint8), tab, rows_of_slot) == colE).all()
+        assert (fetch(h, P.ARR_ELL_VAL, K * n_pad, np.float32 if dtype == "f32" else np.float64)
+                .astype(np.float64) == valE).all()
+        assert info["stored_bytes"] == K * n_pad * (1 + (4 if dtype == "f32" else 8)) + 1024
+        for alpha, beta in [(1.0, 0.0), (2.5, -0.5)]:
+            check_y(h, coo, dtype, P.FMT_ELL, alpha, beta)
+        for knob in [32, 64, 128, 256 | (1 << 16)]:
+            P.spmv_set_launch(h, P.FMT_ELL, 256, 64, -1, knob)
+            check_y(h, coo, dtype, P.FMT_ELL, 2.5, -0.5)
+        for Cs, sigma in ((32, 1), (64, 1), (128, 512), (256, 256)):
+            P.spmv_convert(h, P.FMT_SELL, sell_C=Cs, sell_sigma=sigma, index16=2)
+            perm, sp, colS, valS = oracle.sell(coo.rows, rp, C, V, Cs, sigma)
+            assert P.spmv_format_info(h, P.FMT_SELL)["index_bytes"] == 1
+            ros = sell_rows_of_slot(perm, sp, Cs, coo.rows)
+            assert (decode8(fetch(h, P.ARR_SELL_COL8, sp[-1], np.uint8), tab, ros) == colS).all()
+            check_y(h, coo, dtype, P.FMT_SELL, 2.5, -0.5)
+    finally:
+        P.spmv_destroy(h)
+
+
+def test_index8_rejected_when_dictionary_overflows():
+    coo = si.uniform_k(1 << 12, 16)   # thousands of distinct offsets
+    assert n_offsets(coo) > 255
+    h = create(coo, "f64")
+    try:
+        with pytest.raises(P.SpmvError) as e:
+            P.spmv_convert(h, P.FMT_ELL, index16=2)
+        assert e.value.status == P.ERR_UNSUPPORTED
+        P.spmv_convert(h, P.FMT_ELL, index16=-1)
+        assert P.spmv_format_info(h, P.FMT_ELL)["index_bytes"] == auto_bytes(coo)
+    finally:
+        P.spmv_destroy(h)
 
 
 def check_y(h, coo, dtype, fmt, alpha, beta):
@@ -105,8 +187,8 @@ def test_index16_spmv_parity(name, dtype, fmt, params):
             with pytest.raises(P.SpmvError) as e:
                 P.spmv_convert(h, fmt, index16=1, **params)
             assert e.value.status == P.ERR_UNSUPPORTED
-            P.spmv_convert(h, fmt, index16=-1, **params)     # auto: falls back to int32 columns
-            assert P.spmv_format_info(h, fmt)["index_bytes"] == 4
+            P.spmv_convert(h, fmt, index16=-1, **params)     # auto: 8-bit codes if <= 255 offsets, else int32
+            assert P.spmv_format_info(h, fmt)["index_bytes"] == auto_bytes(coo)
         else:
             P.spmv_convert(h, fmt, index16=1, **params)
             assert P.spmv_format_info(h, fmt)["index_bytes"] == 2
@@ -126,10 +208,14 @@ def test_index16_power_step_and_bytes():
     try:
         P.spmv_convert(h, P.FMT_SELL)
         b32 = P.spmv_format_info(h, P.FMT_SELL)["stored_bytes"]
-        P.spmv_convert(h, P.FMT_SELL, index16=-1)
+        P.spmv_convert(h, P.FMT_SELL, index16=1)
         info = P.spmv_format_info(h, P.FMT_SELL)
         assert info["index_bytes"] == 2
         assert info["stored_bytes"] == b32 - 2 * info["slots"]
+        P.spmv_convert(h, P.FMT_SELL, index16=-1)   # 27 offsets: the 8-bit dictionary
+        info = P.spmv_format_info(h, P.FMT_SELL)
+        assert info["index_bytes"] == 1
+        assert info["stored_bytes"] == b32 - 3 * info["slots"] + 1024
         rp, R, C, V = oracle_csr(coo)
         x = torch.from_numpy(vec(n, 3, "f64")).cuda()
         s0 = torch.zeros(2, dtype=torch.float64, device="cuda")
@@ -149,15 +235,15 @@ def test_index16_power_step_and_bytes():
         P.spmv_destroy(h)
 
 
-def test_tuner_uses_index16_when_it_fits():
+def test_tuner_uses_narrowest_index_that_fits():
     coo = si.stencil27(40, random_values=True)
     h = create(coo, "f64")
     try:
         rep = P.spmv_tune(h, P.TUNE_FORMAT, expected_iterations=100000)
         fmt = rep.format
         if fmt in (P.FMT_ELL, P.FMT_SELL):
-            assert rep.params.index16 == 1
-            assert P.spmv_format_info(h, fmt)["index_bytes"] == 2
+            assert rep.params.index16 == 2     # 27 distinct offsets: 8-bit dictionary codes
+            assert P.spmv_format_info(h, fmt)["index_bytes"] == 1
             check_y(h, coo, "f64", fmt, 1.0, 0.0)
     finally:
         P.spmv_destroy(h)
@@ -196,6 +282,33 @@ def test_predict_mode(case):
         rep2 = P.spmv_tune(h2, P.TUNE_FORMAT | P.TUNE_PREDICT, expected_iterations=0)
         assert rep2.format == P.FMT_CSR and rep2.converted == 0
         P.spmv_destroy(h2)
+    finally:
+        P.spmv_destroy(h)
+
+
+@pytest.mark.parametrize("case", ["stencil27_40", "rmat14"])
+def test_predict_decide_only(case):
+    """SPMV_TUNE_DECIDE_ONLY reports the PREDICT verdict without converting;
+    the t_CSR it gates on comes from a row sample scaled to nnz (the whole
+    matrix below 2^26 entries)."""
+    coo = {"stencil27_40": lambda: si.stencil27(40, random_values=True),
+           "rmat14": lambda: si.rmat(14, 16, dtype=np.float64)}[case]()
+    h = create(coo, "f64")
+    try:
+        feats = P.spmv_features(h)
+        pred = P.spmv_predict(feats)
+        rep = P.spmv_tune(h, P.TUNE_FORMAT | P.TUNE_PREDICT | P.TUNE_DECIDE_ONLY, expected_iterations=10 ** 7)
+        assert P.spmv_get_format(h) == P.FMT_CSR          # nothing converted
+        rec = [r for r in P.spmv_decision_log(h) if r.get("kind") == "format_predict"][-1]
+        assert rec["t_csr_sample_nnz"] == coo.nnz
+        if rec["gate"]["convert"]:
+            assert rep.converted == 1 and rep.format == pred["format"]
+        else:
+            assert rep.converted == 0 and rep.format == P.FMT_CSR
+        with pytest.raises(P.SpmvError):
+            P.spmv_tune(h, P.TUNE_FORMAT | P.TUNE_DECIDE_ONLY, 100)          # needs PREDICT
+        with pytest.raises(P.SpmvError):
+            P.spmv_tune(h, P.TUNE_ALL | P.TUNE_PREDICT | P.TUNE_DECIDE_ONLY, 100)  # not with LAUNCH
     finally:
         P.spmv_destroy(h)
 

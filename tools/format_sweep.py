@@ -26,10 +26,12 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
 VARIANTS = [("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)),
             ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE)),
             ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM)),
-            ("ELL", P.FMT_ELL, {}),
+            ("ELL", P.FMT_ELL, dict(index16=0)),
             ("ELL-16", P.FMT_ELL, dict(index16=1)),
-            ("SELL", P.FMT_SELL, {}),
+            ("ELL-8", P.FMT_ELL, dict(index16=2)),
+            ("SELL", P.FMT_SELL, dict(index16=0)),
             ("SELL-16", P.FMT_SELL, dict(index16=1)),
+            ("SELL-8", P.FMT_SELL, dict(index16=2)),
             ("SELL-sigma", P.FMT_SELL, dict(sell_sigma=-1)),
             ("HYB", P.FMT_HYB, {}),
             ("COO", P.FMT_COO, {}),

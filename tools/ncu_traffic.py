@@ -29,8 +29,8 @@ METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.
 
 # label -> kernel_one arguments
 LABELS = {
-    "ELL": ["ELL", "--index16", "0"], "ELL-16": ["ELL", "--index16", "1"],
-    "SELL": ["SELL", "--index16", "0"], "SELL-16": ["SELL", "--index16", "1"],
+    "ELL": ["ELL", "--index16", "0"], "ELL-16": ["ELL", "--index16", "1"], "ELL-8": ["ELL", "--index16", "2"],
+    "SELL": ["SELL", "--index16", "0"], "SELL-16": ["SELL", "--index16", "1"], "SELL-8": ["SELL", "--index16", "2"],
     "CSR-vector": ["CSR", "--csr-alg", "2"], "CSR-merge": ["CSR", "--csr-alg", "3"],
     "CSR-stream": ["CSR", "--csr-alg", "4"], "COO": ["COO"], "HYB": ["HYB"],
     "BELL-2": ["BELL", "--bell-b", "2"], "BELL-3": ["BELL", "--bell-b", "3"],
