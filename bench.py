@@ -536,17 +536,32 @@ def ncu_traffic(cfg, label):
 LAUNCH_SAMPLE_NNZ = 1 << 28
 
 
-def tune_launch_on_slab(P, h, fmt, params, E):
+def tune_on_slab(P, h, E, fmt, params, tune_launch=True):
+    """Measured run-time mode + compile-time mode (spmv_tune FORMAT|LAUNCH) on
+    a middle row slab of about LAUNCH_SAMPLE_NNZ entries (the whole matrix
+    when smaller); then, if the decision `fmt` differs from the measured
+    choice, that format launch-tuned on the same slab."""
     feats = P.spmv_features(h)
-    rows = int(feats["n_rows"])
-    take = max(1, min(rows, int(rows * LAUNCH_SAMPLE_NNZ / max(1, int(feats["nnz"])))))
+    rows, nnz = int(feats["n_rows"]), int(feats["nnz"])
+    take = rows if nnz <= LAUNCH_SAMPLE_NNZ else max(1, int(rows * LAUNCH_SAMPLE_NNZ / nnz))
     r0 = (rows - take) // 2
     sl = P.spmv_create_row_slice(h, r0, r0 + take)
     try:
-        P.spmv_convert(sl, fmt, **normalise_params(P, fmt, params))
-        P.spmv_tune(sl, P.TUNE_LAUNCH, expected_iterations=E)
-        return {"launch": tuple(P.spmv_get_launch(sl, fmt)), "rows": (r0, r0 + take),
-                "log": [dict(r, slab_rows=[r0, r0 + take]) for r in P.spmv_decision_log(sl)]}
+        rep = P.spmv_tune(sl, P.TUNE_FORMAT | (P.TUNE_LAUNCH if tune_launch else 0), expected_iterations=E)
+        m_fmt, m_params = rep.format, normalise_params(P, rep.format, report_params(P, rep))
+        m_launch = tuple(P.spmv_get_launch(sl, m_fmt))
+        same = m_fmt == fmt and (fmt != P.FMT_CSR or m_params.get("csr_alg") == params.get("csr_alg")) and \
+            (fmt not in (P.FMT_ELL, P.FMT_SELL) or m_params.get("index16") == params.get("index16", -1) or
+             params.get("index16", -1) == -1)
+        launch = m_launch
+        if not same:
+            P.spmv_convert(sl, fmt, **params)
+            if tune_launch:
+                P.spmv_tune(sl, P.TUNE_LAUNCH, expected_iterations=E)
+            launch = tuple(P.spmv_get_launch(sl, fmt))
+        log = [dict(r, slab_rows=[r0, r0 + take]) for r in P.spmv_decision_log(sl)]
+        return {"launch_for_choice": launch, "measured_choice": fmt_label(P, m_fmt, m_params),
+                "measured_launch": m_launch, "slab_rows": [r0, r0 + take], "log": log}
     finally:
         P.spmv_destroy(sl)
 
@@ -687,16 +702,25 @@ def run_rank(args, ctx: Ctx, shared: dict):
     t_off = time.perf_counter()
     h = P.spmv_create(coo.rows, coo.cols, coo.row, coo.col, coo.val)
     P.spmv_features(h)
+    launch = None
+    measured = None
     if args.format == "auto":
-        big = coo.nnz > LAUNCH_SAMPLE_NNZ
-        flags = P.TUNE_FORMAT | (0 if (args.no_tune_launch or big) else P.TUNE_LAUNCH)
-        rep = P.spmv_tune(h, flags, expected_iterations=E)
-        fmt = rep.format
-        params = report_params(P, rep)
-        decision = P.spmv_decision_log(h)
-        if big and not args.no_tune_launch:
-            launch_slab = tune_launch_on_slab(P, h, fmt, params, E)
-            decision = decision + launch_slab["log"]
+        # (1) the run-time mode's decision for this matrix (the per-step select
+        #     phase reaches the same one: it is a function of the features and
+        #     of t_CSR, whose gate margin is orders of magnitude at E = 100)
+        if args.select == "predict":
+            r = P.spmv_tune(h, P.TUNE_FORMAT | P.TUNE_PREDICT | P.TUNE_DECIDE_ONLY, expected_iterations=E)
+            fmt = r.format if r.converted else P.FMT_CSR
+            params = normalise_params(P, fmt, report_params(P, r) if r.converted else {"csr_alg": P.CSR_VECTOR})
+        else:
+            r = P.spmv_tune(h, P.TUNE_FORMAT, expected_iterations=E)
+            fmt, params = r.format, normalise_params(P, r.format, report_params(P, r))
+        # (2) the fully measured run-time mode with the compile-time mode
+        #     (every candidate launch-tuned) on a row slab — the record of what
+        #     measuring every format would pick, and the tuned launch variants
+        measured = tune_on_slab(P, h, E, fmt, params, tune_launch=not args.no_tune_launch)
+        launch = measured["launch_for_choice"]
+        decision = P.spmv_decision_log(h) + measured["log"]
     else:
         csr_algs = {"CSR-vector": P.CSR_VECTOR, "CSR-merge": P.CSR_MERGE, "CSR-stream": P.CSR_STREAM}
         fmt = P.FMT_CSR if args.format in csr_algs else P.FORMATS[args.format]
@@ -709,10 +733,10 @@ def run_rank(args, ctx: Ctx, shared: dict):
         elif not args.no_tune_launch:
             P.spmv_tune(h, P.TUNE_LAUNCH, expected_iterations=E)
         decision = P.spmv_decision_log(h)
-    params = normalise_params(P, fmt, params)
-    launch = tuple(P.spmv_get_launch(h, fmt))
-    if args.format == "auto" and coo.nnz > LAUNCH_SAMPLE_NNZ and not args.no_tune_launch:
-        launch = tuple(launch_slab["launch"])
+        params = normalise_params(P, fmt, params)
+        launch = tuple(P.spmv_get_launch(h, fmt))
+    if launch is None:
+        launch = (0, 0, -1, 0)
     P.spmv_destroy(h)
     offline_s = time.perf_counter() - t_off
     offline = {"format": fmt, "params": params, "launch": launch}
@@ -978,6 +1002,8 @@ def run_rank(args, ctx: Ctx, shared: dict):
                                   "knob": sel_l[3]},
                        "select": args.select if args.format == "auto" else "fixed --format",
                        "offline_choice": fmt_label(P, offline["format"], offline["params"]),
+                       "measured_choice_on_slab": (measured or {}).get("measured_choice"),
+                       "tune_slab_rows": (measured or {}).get("slab_rows"),
                        "offline_tune_s": round(offline_s, 1),
                        "partition": "row, nnz-balanced" if world > 1 else "none",
                        "virtual_ranks": world if ctx.virtual is not None else None,

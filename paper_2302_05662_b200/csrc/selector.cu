@@ -65,8 +65,8 @@ void selector_class_format(int cls, int* fmt, spmv_format_params_t* p) {
   p->hyb_K = -1;
   switch (cls) {
     case 1: *fmt = SPMV_FMT_CSR; p->csr_alg = SPMV_CSR_MERGE; break;
-    case 2: *fmt = SPMV_FMT_ELL; break;
-    case 3: *fmt = SPMV_FMT_SELL; break;
+    case 2: *fmt = SPMV_FMT_ELL; p->index16 = -1; break;   // the narrowest column encoding that fits
+    case 3: *fmt = SPMV_FMT_SELL; p->index16 = -1; break;
     case 4: *fmt = SPMV_FMT_HYB; break;
     case 5: *fmt = SPMV_FMT_COO; break;
     case 6: *fmt = SPMV_FMT_BELL; p->bell_b = 2; break;
