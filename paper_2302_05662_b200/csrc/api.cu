@@ -385,7 +385,8 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
   switch (fmt) {
     case SPMV_FMT_CSR:
       if (h->csr_alg == SPMV_CSR_MERGE)  // per-warp merge walk, or row-interleaved tiles of block·IPT items
-        return {4, 8, 16, kern::kMergeTile | 4, kern::kMergeTile | 8, kern::kMergeTile | 16};
+        return {4, 8, 16, kern::kMergeTile | 4, kern::kMergeTile | 8, kern::kMergeTile | 16,
+                kern::kMergeStream | 4, kern::kMergeStream | 8, kern::kMergeStream | 16};
       if (h->csr_alg == SPMV_CSR_STREAM) return {16, 32, 64};
       {
         int t = csr_default_lanes(h);

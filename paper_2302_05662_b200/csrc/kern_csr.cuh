@@ -523,6 +523,255 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_merge_tile(
   }
 }
 
+// Pipelined merge-path CSR: the merge-path chunks of k_csr_merge_tile, fed
+// by CSR-stream's TMA pipeline. The block is persistent over chunks; one
+// producer warp moves each chunk's contiguous col/val segment [y0, y1) and
+// its row starts rp[x0 .. x1+1] into a two-stage shared-memory ring with
+// cp.async.bulk (16-byte aligned interiors; < 16 B heads/tails by the lanes)
+// while the B consumer threads walk the other stage thread per row
+// (row-interleaved gathers). Rows longer than kLong entries are cut into
+// pieces of kPiece entries that the consumer warps sum with kU gathers in
+// flight per lane (a 150K-entry hub row fills whole chunks: every warp works
+// on it); the pieces of a row are added in piece order (deterministic).
+// Chunk records and the fixup are those of the other merge kernels.
+template <int B, int R, class T, int IPT, class RP>
+__global__ void __launch_bounds__(B + 32) __maxnreg__(regcap(B + 32, R)) k_csr_merge_stream(const CsrParams p) {
+  constexpr int ITEMS = B * IPT;
+  constexpr int NS = kStreamStages;
+  constexpr int NW = B / 32;
+  constexpr int VP = StreamStage<T>::kValPad;
+  constexpr int RPP = MergeStage<T, RP>::kRpPad;
+  constexpr int U = 8;
+  constexpr int kLong = 64, kPiece = 256, kU = 4;
+  constexpr int kMaxPieces = ITEMS / kPiece + ITEMS / kLong + 1;
+  constexpr size_t STAGE = MergeStage<T, RP>::bytes(ITEMS);
+  constexpr size_t COLB = StreamStage<T>::col_bytes(ITEMS);
+  constexpr size_t RPOFF = MergeStage<T, RP>::rp_off(ITEMS);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS];
+  __shared__ int64_t m_x0[NS], m_y0[NS], m_rb[NS];
+  __shared__ int m_nseg[NS], m_nnz[NS], m_in[NS], m_out[NS];
+  __shared__ int s_nlong, s_npiece;
+  __shared__ int s_lrow[ITEMS / kLong + 1], s_lfirst[ITEMS / kLong + 2];
+  __shared__ int s_pa[kMaxPieces], s_pb[kMaxPieces];
+  __shared__ double s_part[kMaxPieces];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) {
+    for (int s = 0; s < NS; ++s) {
+      tma::mbar_init(&full_bar[s], 32);
+      tma::mbar_init(&empty_bar[s], NW);
+    }
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  const RP* __restrict__ rp = static_cast<const RP*>(p.rp);
+  const T* __restrict__ val = static_cast<const T*>(p.val);
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  T* __restrict__ y = static_cast<T*>(p.y);
+  const int64_t nchunks = p.nchunks;
+  if (warp == NW) {
+    // ------------------------------------------------------------ producer
+    const uint64_t pol = tma::policy_evict_first();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      const int64_t x0 = p.coords[2 * c], y0 = p.coords[2 * c + 1];
+      const int64_t x1 = p.coords[2 * c + 2], y1 = p.coords[2 * c + 3];
+      const bool cin = x0 < p.rows && y0 > (int64_t)rp[x0];
+      const bool cout = x1 < p.rows && y1 > (int64_t)rp[x1];
+      const int nseg = (int)(x1 - x0) + (cout ? 1 : 0);
+      // row starts rp[x0 .. x0 + nseg] (nseg + 1 values, all <= rows)
+      const int64_t r0 = x0, r1 = x0 + nseg + 1;
+      tma::mbar_wait(&empty_bar[stage], phase ^ 1);
+      unsigned char* st = smem_raw + (size_t)stage * STAGE;
+      int32_t* s_col = reinterpret_cast<int32_t*>(st);
+      T* s_val = reinterpret_cast<T*>(st + COLB);
+      RP* s_rp = reinterpret_cast<RP*>(st + RPOFF);
+      if (lane == 0) {
+        m_x0[stage] = x0;
+        m_y0[stage] = y0;
+        m_rb[stage] = r0 & ~(int64_t)(RPP - 1);
+        m_nseg[stage] = nseg;
+        m_nnz[stage] = (int)(y1 - y0);
+        m_in[stage] = cin;
+        m_out[stage] = cout;
+      }
+      // aligned interiors by bulk copy, heads/tails (< 16 B) by the lanes
+      const int64_t cb = y0 & ~3LL;
+      int64_t ci0 = (y0 + 3) & ~3LL, ci1 = y1 & ~3LL;
+      if (ci1 <= ci0) ci0 = ci1 = y1;
+      const int64_t vb = y0 & ~(int64_t)(VP - 1);
+      int64_t vi0 = (y0 + VP - 1) & ~(int64_t)(VP - 1), vi1 = y1 & ~(int64_t)(VP - 1);
+      if (vi1 <= vi0) vi0 = vi1 = y1;
+      const int64_t rb = r0 & ~(int64_t)(RPP - 1);
+      int64_t ri0 = (r0 + RPP - 1) & ~(int64_t)(RPP - 1), ri1 = r1 & ~(int64_t)(RPP - 1);
+      if (ri1 <= ri0) ri0 = ri1 = r1;
+      if (lane == 0) {
+        const uint32_t tx = (uint32_t)((ci1 - ci0) * 4 + (vi1 - vi0) * (int64_t)sizeof(T) +
+                                       (ri1 - ri0) * (int64_t)sizeof(RP));
+        if (tx) tma::mbar_expect_tx(&full_bar[stage], tx);
+        if (ci1 > ci0)
+          tma::bulk_g2s(s_col + (ci0 - cb), p.col + ci0, (uint32_t)((ci1 - ci0) * 4), &full_bar[stage], pol);
+        if (vi1 > vi0)
+          tma::bulk_g2s(s_val + (vi0 - vb), val + vi0, (uint32_t)((vi1 - vi0) * sizeof(T)), &full_bar[stage], pol);
+        if (ri1 > ri0)
+          tma::bulk_g2s(s_rp + (ri0 - rb), rp + ri0, (uint32_t)((ri1 - ri0) * sizeof(RP)), &full_bar[stage], pol);
+      }
+      const int ch = (int)(ci0 - y0), ct = (int)(y1 - ci1);
+      if (lane < ch) s_col[y0 + lane - cb] = ld_stream(p.col + y0 + lane);
+      else if (lane >= 16 && lane - 16 < ct) s_col[ci1 + lane - 16 - cb] = ld_stream(p.col + ci1 + lane - 16);
+      const int vh = (int)(vi0 - y0), vt = (int)(y1 - vi1);
+      if (lane < vh) s_val[y0 + lane - vb] = ld_stream(val + y0 + lane);
+      else if (lane >= 16 && lane - 16 < vt) s_val[vi1 + lane - 16 - vb] = ld_stream(val + vi1 + lane - 16);
+      const int rh = (int)(ri0 - r0), rt = (int)(r1 - ri1);
+      if (lane < rh) s_rp[r0 + lane - rb] = rp[r0 + lane];
+      else if (lane >= 16 && lane - 16 < rt) s_rp[ri1 + lane - 16 - rb] = rp[ri1 + lane - 16];
+      tma::mbar_arrive(&full_bar[stage]);
+      if (++stage == NS) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------ consumers
+  const double alpha = epi_alpha(p.e);
+  int stage = 0;
+  uint32_t phase = 0;
+  auto cbar = [] { asm volatile("bar.sync 1, %0;" ::"r"(B) : "memory"); };  // consumer warps only
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    tma::mbar_wait(&full_bar[stage], phase);
+    const unsigned char* st = smem_raw + (size_t)stage * STAGE;
+    const int64_t y0 = m_y0[stage], x0 = m_x0[stage];
+    const int nseg = m_nseg[stage], nnzc = m_nnz[stage];
+    const bool cin = m_in[stage], cout = m_out[stage];
+    const int32_t* s_col = reinterpret_cast<const int32_t*>(st) + (int)(y0 & 3);
+    const T* s_val = reinterpret_cast<const T*>(st + COLB) + (int)(y0 & (VP - 1));
+    const RP* s_rp = reinterpret_cast<const RP*>(st + RPOFF) + (int)(x0 - m_rb[stage]);
+    auto seg_start = [&](int j) {  // row x0 + j's first entry, relative to y0, clamped to the chunk
+      int64_t v = (int64_t)s_rp[j] - y0;
+      return (int)(v < 0 ? 0 : (v > nnzc ? nnzc : v));
+    };
+    auto finish = [&](int j, double acc) {
+      const int64_t row = x0 + j;
+      const bool first = j == 0 && cin, last = j == nseg - 1 && cout;
+      if (first || last) {
+        ChunkRec& rec = p.recs[c];
+        if (first) rec.head = acc;
+        if (last) rec.tail = acc;
+      } else {
+        y[row] = epi_value<T>(p.e, alpha, acc, y, row);
+      }
+    };
+    if (t == 0) s_nlong = 0;
+    cbar();
+    for (int j = t; j < nseg; j += B) {
+      const int a = seg_start(j), len = seg_start(j + 1) - a;
+      if (len > kLong) {
+        s_lrow[atomicAdd(&s_nlong, 1)] = j;
+        continue;
+      }
+      int rot = (len & 7) == 0 && len > 0 ? lane : 0;
+      if (len > 0 && rot >= len) rot %= len;
+      double acc = 0.0;
+      for (int k = 0; k < len; k += U) {
+        int cc[U];
+        T v[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          int i = k + q + rot;
+          i = i >= len ? i - len : i;
+          const bool ok = k + q < len;
+          cc[q] = ok ? s_col[a + i] : 0;
+          v[q] = ok ? s_val[a + i] : T(0);
+        }
+        T xv[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) xv[q] = k + q < len ? ld_x(x + cc[q]) : T(0);
+#pragma unroll
+        for (int q = 0; q < U; ++q) acc = fma((double)v[q], (double)xv[q], acc);
+      }
+      finish(j, acc);
+    }
+    cbar();
+    const int nlong = s_nlong;
+    if (nlong > 0) {
+      if (t == 0) {  // pieces of kPiece entries, rows in ascending order (deterministic)
+        for (int i = 1; i < nlong; ++i) {  // insertion sort of the (few) long rows
+          const int v = s_lrow[i];
+          int q = i - 1;
+          while (q >= 0 && s_lrow[q] > v) {
+            s_lrow[q + 1] = s_lrow[q];
+            --q;
+          }
+          s_lrow[q + 1] = v;
+        }
+        int np = 0;
+        for (int i = 0; i < nlong; ++i) {
+          const int a = seg_start(s_lrow[i]), b = seg_start(s_lrow[i] + 1);
+          s_lfirst[i] = np;
+          for (int q = a; q < b; q += kPiece) {
+            s_pa[np] = q;
+            s_pb[np] = q + kPiece < b ? q + kPiece : b;
+            ++np;
+          }
+        }
+        s_lfirst[nlong] = np;
+        s_npiece = np;
+      }
+      cbar();
+      const int np = s_npiece;
+      for (int q = warp; q < np; q += NW) {
+        const int a = s_pa[q], b = s_pb[q];
+        double acc = 0.0;
+        for (int k = a + lane; k < b; k += 32 * kU) {
+          T v[kU], xv[kU];
+          int cc[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int i = k + 32 * u;
+            cc[u] = i < b ? s_col[i] : 0;
+            v[u] = i < b ? s_val[i] : T(0);
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) xv[u] = k + 32 * u < b ? ld_x(x + cc[u]) : T(0);
+#pragma unroll
+          for (int u = 0; u < kU; ++u) acc = fma((double)v[u], (double)xv[u], acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) s_part[q] = acc;
+      }
+      cbar();
+      for (int i = t; i < nlong; i += B) {
+        double acc = 0.0;
+        for (int q = s_lfirst[i]; q < s_lfirst[i + 1]; ++q) acc += s_part[q];
+        finish(s_lrow[i], acc);
+      }
+    }
+    if (t == 0) {
+      ChunkRec& rec = p.recs[c];
+      rec.first_row = (int32_t)x0;
+      rec.cont_in = cin;
+      const int64_t x1 = x0 + nseg - (cout ? 1 : 0);
+      rec.last_row = (int32_t)(cout ? x1 : (x1 - 1 > x0 ? x1 - 1 : x0));
+      rec.cont_out = cout;
+    }
+    // every consumer warp is done with this stage (incl. the long pieces)
+    __syncwarp();
+    if (lane == 0) tma::mbar_arrive(&empty_bar[stage]);
+    if (++stage == NS) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+}
+
+template <int B, int R, class T, int I, class RP>
+constexpr CsrFn merge_stream_ptr() {
+  if constexpr (B + 32 > 1024 || merge_stream_smem<T, RP>(B, I) > 200 * 1024) return nullptr;
+  else return &k_csr_merge_stream<B, R, T, I, RP>;
+}
+
 template <int B, int R, class T, int I, class RP>
 constexpr CsrFn merge_tile_ptr() {
   if constexpr (merge_tile_smem<T>(B, I) > 200 * 1024) return nullptr;
@@ -571,6 +820,16 @@ CsrFn csr_stream_fn(int bi, int ri) {
 }
 #undef CSRS_TAB
 #undef CSRS_ROW
+
+#define CSRMS_ROW(B, I) {merge_stream_ptr<B, 32, T, I, RP>(), merge_stream_ptr<B, 64, T, I, RP>(), \
+                         merge_stream_ptr<B, 128, T, I, RP>(), merge_stream_ptr<B, 255, T, I, RP>()}
+template <class T, class RP, int I>
+CsrFn csr_merge_stream_fn(int bi, int ri) {
+  static const CsrFn tab[5][4] = {CSRMS_ROW(64, I), CSRMS_ROW(128, I), CSRMS_ROW(256, I), CSRMS_ROW(512, I),
+                                  CSRMS_ROW(1024, I)};
+  return tab[bi][ri];
+}
+#undef CSRMS_ROW
 
 #define CSRMT_ROW(B, I) {merge_tile_ptr<B, 32, T, I, RP>(), merge_tile_ptr<B, 64, T, I, RP>(), \
                          merge_tile_ptr<B, 128, T, I, RP>(), merge_tile_ptr<B, 255, T, I, RP>()}

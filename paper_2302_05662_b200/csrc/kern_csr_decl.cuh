@@ -65,6 +65,24 @@ constexpr size_t merge_tile_smem(int block, int ipt) {
   // col + value of up to block·IPT entries, then up to block·IPT + 2 row starts
   return (size_t)block * ipt * (4 + sizeof(T)) + ((size_t)block * ipt + 2) * 4 + 16;
 }
+// Pipelined merge-path (k_csr_merge_stream): knob kMergeStream | IPT; B
+// consumer threads + one TMA producer warp, two stages of B·IPT merge items.
+constexpr int kMergeStream = 0x200;
+template <class T, class RP, int IPT>
+CsrFn csr_merge_stream_fn(int bi, int ri);
+template <class T, class RP>
+struct MergeStage {
+  // col + val (StreamStage layout), then row starts (RP, 16-byte slack on both ends)
+  static constexpr int kRpPad = 16 / (int)sizeof(RP);
+  __host__ __device__ static constexpr size_t rp_off(int items) { return StreamStage<T>::bytes(items); }
+  __host__ __device__ static constexpr size_t bytes(int items) {
+    return rp_off(items) + ((size_t)(items + 2 + 2 * kRpPad) * sizeof(RP) + 15) / 16 * 16;
+  }
+};
+template <class T, class RP>
+constexpr size_t merge_stream_smem(int block, int ipt) {
+  return (size_t)kStreamStages * MergeStage<T, RP>::bytes(block * ipt);
+}
 // Merge-path partition pre-pass: coords[2c], coords[2c+1] = start of chunk c.
 void merge_partition(const void* rp, bool rp64, int64_t rows, int64_t nnz, int64_t items_per_chunk,
                      int64_t nchunks, int64_t* coords, cudaStream_t s);

@@ -68,23 +68,29 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
     return;
   }
-  const bool tile = (L.knob & kern::kMergeTile) != 0;
+  const bool tile = (L.knob & kern::kMergeTile) != 0, pipe = (L.knob & kern::kMergeStream) != 0;
   const int ipt = L.knob & 0xff;
+  if (tile && pipe) fail(SPMV_ERR_INVALID_ARG, "merge-path knob: kMergeTile and kMergeStream are exclusive");
   const void* fn;
+#define MERGE_PICK(I)                                                              \
+  fn = pipe ? (const void*)kern::csr_merge_stream_fn<T, RP, I>(bi, ri)            \
+            : (tile ? (const void*)kern::csr_merge_tile_fn<T, RP, I>(bi, ri)      \
+                    : (const void*)kern::csr_merge_fn<T, RP, I>(bi, ri))
   switch (ipt) {
-    case 4: fn = tile ? (const void*)kern::csr_merge_tile_fn<T, RP, 4>(bi, ri)
-                      : (const void*)kern::csr_merge_fn<T, RP, 4>(bi, ri); break;
-    case 8: fn = tile ? (const void*)kern::csr_merge_tile_fn<T, RP, 8>(bi, ri)
-                      : (const void*)kern::csr_merge_fn<T, RP, 8>(bi, ri); break;
-    case 16: fn = tile ? (const void*)kern::csr_merge_tile_fn<T, RP, 16>(bi, ri)
-                       : (const void*)kern::csr_merge_fn<T, RP, 16>(bi, ri); break;
-    default: fail(SPMV_ERR_INVALID_ARG, "merge-path items per thread must be 4, 8 or 16 (or kMergeTile | 4, 8, 16)");
+    case 4: MERGE_PICK(4); break;
+    case 8: MERGE_PICK(8); break;
+    case 16: MERGE_PICK(16); break;
+    default: fail(SPMV_ERR_INVALID_ARG, "merge-path items per thread must be 4, 8 or 16 (| kMergeTile or kMergeStream)");
   }
-  if (!fn) fail(SPMV_ERR_UNSUPPORTED, "merge-path tile: block × items per thread exceeds shared memory");
-  const size_t smem = tile ? kern::merge_tile_smem<T>(L.block, ipt) : kern::merge_smem_bytes<T>(L.block, ipt);
+#undef MERGE_PICK
+  if (!fn) fail(SPMV_ERR_UNSUPPORTED, "merge-path tile: block (+ producer warp) × items exceeds the block or shared memory");
+  if (pipe && (((uintptr_t)h->col | (uintptr_t)h->val | (uintptr_t)h->row_ptr) & 15))
+    fail(SPMV_ERR_UNSUPPORTED, "merge-path stream: row_ptr/col/val must be 16-byte aligned for the bulk copies");
+  const size_t smem = pipe ? kern::merge_stream_smem<T, RP>(L.block, ipt)
+                           : (tile ? kern::merge_tile_smem<T>(L.block, ipt) : kern::merge_smem_bytes<T>(L.block, ipt));
   const LaunchAttrs attrs(fn, L.carveout_pct, smem);
   const int64_t total = h->rows + h->nnz;
-  const int64_t items = tile ? (int64_t)L.block * ipt : 32LL * ipt;
+  const int64_t items = (tile || pipe) ? (int64_t)L.block * ipt : 32LL * ipt;
   const int64_t nchunks = (total + items - 1) / items;
   if (nchunks <= 0) return;
   p.recs = static_cast<ChunkRec*>(ensure_seg_scratch(h, (size_t)nchunks * sizeof(ChunkRec)));
@@ -101,9 +107,11 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
   p.nchunks = nchunks;
   // mode 1 (power step): alpha from device, beta = 0; the norms are computed
   // afterwards by run_norms because boundary rows finish in the fixup.
-  const int64_t grid = tile ? nchunks : (nchunks * 32 + L.block - 1) / L.block;
+  const int64_t grid = pipe ? persistent_grid(fn, L.block + 32, nchunks, smem)
+                            : (tile ? nchunks : (nchunks * 32 + L.block - 1) / L.block);
+  const int threads = pipe ? L.block + 32 : L.block;
   void* args[] = {&p};
-  launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, smem, h->stream);
+  launch_checked(fn, dim3((unsigned)grid), dim3(threads), args, smem, h->stream);
   run_seg_fixup(h, p.recs, nchunks, e, y);
 }
 

@@ -246,7 +246,7 @@ def test_spmv_parity(name, dtype, fname, fmt, params):
 
 @pytest.mark.parametrize("fname,fmt,params,knobs", [
     ("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR), [1, 2, 4, 8, 16, 32]),
-    ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), [4, 8, 16, 0x104, 0x108, 0x110]),
+    ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), [4, 8, 16, 0x104, 0x108, 0x110, 0x204, 0x208, 0x210]),
     ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM), [16, 32, 64]),
     ("ELL", P.FMT_ELL, {}, [32, 64, 128, 64 | (1 << 16), 256 | (1 << 16)]),
     ("SELL", P.FMT_SELL, {}, [0, 64, 64 | (1 << 16)]),
@@ -302,31 +302,33 @@ def test_csr_stream_tma_all_launches(case, dtype):
 
 @pytest.mark.parametrize("case", ["mixed_tiles", "long_rows", "rmat10", "stencil27_9", "ragged_empty"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("fmt", [P.FMT_COO, P.FMT_HYB, "merge"])
+@pytest.mark.parametrize("fmt", [P.FMT_COO, P.FMT_HYB, "merge", "merge-stream"])
 def test_coo_tile_all_launches(case, dtype, fmt):
     """Row-interleaved COO tiles (knob 0x100 | EPT) over every block size and
     tile depth: rows crossing tiles (fixup records), rows longer than the
     thread pass takes (warp-cooperative pass), empty rows, the ragged last
     tile; plain COO, the HYB tail (accumulate mode) and merge-path CSR tiles
-    (block·IPT merge items, empty rows written by the tile): O9 parity and
-    NaN y with beta = 0."""
+    (block·IPT merge items, empty rows written by the tile), also fed by the
+    TMA producer warp (0x200 | IPT, two-stage ring, long rows cut into pieces
+    summed by all consumer warps): O9 parity and NaN y with beta = 0."""
     coo = CASES[case]
     h = create(coo, dtype)
     try:
         ref = oracle_csr(coo)
-        if fmt == "merge":
+        flag = 0x200 if fmt == "merge-stream" else 0x100
+        if fmt in ("merge", "merge-stream"):
             fmt = P.FMT_CSR
             P.spmv_convert(h, fmt, csr_alg=P.CSR_MERGE)
         else:
             P.spmv_convert(h, fmt)
         for block in (64, 128, 256, 512, 1024):
             for ept in (4, 8, 16):
-                P.spmv_set_launch(h, fmt, block, 255 if block <= 256 else 64, -1, 0x100 | ept)
+                P.spmv_set_launch(h, fmt, block, 255 if block <= 256 else 64, -1, flag | ept)
                 try:
                     check_y(h, coo, dtype, fmt, 2.5, -0.5, ref)
                     check_y(h, coo, dtype, fmt, 1.0, 0.0, ref, nan_y=True)
-                except P.SpmvError as ex:   # tile over the shared-memory cap
-                    assert ex.status == P.ERR_UNSUPPORTED and block * ept >= 8192
+                except P.SpmvError as ex:   # tile over the shared-memory cap / block + producer warp > 1024
+                    assert ex.status == P.ERR_UNSUPPORTED and (block * ept >= 4096 or block == 1024)
                     torch.cuda.synchronize()
     finally:
         P.spmv_destroy(h)
