@@ -751,7 +751,7 @@ def run_rank(args, ctx: Ctx, shared: dict):
     plan_flags = 0
     for f in (args.plan or "").split(","):
         plan_flags |= {"overlap": P.PLAN_OVERLAP, "halo": P.PLAN_HALO}.get(f.strip(), 0)
-    state = {"kms": [], "time_kernels": False, "phase_events": None, "selected": None}
+    state = {"kms": [], "time_kernels": False, "phase_events": None, "host_marks": None, "selected": None}
 
     class _C:  # native_power_iteration expects an object with .comm
         def __init__(self, c):
@@ -785,11 +785,14 @@ def run_rank(args, ctx: Ctx, shared: dict):
     ev_names = ["create", "features", "select", "convert", "power", "destroy"]
 
     def ev_mark():
-        # CUDA events at phase boundaries on the stream (no synchronisation)
+        # CUDA events at phase boundaries on the stream (no synchronisation),
+        # plus the host clock at the same points (host-side stalls show up as
+        # host phase time the device phases do not have)
         if state["phase_events"] is not None:
             e = torch.cuda.Event(enable_timing=True)
             e.record(stream)
             state["phase_events"][-1].append(e)
+            state["host_marks"][-1].append(time.perf_counter())
 
     def select(h):
         """a7 run-time mode for this matrix: (format, params, launch)."""
@@ -805,6 +808,7 @@ def run_rank(args, ctx: Ctx, shared: dict):
     def one_step(coo_in, want_info=False):
         if state["phase_events"] is not None:
             state["phase_events"].append([])
+            state["host_marks"].append([])
         ev_mark()
         h = P.spmv_create(coo_in.rows, coo_in.cols, coo_in.row, coo_in.col, coo_in.val)
         ev_mark()
@@ -837,6 +841,7 @@ def run_rank(args, ctx: Ctx, shared: dict):
     state["time_kernels"] = not os.environ.get("BENCH_NO_KEVENTS")
     state["kms"] = []
     state["phase_events"] = []
+    state["host_marks"] = []
     l0 = P.launch_count()
     energy.start_sampler()
     e_j0 = energy.read_j()
@@ -868,10 +873,18 @@ def run_rank(args, ctx: Ctx, shared: dict):
     phase_ms = {}
     pe = state["phase_events"] or []
     state["phase_events"] = None
+    host_phase_ms = {}
+    hm = state["host_marks"] or []
     for i, name in enumerate(ev_names):
         vals = [st[i].elapsed_time(st[i + 1]) for st in pe[: args.steps] if len(st) > i + 1]
         if vals:
             phase_ms[name] = round(statistics.median(vals), 4)
+        hv = [(st[i + 1] - st[i]) * 1e3 for st in hm[: args.steps] if len(st) > i + 1]
+        if hv:
+            host_phase_ms[name] = round(statistics.median(hv), 3)
+    gaps = [(hm[k + 1][0] - hm[k][-1]) * 1e3 for k in range(min(len(hm), args.steps) - 1) if hm[k] and hm[k + 1]]
+    if gaps:
+        host_phase_ms["between_steps"] = round(statistics.median(gaps), 3)
     ms_max = ctx.reduce(ms, "max")
     nnz_total = ctx.reduce(float(nnz_local), "sum")
     flops = 2.0 * nnz_total * E * args.steps
@@ -1021,6 +1034,7 @@ def run_rank(args, ctx: Ctx, shared: dict):
                          "peak_source": peak_kind, "frac_of_8TBs": round(achieved / 8000.0, 4)},
             "hbm_gbs": round(achieved, 1),
             "step_phases_ms": phase_ms,
+            "host_phases_ms": host_phase_ms,
             "mflops_per_w": round(mflops_w, 1) if mflops_w else None,
             "energy": energy_rec,
             "cpu_baseline": None,

@@ -43,7 +43,12 @@ __global__ void k_dict_flags(const RP* __restrict__ rp, const int32_t* __restric
                              int64_t origin, int64_t m, int64_t* __restrict__ flags) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride)
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) flags[(int64_t)col[k] - origin - i + m] = 1;
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      // read before write: a banded matrix hits the same few dozen flags from
+      // every thread; stores to one address serialise in L2, cached reads do not
+      int64_t* f = flags + ((int64_t)col[k] - origin - i + m);
+      if (*f == 0) *f = 1;
+    }
 }
 __global__ void k_dict_build(const int64_t* __restrict__ flags, const int64_t* __restrict__ codes, int64_t bins,
                              int64_t m, uint8_t* __restrict__ map, int32_t* __restrict__ tab) {
