@@ -885,6 +885,9 @@ def run_rank(args, ctx: Ctx, shared: dict):
     gaps = [(hm[k + 1][0] - hm[k][-1]) * 1e3 for k in range(min(len(hm), args.steps) - 1) if hm[k] and hm[k + 1]]
     if gaps:
         host_phase_ms["between_steps"] = round(statistics.median(gaps), 3)
+    # every timed step's device time and the device gaps between steps
+    steps_ms = [round(st[0].elapsed_time(st[-1]), 3) for st in pe[: args.steps] if len(st) > 1]
+    dev_gaps = [round(pe[k][-1].elapsed_time(pe[k + 1][0]), 3) for k in range(min(len(pe), args.steps) - 1)]
     ms_max = ctx.reduce(ms, "max")
     nnz_total = ctx.reduce(float(nnz_local), "sum")
     flops = 2.0 * nnz_total * E * args.steps
@@ -1035,6 +1038,7 @@ def run_rank(args, ctx: Ctx, shared: dict):
             "hbm_gbs": round(achieved, 1),
             "step_phases_ms": phase_ms,
             "host_phases_ms": host_phase_ms,
+            "steps_ms": steps_ms, "device_gaps_ms": dev_gaps,
             "mflops_per_w": round(mflops_w, 1) if mflops_w else None,
             "energy": energy_rec,
             "cpu_baseline": None,

@@ -41,14 +41,32 @@ __device__ __forceinline__ IDX pad_col() {
 template <class RP>
 __global__ void k_dict_flags(const RP* __restrict__ rp, const int32_t* __restrict__ col, int64_t rows,
                              int64_t origin, int64_t m, int64_t* __restrict__ flags) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride)
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
-      // read before write: a banded matrix hits the same few dozen flags from
-      // every thread; stores to one address serialise in L2, cached reads do not
-      int64_t* f = flags + ((int64_t)col[k] - origin - i + m);
-      if (*f == 0) *f = 1;
+  // warp per 32 consecutive rows: their entries are one contiguous range, read
+  // coalesced; the row of an entry is found among the 32 row starts the lanes
+  // hold (binary search over shuffles)
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r0 = w0 * 32; r0 < rows; r0 += nw * 32) {
+    const int64_t my = r0 + lane < rows ? (int64_t)rp[r0 + lane] : (int64_t)rp[rows];
+    const int64_t end = (int64_t)rp[r0 + 32 < rows ? r0 + 32 : rows];
+    const int64_t beg = __shfl_sync(0xffffffffu, my, 0);
+    for (int64_t k0 = beg; k0 < end; k0 += 32) {
+      const int64_t k = k0 + lane;
+      int lo = 0;  // largest j with start_j <= k (rows without entries share a start: the last one wins)
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int64_t sj = __shfl_sync(0xffffffffu, my, lo + step);
+        if (sj <= k) lo += step;
+      }
+      if (k < end) {
+        // read before write: a banded matrix hits the same few dozen flags from
+        // every warp; stores to one address serialise in L2, cached reads do not
+        int64_t* f = flags + ((int64_t)col[k] - origin - (r0 + lo) + m);
+        if (*f == 0) *f = 1;
+      }
     }
+  }
 }
 __global__ void k_dict_build(const int64_t* __restrict__ flags, const int64_t* __restrict__ codes, int64_t bins,
                              int64_t m, uint8_t* __restrict__ map, int32_t* __restrict__ tab) {
@@ -614,7 +632,7 @@ int dict8_codes(spmv_matrix* h) {
   int64_t* flags = sc.get<int64_t>(bins);
   int64_t* codes = sc.get<int64_t>(bins + 1);
   CK(cudaMemsetAsync(flags, 0, (size_t)bins * sizeof(int64_t), s));
-  const unsigned g = grid_for(h->rows, 256);
+  const unsigned g = grid_for((h->rows + 31) / 32 * 32, 256, (int64_t)kNumSMs * 8);
   if (h->rows > 0) {
     if (h->rp64)
       LAUNCH(k_dict_flags<int64_t>, g, 256, 0, s, static_cast<const int64_t*>(h->row_ptr), h->col, h->rows,
