@@ -566,6 +566,44 @@ def tune_on_slab(P, h, E, fmt, params, tune_launch=True):
         P.spmv_destroy(sl)
 
 
+def refine_on_full(P, h, fmt, params, log, launch, tdt, k=4):
+    """The k fastest launch variants of the slab sweep of `fmt`, timed on the
+    whole matrix (3 plain SpMVs each after one warm-up): the slab ranks the
+    variants, the whole matrix decides among the close ones (x-gather L1
+    reuse depends on how many consecutive rows a block covers, which a slab
+    reproduces only approximately)."""
+    import torch
+    sweeps = [r for r in log if r.get("kind") == "launch_sweep" and r.get("format") == P.FORMAT_NAMES[fmt]]
+    if not sweeps:
+        return launch, None
+    var = sorted((v for v in sweeps[-1].get("variants", []) if len(v) >= 5), key=lambda v: v[4])
+    cands = [tuple(launch)] + [tuple(int(q) for q in v[:4]) for v in var[: k] if tuple(int(q) for q in v[:4]) != tuple(launch)]
+    P.spmv_convert(h, fmt, **params)
+    feats = P.spmv_features(h)
+    xs = torch.ones(int(feats["n_cols"]), dtype=tdt, device="cuda")
+    ys = torch.empty(int(feats["n_rows"]), dtype=tdt, device="cuda")
+    s = torch.cuda.current_stream()
+    res = []
+    for L in cands:
+        try:
+            P.spmv_set_launch(h, fmt, *L)
+            P.spmv_run(h, 1.0, xs, 0.0, ys, fmt=fmt)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(3):
+                P.spmv_run(h, 1.0, xs, 0.0, ys, fmt=fmt)
+            e1.record(s)
+            torch.cuda.synchronize()
+            res.append((e0.elapsed_time(e1) / 3, L))
+        except P.SpmvError:
+            torch.cuda.synchronize()
+    del xs, ys
+    if not res:
+        return launch, None
+    best = min(res)
+    return best[1], [{"launch": list(L), "ms": round(t, 4)} for t, L in res]
+
+
 def time_plain(P, h, fmt, x, y, min_ms=200.0):
     """Median of 5 batches of back-to-back plain SpMVs (alpha=1, beta=0) with
     CUDA events on the current stream; each batch >= min_ms/5."""
@@ -721,6 +759,9 @@ def run_rank(args, ctx: Ctx, shared: dict):
         measured = tune_on_slab(P, h, E, fmt, params, tune_launch=not args.no_tune_launch)
         launch = measured["launch_for_choice"]
         decision = P.spmv_decision_log(h) + measured["log"]
+        if measured["slab_rows"][1] - measured["slab_rows"][0] < int(coo.rows) and not args.no_tune_launch:
+            # (3) the slab's best few variants re-timed on the whole matrix
+            launch, measured["refine"] = refine_on_full(P, h, fmt, params, measured["log"], launch, tdt)
     else:
         csr_algs = {"CSR-vector": P.CSR_VECTOR, "CSR-merge": P.CSR_MERGE, "CSR-stream": P.CSR_STREAM}
         fmt = P.FMT_CSR if args.format in csr_algs else P.FORMATS[args.format]
@@ -1020,6 +1061,7 @@ def run_rank(args, ctx: Ctx, shared: dict):
                        "offline_choice": fmt_label(P, offline["format"], offline["params"]),
                        "measured_choice_on_slab": (measured or {}).get("measured_choice"),
                        "tune_slab_rows": (measured or {}).get("slab_rows"),
+                       "launch_refined_on_full": (measured or {}).get("refine"),
                        "offline_tune_s": round(offline_s, 1),
                        "partition": "row, nnz-balanced" if world > 1 else "none",
                        "virtual_ranks": world if ctx.virtual is not None else None,
