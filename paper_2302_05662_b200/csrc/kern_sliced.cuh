@@ -83,11 +83,14 @@ __device__ __forceinline__ void load_c8(const uint8_t* p, int (&d)[N]) {
 //             (fastest on scattered gathers: c4 ELL 539 vs 564 µs).
 template <int B, int R, class T, int C, int ENC, bool CARRY>
 __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const SlicedParams p) {
-  constexpr bool D16 = ENC == 1, D8 = ENC == 2, DOFF = ENC != 0;
+  // ENC 3 = 8-bit codes with twice the k-steps per batch (more loads in
+  // flight: a 9-byte slot carries 25 % fewer bytes than a 12-byte one)
+  constexpr bool D16 = ENC == 1, D8 = ENC >= 2, DOFF = ENC != 0;
+  constexpr int UX = ENC == 3 ? 2 : 1;
   constexpr int RPL = C / 32;                                       // rows per lane
   constexpr int VW = (int)(16 / sizeof(T)) < RPL ? (int)(16 / sizeof(T)) : RPL;  // elems per vector load
   constexpr int NV = RPL / VW;
-  constexpr int U = RPL >= 8 ? 1 : 8 / RPL;                         // k-unroll (loads in flight)
+  constexpr int U = (RPL >= 8 ? 1 : 8 / RPL) * UX;                  // k-unroll (loads in flight)
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * (B / 32);
@@ -124,13 +127,13 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
     const uint8_t* __restrict__ bp = D8 ? p.col8 + base + lane * RPL : nullptr;
     const T* __restrict__ vp = val + base + lane * RPL;
     double acc[RPL];
-    int64_t rowv[DOFF ? RPL : 1];  // 16/8-bit: column origin of each of the lane's rows
+    int rowv[DOFF ? RPL : 1];  // 16/8-bit: column origin of each of the lane's rows (< 2^31)
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       acc[r] = 0.0;
       if constexpr (DOFF) {
         const int64_t ri = slice * C + lane * RPL + r;
-        rowv[r] = p.col_origin + (ri < p.rows ? (p.perm ? (int64_t)p.perm[ri] : ri) : 0);
+        rowv[r] = (int)(p.col_origin + (ri < p.rows ? (p.perm ? (int64_t)p.perm[ri] : ri) : 0));
       }
     }
     // One batch = U consecutive k-steps of the lane's RPL rows (values +
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
             for (int r = 0; r < RPL; ++r) dd[r] = -32768;
           }
 #pragma unroll
-          for (int r = 0; r < RPL; ++r) c[u][r] = dd[r] == -32768 ? -1 : (int)(rowv[r] + dd[r]);
+          for (int r = 0; r < RPL; ++r) c[u][r] = dd[r] == -32768 ? -1 : rowv[r] + dd[r];
         }
         if constexpr (D8) {
           int dd[RPL];
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
             for (int r = 0; r < RPL; ++r) dd[r] = 255;
           }
 #pragma unroll
-          for (int r = 0; r < RPL; ++r) c[u][r] = dd[r] == 255 ? -1 : (int)(rowv[r] + s_tab[dd[r]]);
+          for (int r = 0; r < RPL; ++r) c[u][r] = dd[r] == 255 ? -1 : rowv[r] + s_tab[dd[r]];
         }
       }
     };

@@ -15,12 +15,18 @@ import paper_2302_05662_b200 as P  # noqa: E402
 import spmv_inputs as si  # noqa: E402
 from gpu_cases import corpus  # noqa: E402
 
-FMTS = [(P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR)), (P.FMT_CSR, dict(csr_alg=P.CSR_SCALAR)),
-        (P.FMT_CSR, dict(csr_alg=P.CSR_MERGE)), (P.FMT_ELL, {}), (P.FMT_SELL, {}),
-        (P.FMT_SELL, dict(sell_C=32, sell_sigma=64)), (P.FMT_HYB, {}), (P.FMT_COO, {}),
-        (P.FMT_CSR, dict(csr_alg=P.CSR_STREAM)), (P.FMT_BELL, dict(bell_b=2)), (P.FMT_BELL, dict(bell_b=3)),
-        (P.FMT_ELL, dict(index16=-1)), (P.FMT_SELL, dict(index16=-1)), (P.FMT_SELL, dict(sell_C=32, sell_sigma=64,
-                                                                                       index16=-1))]
+# (format, params, launch or None): every kernel family incl. the round-2 tile,
+# merge-stream and 8-bit dictionary variants
+FMTS = [(P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR), None), (P.FMT_CSR, dict(csr_alg=P.CSR_SCALAR), None),
+        (P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), None), (P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), (128, 255, -1, 0x108)),
+        (P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), (128, 255, -1, 0x208)),
+        (P.FMT_ELL, dict(index16=0), None), (P.FMT_SELL, dict(index16=0), None),
+        (P.FMT_SELL, dict(sell_C=32, sell_sigma=64, index16=0), None), (P.FMT_HYB, {}, None),
+        (P.FMT_HYB, {}, (256, 255, -1, 0x108)), (P.FMT_COO, {}, None), (P.FMT_COO, {}, (256, 255, -1, 0x108)),
+        (P.FMT_CSR, dict(csr_alg=P.CSR_STREAM), None), (P.FMT_BELL, dict(bell_b=2), None),
+        (P.FMT_BELL, dict(bell_b=3), None),
+        (P.FMT_ELL, dict(index16=-1), None), (P.FMT_SELL, dict(index16=-1), None),
+        (P.FMT_SELL, dict(sell_C=32, sell_sigma=64, index16=-1), None)]
 
 
 def main():
@@ -39,10 +45,11 @@ def main():
                 P.spmv_features(h)
             x = torch.from_numpy(si.vector(max(coo.cols, 1))[:coo.cols]).to(tdt).cuda()
             y = torch.ones(coo.rows, dtype=tdt, device="cuda")
-            for fmt, params in FMTS:
+            for fmt, params, launch in FMTS:
                 if coo.rows == 0 and fmt != P.FMT_CSR:
                     continue
                 P.spmv_convert(h, fmt, **params)
+                P.spmv_set_launch(h, fmt, *(launch or (0, 0, -1, 0)))
                 P.spmv_run(h, 2.5, x, -0.5, y)
                 P.spmv_run(h, 1.0, x, 0.0, y)
                 if coo.rows == coo.cols and coo.rows > 0:
