@@ -129,8 +129,7 @@ typedef struct {
                            per lane (2/4/8: warp chunks of 32·knob entries) or 0x100 | EPT (EPT =
                            4/8/16: row-interleaved tiles of block·EPT entries staged in shared memory,
                            thread per row); ELL: rows per warp (32/64/128/256) in the low 16 bits; ELL
-                           and SELL: bit 16 (65536) selects the carried-batch loop (see kern_sliced.cuh); with 8-bit
-                           column codes, bit 17 (131072) doubles the k-steps per batch */
+                           and SELL: bit 16 (65536) selects the carried-batch loop (see kern_sliced.cuh) */
 } spmv_launch_t;
 
 /* spmv_tune flags */

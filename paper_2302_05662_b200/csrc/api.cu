@@ -395,17 +395,9 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
         if (t * 2 <= 32) v.push_back(t * 2);
         return v;
       }
-    case SPMV_FMT_ELL: {  // rows per warp × batch loop (kSlicedCarry) [× doubled batch with 8-bit codes]
-      std::vector<int> v{32, 64, 128, 32 | kern::kSlicedCarry, 64 | kern::kSlicedCarry, 128 | kern::kSlicedCarry};
-      if (h->ell_col8)
-        for (int b : {32, 64, 128}) v.push_back(b | kern::kSlicedCarry | kern::kSlicedWide);
-      return v;
-    }
-    case SPMV_FMT_SELL: {
-      std::vector<int> v{(int)h->sell_C, (int)h->sell_C | kern::kSlicedCarry};
-      if (h->sell_col8) v.push_back((int)h->sell_C | kern::kSlicedCarry | kern::kSlicedWide);
-      return v;
-    }
+    case SPMV_FMT_ELL:  // rows per warp × batch loop (kern::kSlicedCarry)
+      return {32, 64, 128, 32 | kern::kSlicedCarry, 64 | kern::kSlicedCarry, 128 | kern::kSlicedCarry};
+    case SPMV_FMT_SELL: return {(int)h->sell_C, (int)h->sell_C | kern::kSlicedCarry};
     case SPMV_FMT_COO:  // warp chunks of 32·W entries, or row-interleaved tiles of block·EPT entries
     case SPMV_FMT_HYB:
       return {2, 4, 8, kern::kCooTile | 4, kern::kCooTile | 8, kern::kCooTile | 16};

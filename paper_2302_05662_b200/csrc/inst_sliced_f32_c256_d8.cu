@@ -4,7 +4,5 @@ namespace spmv {
 namespace kern {
 template SlicedFn sliced_fn<float, 256, 2, false>(int, int);
 template SlicedFn sliced_fn<float, 256, 2, true>(int, int);
-template SlicedFn sliced_fn<float, 256, 3, false>(int, int);
-template SlicedFn sliced_fn<float, 256, 3, true>(int, int);
 }  // namespace kern
 }  // namespace spmv

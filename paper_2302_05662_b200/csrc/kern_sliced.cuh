@@ -83,14 +83,11 @@ __device__ __forceinline__ void load_c8(const uint8_t* p, int (&d)[N]) {
 //             (fastest on scattered gathers: c4 ELL 539 vs 564 µs).
 template <int B, int R, class T, int C, int ENC, bool CARRY>
 __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const SlicedParams p) {
-  // ENC 3 = 8-bit codes with twice the k-steps per batch (more loads in
-  // flight: a 9-byte slot carries 25 % fewer bytes than a 12-byte one)
-  constexpr bool D16 = ENC == 1, D8 = ENC >= 2, DOFF = ENC != 0;
-  constexpr int UX = ENC == 3 ? 2 : 1;
+  constexpr bool D16 = ENC == 1, D8 = ENC == 2, DOFF = ENC != 0;
   constexpr int RPL = C / 32;                                       // rows per lane
   constexpr int VW = (int)(16 / sizeof(T)) < RPL ? (int)(16 / sizeof(T)) : RPL;  // elems per vector load
   constexpr int NV = RPL / VW;
-  constexpr int U = (RPL >= 8 ? 1 : 8 / RPL) * UX;                  // k-unroll (loads in flight)
+  constexpr int U = RPL >= 8 ? 1 : 8 / RPL;                         // k-unroll (loads in flight)
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * (B / 32);

@@ -24,14 +24,11 @@ struct SlicedParams {
 };
 
 using SlicedFn = void (*)(const SlicedParams);
-// ENC: column encoding, 0 = int32 columns, 1 = 16-bit offsets, 2 = 8-bit dictionary codes,
-// 3 = 8-bit codes with twice the k-steps per batch (knob kSlicedWide)
+// ENC: column encoding, 0 = int32 columns, 1 = 16-bit offsets, 2 = 8-bit dictionary codes
 template <class T, int C, int ENC, bool CARRY>
 SlicedFn sliced_fn(int bi, int ri);
 // launch knob flag of ELL/SELL: the carried-batch loop (see k_sliced)
 constexpr int kSlicedCarry = 1 << 16;
-// launch knob flag of ELL/SELL with 8-bit codes: twice the k-steps per batch
-constexpr int kSlicedWide = 1 << 17;
 
 }  // namespace kern
 }  // namespace spmv

@@ -8,12 +8,11 @@ template <class T>
 void launch_sliced(spmv_matrix* h, kern::SlicedParams& p, int C, const spmv_launch_t& L) {
   const int bi = block_index(L.block), ri = reg_index(L.maxreg);
   const void* fn;
-  const int enc = p.col8 ? ((L.knob & kern::kSlicedWide) ? 3 : 2) : (p.col16 ? 1 : 0);
+  const int enc = p.col8 ? 2 : (p.col16 ? 1 : 0);
   const bool carry = (L.knob & kern::kSlicedCarry) != 0;
 #define SL_ENC(CC, E) (carry ? (const void*)kern::sliced_fn<T, CC, E, true>(bi, ri) \
                              : (const void*)kern::sliced_fn<T, CC, E, false>(bi, ri))
-#define SL_PICK(CC) \
-  fn = enc == 3 ? SL_ENC(CC, 3) : (enc == 2 ? SL_ENC(CC, 2) : (enc == 1 ? SL_ENC(CC, 1) : SL_ENC(CC, 0)))
+#define SL_PICK(CC) fn = enc == 2 ? SL_ENC(CC, 2) : (enc == 1 ? SL_ENC(CC, 1) : SL_ENC(CC, 0))
   switch (C) {
     case 32: SL_PICK(32); break;
     case 64: SL_PICK(64); break;
