@@ -124,10 +124,10 @@ typedef struct {
   int32_t maxreg;       /* 32, 64, 128, 255 */
   int32_t carveout_pct; /* -1 = driver default, else 0..100 */
   int32_t knob;         /* CSR-vector: lanes per row; merge-path: items per thread (4/8/16: per-warp
-                           merge walk; 0x100 | IPT: row-interleaved tiles of block·IPT items; 0x200 | IPT:
-                           the same tiles fed by a TMA producer warp, block + 32 threads); COO/HYB: entries
+                           merge walk; 0x100 | IPT (IPT 4/8/16/32): row-interleaved tiles of block·IPT items;
+                           0x200 | IPT: the same tiles fed by a TMA producer warp, block + 32 threads); COO/HYB: entries
                            per lane (2/4/8: warp chunks of 32·knob entries) or 0x100 | EPT (EPT =
-                           4/8/16: row-interleaved tiles of block·EPT entries staged in shared memory,
+                           4/8/16/32: row-interleaved tiles of block·EPT entries staged in shared memory,
                            thread per row); ELL: rows per warp (32/64/128/256) in the low 16 bits; ELL
                            and SELL: bit 16 (65536) selects the carried-batch loop (see kern_sliced.cuh) */
 } spmv_launch_t;

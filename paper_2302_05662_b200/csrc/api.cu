@@ -385,8 +385,8 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
   switch (fmt) {
     case SPMV_FMT_CSR:
       if (h->csr_alg == SPMV_CSR_MERGE)  // per-warp merge walk, or row-interleaved tiles of block·IPT items
-        return {4, 8, 16, kern::kMergeTile | 4, kern::kMergeTile | 8, kern::kMergeTile | 16,
-                kern::kMergeStream | 4, kern::kMergeStream | 8, kern::kMergeStream | 16};
+        return {4, 8, 16, kern::kMergeTile | 4, kern::kMergeTile | 8, kern::kMergeTile | 16, kern::kMergeTile | 32,
+                kern::kMergeStream | 4, kern::kMergeStream | 8, kern::kMergeStream | 16, kern::kMergeStream | 32};
       if (h->csr_alg == SPMV_CSR_STREAM) return {16, 32, 64};
       {
         int t = csr_default_lanes(h);
@@ -400,7 +400,7 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
     case SPMV_FMT_SELL: return {(int)h->sell_C, (int)h->sell_C | kern::kSlicedCarry};
     case SPMV_FMT_COO:  // warp chunks of 32·W entries, or row-interleaved tiles of block·EPT entries
     case SPMV_FMT_HYB:
-      return {2, 4, 8, kern::kCooTile | 4, kern::kCooTile | 8, kern::kCooTile | 16};
+      return {2, 4, 8, kern::kCooTile | 4, kern::kCooTile | 8, kern::kCooTile | 16, kern::kCooTile | 32};
     case SPMV_FMT_BELL: return {(int)h->bell_b};
   }
   return {0};

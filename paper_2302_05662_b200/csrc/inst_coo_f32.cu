@@ -8,5 +8,6 @@ template CooFn coo_fn<float, 8>(int, int);
 template CooFn coo_tile_fn<float, 4>(int, int);
 template CooFn coo_tile_fn<float, 8>(int, int);
 template CooFn coo_tile_fn<float, 16>(int, int);
+template CooFn coo_tile_fn<float, 32>(int, int);
 }  // namespace kern
 }  // namespace spmv

@@ -8,5 +8,6 @@ template CooFn coo_fn<double, 8>(int, int);
 template CooFn coo_tile_fn<double, 4>(int, int);
 template CooFn coo_tile_fn<double, 8>(int, int);
 template CooFn coo_tile_fn<double, 16>(int, int);
+template CooFn coo_tile_fn<double, 32>(int, int);
 }  // namespace kern
 }  // namespace spmv

@@ -8,8 +8,10 @@ template CsrFn csr_merge_fn<float, int64_t, 16>(int, int);
 template CsrFn csr_merge_tile_fn<float, int64_t, 4>(int, int);
 template CsrFn csr_merge_tile_fn<float, int64_t, 8>(int, int);
 template CsrFn csr_merge_tile_fn<float, int64_t, 16>(int, int);
+template CsrFn csr_merge_tile_fn<float, int64_t, 32>(int, int);
 template CsrFn csr_merge_stream_fn<float, int64_t, 4>(int, int);
 template CsrFn csr_merge_stream_fn<float, int64_t, 8>(int, int);
 template CsrFn csr_merge_stream_fn<float, int64_t, 16>(int, int);
+template CsrFn csr_merge_stream_fn<float, int64_t, 32>(int, int);
 }  // namespace kern
 }  // namespace spmv

@@ -8,8 +8,10 @@ template CsrFn csr_merge_fn<double, int32_t, 16>(int, int);
 template CsrFn csr_merge_tile_fn<double, int32_t, 4>(int, int);
 template CsrFn csr_merge_tile_fn<double, int32_t, 8>(int, int);
 template CsrFn csr_merge_tile_fn<double, int32_t, 16>(int, int);
+template CsrFn csr_merge_tile_fn<double, int32_t, 32>(int, int);
 template CsrFn csr_merge_stream_fn<double, int32_t, 4>(int, int);
 template CsrFn csr_merge_stream_fn<double, int32_t, 8>(int, int);
 template CsrFn csr_merge_stream_fn<double, int32_t, 16>(int, int);
+template CsrFn csr_merge_stream_fn<double, int32_t, 32>(int, int);
 }  // namespace kern
 }  // namespace spmv

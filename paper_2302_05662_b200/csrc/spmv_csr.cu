@@ -80,6 +80,11 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     case 4: MERGE_PICK(4); break;
     case 8: MERGE_PICK(8); break;
     case 16: MERGE_PICK(16); break;
+    case 32:  // tiles only: a tile of block·32 items keeps every thread on a row of a ~30-entry stencil
+      if (!tile && !pipe) fail(SPMV_ERR_INVALID_ARG, "merge-path per-warp walk takes 4, 8 or 16 items per thread");
+      fn = pipe ? (const void*)kern::csr_merge_stream_fn<T, RP, 32>(bi, ri)
+                : (const void*)kern::csr_merge_tile_fn<T, RP, 32>(bi, ri);
+      break;
     default: fail(SPMV_ERR_INVALID_ARG, "merge-path items per thread must be 4, 8 or 16 (| kMergeTile or kMergeStream)");
   }
 #undef MERGE_PICK

@@ -119,7 +119,8 @@ void coo_launch(spmv_matrix* h, const int32_t* row, const int32_t* col, const vo
       case 4: fn = (const void*)kern::coo_tile_fn<T, 4>(bi, ri); break;
       case 8: fn = (const void*)kern::coo_tile_fn<T, 8>(bi, ri); break;
       case 16: fn = (const void*)kern::coo_tile_fn<T, 16>(bi, ri); break;
-      default: fail(SPMV_ERR_INVALID_ARG, "COO tile entries per thread must be 4, 8 or 16");
+      case 32: fn = (const void*)kern::coo_tile_fn<T, 32>(bi, ri); break;
+      default: fail(SPMV_ERR_INVALID_ARG, "COO tile entries per thread must be 4, 8, 16 or 32");
     }
     if (!fn) fail(SPMV_ERR_UNSUPPORTED, "COO tile: block × entries per thread exceeds shared memory");
     if (((uintptr_t)row | (uintptr_t)col | (uintptr_t)val) & 15)

@@ -322,7 +322,7 @@ def test_coo_tile_all_launches(case, dtype, fmt):
         else:
             P.spmv_convert(h, fmt)
         for block in (64, 128, 256, 512, 1024):
-            for ept in (4, 8, 16):
+            for ept in (4, 8, 16, 32):
                 P.spmv_set_launch(h, fmt, block, 255 if block <= 256 else 64, -1, flag | ept)
                 try:
                     check_y(h, coo, dtype, fmt, 2.5, -0.5, ref)
