@@ -771,7 +771,7 @@ static void tune_predict(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tu
   h->csr_alg = orig_alg;
   const double ratio = selector_speed_ratio(cls, x);
   const double t_pred = t_csr * ratio;
-  const double c_pred = (fmt == SPMV_FMT_CSR) ? 0.0 : selector_c_latency(cls, x);
+  const double c_pred = (fmt == SPMV_FMT_CSR) ? 0.0 : selector_c_latency(cls, f);
   const double gain = (double)iters * (t_csr - t_pred);
   const double overhead = h->f_latency + c_pred;
   bool convert = cls != 0 && gain > overhead;
@@ -1125,8 +1125,8 @@ spmv_status_t spmv_predict(const spmv_features_t* f, spmv_dtype_t dtype, spmv_pr
   selector_class_format(out->cls, &fmt, &out->params);
   out->format = fmt;
   out->speed_ratio = selector_speed_ratio(out->cls, x);
-  out->c_latency_s = fmt == SPMV_FMT_CSR ? 0.0 : selector_c_latency(out->cls, x);
-  out->f_latency_s = selector_f_latency(x);
+  out->c_latency_s = fmt == SPMV_FMT_CSR ? 0.0 : selector_c_latency(out->cls, *f);
+  out->f_latency_s = selector_f_latency(*f);
   return SPMV_OK;
 }
 

@@ -49,12 +49,39 @@ double selector_speed_ratio(int cls, const double* x) {
   return std::exp(eval_tree(model::kRatio[cls], x));
 }
 
-double selector_c_latency(int cls, const double* x) {
-  if (cls < 0 || cls >= model::kNumClasses) return 0.0;
-  return std::exp(eval_tree(model::kCLatency[cls], x));
+// Predictors of the overhead estimators (tools/train_selector.py
+// overhead_predictors: same order, same arithmetic): the conversions and the
+// feature pass are bandwidth-bound kernels plus a few launches, so their
+// device time is a constant plus per-entry, per-row and per-ELL-slot costs
+// (and, for ELL/SELL, the 8-bit dictionary's flag array of 2·bandwidth + 1 bins).
+static void overhead_predictors(const spmv_features_t& f, double phi[model::kNumOverheadPredictors]) {
+  const double n = (double)f.n_rows;
+  phi[0] = 1.0;
+  phi[1] = (double)f.nnz * 1e-6;
+  phi[2] = n * 1e-6;
+  phi[3] = std::ceil(n / 128.0) * 128.0 * (double)f.max_len * 1e-6;
+  phi[4] = 2.0 * (double)(f.bandwidth < (1LL << 22) ? f.bandwidth : (1LL << 22)) * 1e-6;  // dictionary flags
+  phi[5] = n * f.std * 1e-6;  // >= Σ|L_i − mean|: the row-length dispersion SELL pads
 }
 
-double selector_f_latency(const double* x) { return std::exp(eval_tree(model::kFLatency, x)); }
+static double linear(const double* w, const double* phi, int k) {
+  double s = 0.0;
+  for (int i = 0; i < k; ++i) s += w[i] * phi[i];
+  return s > 1e-6 ? s : 1e-6;
+}
+
+double selector_c_latency(int cls, const spmv_features_t& f) {
+  if (cls < 0 || cls >= model::kNumClasses) return 0.0;
+  double phi[model::kNumOverheadPredictors];
+  overhead_predictors(f, phi);
+  return linear(model::kCLatencyLin[cls], phi, model::kNumOverheadPredictors);
+}
+
+double selector_f_latency(const spmv_features_t& f) {
+  double phi[model::kNumOverheadPredictors];
+  overhead_predictors(f, phi);
+  return linear(model::kFLatencyLin, phi, 3);
+}
 
 const char* selector_class_name(int cls) {
   return (cls >= 0 && cls < model::kNumClasses) ? model::kClassNames[cls] : "?";

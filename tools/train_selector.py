@@ -12,8 +12,11 @@ conversion (fig:overhead_prediction P:461-516). Here:
   * classifier: sklearn DecisionTreeClassifier, criterion and depth chosen by
     5-fold cross-validation on the 80% split (the paper tuned with Optuna);
   * gain estimate: per-format DecisionTreeRegressor of log(t_format / t_CSR-vector);
-  * overheads: least-squares c_latency_f = a + b·nnz + c·rows per format and
-    f_latency = a + b·nnz + c·rows (both HBM-bound on B200: linear in bytes).
+  * overheads: c_latency_f = w·[1, nnz, rows, ELL slots] per format and
+    f_latency = w·[1, nnz, rows], non-negative least squares on the warm
+    latencies of profiles/overhead_corpus.jsonl (tools/overhead_corpus.py):
+    the conversions and the feature pass are bandwidth-bound kernels plus a
+    few launches, so their device time is a constant plus per-byte costs.
 
 Outputs: paper_2302_05662_b200/csrc/selector_model.h (generated),
 profiles/selector_model.json (the same model, for the CPU tests) and
@@ -58,6 +61,58 @@ def load(path):
     return recs
 
 
+def overhead_predictors(f):
+    """Same order and arithmetic as selector.cu overhead_predictors."""
+    n = float(f["n_rows"])
+    return [1.0, float(f["nnz"]) * 1e-6, n * 1e-6, math.ceil(n / 128.0) * 128.0 * float(f["max_len"]) * 1e-6,
+            2.0 * float(min(f["bandwidth"], 1 << 22)) * 1e-6, n * float(f["std"]) * 1e-6]
+
+
+def linear_pred(w, phi):
+    s = sum(a * b for a, b in zip(w, phi))
+    return s if s > 1e-6 else 1e-6
+
+
+def fit_overheads(path, seed):
+    """Non-negative linear models of the warm conversion / feature latencies,
+    with 5-fold cross-validated R² on the seconds and on their logarithm."""
+    from scipy.optimize import nnls
+    from sklearn.model_selection import KFold
+    recs = [json.loads(line) for line in open(path)]
+    recs = [r for r in recs if "features" in r]
+
+    def fit(rows, k):
+        X = np.array([overhead_predictors(f)[:k] for f, _ in rows])
+        Y = np.array([t for _, t in rows])
+        # relative least squares (rows scaled by 1/t): µs-scale small-matrix
+        # conversions matter as much as 100 ms ones for the gate
+        wts = 1.0 / Y
+        w, _ = nnls(X * wts[:, None], Y * wts)
+        pred_cv = np.zeros_like(Y)
+        for tr, te in KFold(5, shuffle=True, random_state=seed).split(X):
+            wf, _ = nnls(X[tr] * wts[tr, None], Y[tr] * wts[tr])
+            pred_cv[te] = np.maximum(X[te] @ wf, 1e-6)
+        pred = np.maximum(X @ w, 1e-6)
+
+        def r2(y, p):
+            ss = float(np.sum((y - y.mean()) ** 2))
+            return 1.0 - float(np.sum((y - p) ** 2)) / ss if ss > 0 else 1.0
+        ly = np.log(Y)
+        return [float(v) for v in w], {"n": len(rows), "r2_train": r2(Y, pred), "r2_cv": r2(Y, pred_cv),
+                                       "r2_log_train": r2(ly, np.log(pred)), "r2_log_cv": r2(ly, np.log(pred_cv))}
+
+    clat, stats = {}, {}
+    for c in CLASSES:
+        rows = [(r["features"], r["formats"][c]["c_latency_s"]) for r in recs
+                if "c_latency_s" in r.get("formats", {}).get(c, {})]
+        if len(rows) < 6:
+            clat[c], stats[c] = [0.0] * 6, None
+            continue
+        clat[c], stats[c] = fit(rows, 6)
+    fw, fstats = fit([(r["features"], r["f_latency_s"]) for r in recs], 3)
+    return clat, stats, fw + [0.0, 0.0, 0.0], fstats
+
+
 def tree_to_nodes(t, leaf_value):
     tr = t.tree_
     nodes = []
@@ -82,6 +137,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--corpus", default=os.path.join(ROOT, "profiles", "selector_corpus.jsonl"))
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--overheads", default=os.path.join(ROOT, "profiles", "overhead_corpus.jsonl"))
     a = ap.parse_args()
     from sklearn.model_selection import GridSearchCV, train_test_split
     from sklearn.tree import DecisionTreeClassifier, DecisionTreeRegressor
@@ -159,14 +215,19 @@ def main():
     flat, r2, r2cv = logtree(list(idx), [r["f_latency_s"] for r in recs])
     flat_r2 = {"train": r2, "cv": r2cv}
 
+    clat_lin, clat_lin_stats, flat_lin, flat_lin_stats = fit_overheads(a.overheads, a.seed)
     model = {"classes": CLASSES, "features": FEATURES, "classifier": cls_nodes, "params": gs.best_params_,
              "ratio": ratio_nodes, "c_latency": clat, "f_latency": flat,
+             "overhead_predictors": ["1", "nnz/1e6", "rows/1e6", "ceil(rows/128)*128*max_len/1e6",
+                                     "2*min(bandwidth, 2^22)/1e6", "rows*std/1e6"],
+             "c_latency_lin": clat_lin, "f_latency_lin": flat_lin,
              "stats": {"n_matrices": len(recs), "train": len(tr_i), "test": len(te_i), "cv_score": gs.best_score_,
                        "acc_train": acc_tr, "acc_test": acc_te, "perf_ratio_test_geomean": pr_te[0],
                        "perf_ratio_test_min": pr_te[1], "perf_ratio_all_geomean": pr_all[0],
                        "perf_ratio_all_min": pr_all[1], "perf_ratio_deployed_all_geomean": pr_final[0],
                        "perf_ratio_deployed_all_min": pr_final[1], "ratio_r2": ratio_r2, "c_latency_r2": clat_r2,
-                       "f_latency_r2": flat_r2}}
+                       "f_latency_r2": flat_r2, "c_latency_lin_r2": clat_lin_stats,
+                       "f_latency_lin_r2": flat_lin_stats}}
     # self-check: node evaluation == sklearn
     for i in range(len(recs)):
         assert int(eval_nodes(cls_nodes, X[i])) == int(final.predict(X[i:i + 1])[0])
@@ -207,6 +268,17 @@ def write_header(m):
     L.append("constexpr const Node* kCLatency[kNumClasses] = {" +
              ", ".join(f"kCLat{i}" for i in range(len(m["classes"]))) + "};")
     nodes("kFLatency", m["f_latency"])
+    L.append("// overhead estimators used by the run-time mode: seconds = w · [1, nnz/1e6, rows/1e6,")
+    L.append("// ceil(rows/128)*128*max_len/1e6, 2*min(bandwidth, 2^22)/1e6, rows*std/1e6] (non-negative least")
+    L.append("// squares on warm device latencies; 2·bandwidth = the dictionary's flag array, rows·std bounds the")
+    L.append("// total deviation of the row lengths, hence SELL's padding)")
+    L.append("constexpr int kNumOverheadPredictors = 6;")
+    L.append("constexpr double kCLatencyLin[kNumClasses][kNumOverheadPredictors] = {")
+    for c in m["classes"]:
+        L.append("    {" + ", ".join(_fmt(v) for v in m["c_latency_lin"][c]) + "},  // " + c)
+    L.append("};")
+    L.append("constexpr double kFLatencyLin[kNumOverheadPredictors] = {" +
+             ", ".join(_fmt(v) for v in m["f_latency_lin"]) + "};")
     L += ["", "}  // namespace model", "}  // namespace spmv", ""]
     open(p, "w").write("\n".join(L))
 
@@ -216,7 +288,7 @@ def write_report(m, recs, X, clf):
     from collections import Counter
     best = Counter(r["best"] for r in recs)
     pred = Counter(CLASSES[int(c)] for c in clf.predict(X))
-    out = ["# Learned format selector — training report (round 1)", "",
+    out = ["# Learned format selector — training report", "",
            "Generated by `tools/train_selector.py` from `profiles/selector_corpus.jsonl` "
            "(`tools/selector_corpus.py` on one B200: every candidate format converted, launch-tuned and timed).", "",
            f"* matrices: {s['n_matrices']} (train {s['train']} / test {s['test']}, 80/20 as P:899)",
@@ -230,6 +302,13 @@ def write_report(m, recs, X, clf):
            f"5-fold CV {s['f_latency_r2']['cv']:.4f}; c_latency R² train/CV per format: " +
            ", ".join(f"{k} {v['train']:.3f}/{v['cv']:.3f}" for k, v in s["c_latency_r2"].items() if v is not None),
            "* log speed-ratio regressors R² (train): " + ", ".join(f"{k} {v:.3f}" for k, v in s["ratio_r2"].items()),
+           "* **overhead estimators used by the run-time mode** (round 2): non-negative linear models in "
+           "[1, nnz, rows, ELL slots, 2·bandwidth (the 8-bit dictionary's flag array), rows·std (SELL padding)] fitted on warm latencies (`profiles/overhead_corpus.jsonl`, median of 3 "
+           "after a warm-up, fresh handle per repetition); 5-fold CV R² on seconds / on log seconds: " +
+           ", ".join(f"{k} {v['r2_cv']:.3f} / {v['r2_log_cv']:.3f} (n={v['n']})"
+                     for k, v in s["c_latency_lin_r2"].items() if v is not None) +
+           f"; f_latency {s['f_latency_lin_r2']['r2_cv']:.3f} / {s['f_latency_lin_r2']['r2_log_cv']:.3f}. "
+           "(The round-1 tree models above, fitted to single cold measurements, are kept in the JSON for comparison.)",
            "", "| format | best on (matrices) | predicted for |", "|---|---|---|"]
     for c in CLASSES:
         out.append(f"| {c} | {best.get(c, 0)} | {pred.get(c, 0)} |")
