@@ -44,7 +44,10 @@ __global__ void k_dict_flags(const RP* __restrict__ rp, const int32_t* __restric
   // warp per 32 consecutive rows: their entries are one contiguous range, read
   // coalesced; the row of an entry is found among the 32 row starts the lanes
   // hold (binary search over shuffles)
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp_in_block = threadIdx.x >> 5;
+  __shared__ int64_t s_seen[8][32];  // 256-thread blocks
+  s_seen[warp_in_block][lane] = INT64_MIN;
+  __syncwarp();
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r0 = w0 * 32; r0 < rows; r0 += nw * 32) {
@@ -60,10 +63,18 @@ __global__ void k_dict_flags(const RP* __restrict__ rp, const int32_t* __restric
         if (sj <= k) lo += step;
       }
       if (k < end) {
-        // read before write: a banded matrix hits the same few dozen flags from
-        // every warp; stores to one address serialise in L2, cached reads do not
-        int64_t* f = flags + ((int64_t)col[k] - origin - (r0 + lo) + m);
-        if (*f == 0) *f = 1;
+        // a banded matrix hits the same few dozen offsets in every warp: a
+        // per-warp cache of recently seen offsets (32 hashed slots in shared
+        // memory) skips the flag array (scattered 8-byte reads, one L1TEX
+        // wavefront per distinct line) for all but the first sightings; on a
+        // miss, read before write (stores to one address serialise in L2)
+        const int64_t d = (int64_t)col[k] - origin - (r0 + lo);
+        const int slot = (int)((d ^ (d >> 5) ^ (d >> 10)) & 31);
+        if (s_seen[warp_in_block][slot] != d) {
+          int64_t* f = flags + (d + m);
+          if (*f == 0) *f = 1;
+          s_seen[warp_in_block][slot] = d;
+        }
       }
     }
   }
