@@ -126,8 +126,7 @@ typedef struct {
   int32_t knob;         /* CSR-vector: lanes per row; merge-path: items per thread (4/8/16: per-warp
                            merge walk; 0x100 | IPT (IPT 4/8/16/32): row-interleaved tiles of block·IPT items;
                            0x200 | IPT: the same tiles fed by a TMA producer warp, block + 32 threads); COO/HYB: entries
-                           per lane (2/4/8: warp chunks of 32·knob entries; 0x400 | W: the same chunks in
-                           warp order, 32 consecutive entries per instruction) or 0x100 | EPT (EPT =
+                           per lane (2/4/8: warp chunks of 32·knob entries) or 0x100 | EPT (EPT =
                            4/8/16/32: row-interleaved tiles of block·EPT entries staged in shared memory,
                            thread per row); ELL: rows per warp (32/64/128/256) in the low 16 bits; ELL
                            and SELL: bit 16 (65536) selects the carried-batch loop (see kern_sliced.cuh) */

@@ -400,8 +400,7 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
     case SPMV_FMT_SELL: return {(int)h->sell_C, (int)h->sell_C | kern::kSlicedCarry};
     case SPMV_FMT_COO:  // warp chunks of 32·W entries, or row-interleaved tiles of block·EPT entries
     case SPMV_FMT_HYB:
-      return {2, 4, 8, kern::kCooWarpOrder | 2, kern::kCooWarpOrder | 4, kern::kCooWarpOrder | 8,
-              kern::kCooTile | 4, kern::kCooTile | 8, kern::kCooTile | 16, kern::kCooTile | 32};
+      return {2, 4, 8, kern::kCooTile | 4, kern::kCooTile | 8, kern::kCooTile | 16, kern::kCooTile | 32};
     case SPMV_FMT_BELL: return {(int)h->bell_b};
   }
   return {0};

@@ -54,26 +54,31 @@ __global__ void k_dict_flags(const RP* __restrict__ rp, const int32_t* __restric
     const int64_t my = r0 + lane < rows ? (int64_t)rp[r0 + lane] : (int64_t)rp[rows];
     const int64_t end = (int64_t)rp[r0 + 32 < rows ? r0 + 32 : rows];
     const int64_t beg = __shfl_sync(0xffffffffu, my, 0);
-    for (int64_t k0 = beg; k0 < end; k0 += 32) {
-      const int64_t k = k0 + lane;
-      int lo = 0;  // largest j with start_j <= k (rows without entries share a start: the last one wins)
+    for (int64_t k0 = beg; k0 < end; k0 += 128) {
+      int cv[4];  // four column loads in flight per lane (the loop is latency-bound otherwise)
 #pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int64_t sj = __shfl_sync(0xffffffffu, my, lo + step);
-        if (sj <= k) lo += step;
-      }
-      if (k < end) {
-        // a banded matrix hits the same few dozen offsets in every warp: a
-        // per-warp cache of recently seen offsets (32 hashed slots in shared
-        // memory) skips the flag array (scattered 8-byte reads, one L1TEX
-        // wavefront per distinct line) for all but the first sightings; on a
-        // miss, read before write (stores to one address serialise in L2)
-        const int64_t d = (int64_t)col[k] - origin - (r0 + lo);
-        const int slot = (int)((d ^ (d >> 5) ^ (d >> 10)) & 31);
-        if (s_seen[warp_in_block][slot] != d) {
-          int64_t* f = flags + (d + m);
-          if (*f == 0) *f = 1;
-          s_seen[warp_in_block][slot] = d;
+      for (int j = 0; j < 4; ++j) cv[j] = k0 + 32 * j + lane < end ? col[k0 + 32 * j + lane] : 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t k = k0 + 32 * j + lane;
+        int lo = 0;  // largest row j with start_j <= k (rows without entries share a start: the last wins)
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int64_t sj = __shfl_sync(0xffffffffu, my, lo + step);
+          if (sj <= k) lo += step;
+        }
+        if (k < end) {
+          // a banded matrix hits the same few dozen offsets in every warp: a
+          // per-warp cache of recently seen offsets (32 hashed slots in shared
+          // memory) skips the flag array for all but the first sightings; on
+          // a miss, read before write (stores to one address serialise in L2)
+          const int64_t d = (int64_t)cv[j] - origin - (r0 + lo);
+          const int slot = (int)((d ^ (d >> 5) ^ (d >> 10)) & 31);
+          if (s_seen[warp_in_block][slot] != d) {
+            int64_t* f = flags + (d + m);
+            if (*f == 0) *f = 1;
+            s_seen[warp_in_block][slot] = d;
+          }
         }
       }
     }

@@ -5,9 +5,6 @@ namespace kern {
 template CooFn coo_fn<float, 2>(int, int);
 template CooFn coo_fn<float, 4>(int, int);
 template CooFn coo_fn<float, 8>(int, int);
-template CooFn coo_wo_fn<float, 2>(int, int);
-template CooFn coo_wo_fn<float, 4>(int, int);
-template CooFn coo_wo_fn<float, 8>(int, int);
 template CooFn coo_tile_fn<float, 4>(int, int);
 template CooFn coo_tile_fn<float, 8>(int, int);
 template CooFn coo_tile_fn<float, 16>(int, int);

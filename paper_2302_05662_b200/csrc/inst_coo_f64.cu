@@ -5,9 +5,6 @@ namespace kern {
 template CooFn coo_fn<double, 2>(int, int);
 template CooFn coo_fn<double, 4>(int, int);
 template CooFn coo_fn<double, 8>(int, int);
-template CooFn coo_wo_fn<double, 2>(int, int);
-template CooFn coo_wo_fn<double, 4>(int, int);
-template CooFn coo_wo_fn<double, 8>(int, int);
 template CooFn coo_tile_fn<double, 4>(int, int);
 template CooFn coo_tile_fn<double, 8>(int, int);
 template CooFn coo_tile_fn<double, 16>(int, int);

@@ -151,84 +151,6 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_coo(const CooPa
   }
 }
 
-// ------------------------------------------------------------------ warp order
-// COO with the chunk's entries in warp order: at step q lane l holds entry
-// base + 32·q + l, so each load instruction is one 128-byte line per array and
-// each gather instruction fetches 32 consecutive stored entries — the order
-// whose measured gather ceiling is 11 % above the lane order's on c3
-// (profiles/r2_gather_ceiling.md). All W loads, then all W gathers are issued
-// before any reduction; each step is a 5-shuffle segmented scan keyed by row
-// whose running sum carries into the next step. Same chunk records as k_coo.
-template <int B, int R, class T, int W>
-__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_coo_wo(const CooParams p) {
-  const int lane = threadIdx.x & 31;
-  const int64_t chunk = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
-  const int64_t base = chunk * 32 * W;
-  if (base >= p.nnz) return;  // warp-uniform
-  const T* __restrict__ val = static_cast<const T*>(p.val);
-  const T* __restrict__ x = static_cast<const T*>(p.x);
-  T* __restrict__ y = static_cast<T*>(p.y);
-  const double alpha = epi_alpha(p.e);
-  int r[W], c[W];
-  T v[W];
-#pragma unroll
-  for (int q = 0; q < W; ++q) {
-    const int64_t k = base + 32 * q + lane;
-    const bool ok = k < p.nnz;
-    r[q] = ok ? ld_stream(p.row + k) : INT_MAX;  // sentinel row past the end
-    c[q] = ok ? ld_stream(p.col + k) : 0;
-    v[q] = ok ? ld_stream(val + k) : T(0);
-  }
-  T xv[W];
-#pragma unroll
-  for (int q = 0; q < W; ++q) xv[q] = r[q] != INT_MAX ? ld_x(x + c[q]) : T(0);
-  const int chunk_first = __shfl_sync(0xffffffffu, r[0], 0);
-  const bool cont_in = base > 0 && p.row[base - 1] == chunk_first;
-  const int64_t end = base + 32 * W;
-  const int after = end < p.nnz ? p.row[end] : INT_MAX;  // first row of the next chunk
-  int carry_row = -1;
-  double carry = 0.0;
-  int last_valid = chunk_first;
-#pragma unroll
-  for (int q = 0; q < W; ++q) {
-    const int key = r[q];
-    double s = (double)v[q] * (double)xv[q];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double su = __shfl_up_sync(0xffffffffu, s, o);
-      const int ku = __shfl_up_sync(0xffffffffu, key, o);
-      if (lane >= o && ku == key) s += su;
-    }
-    if (key == carry_row) s += carry;  // the run that continues from step q-1 (a prefix of the lanes)
-    // next entry's row: the next lane, or step q+1's lane 0, or the next chunk's first
-    int next = __shfl_down_sync(0xffffffffu, key, 1);
-    const int nq = q + 1 < W ? __shfl_sync(0xffffffffu, r[q + 1 < W ? q + 1 : q], 0) : after;
-    if (lane == 31) next = nq;
-    if (key != INT_MAX && next != key) {  // the run of `key` ends at this entry
-      const bool first = cont_in && key == chunk_first;
-      if (first) p.recs[chunk].head = s;
-      else y[key] = epi_value<T>(p.e, alpha, s, y, key);
-    }
-    carry_row = __shfl_sync(0xffffffffu, key, 31);
-    carry = __shfl_sync(0xffffffffu, s, 31);
-    const unsigned valid = __ballot_sync(0xffffffffu, key != INT_MAX);
-    if (valid) last_valid = __shfl_sync(0xffffffffu, key, 31 - __clz((int)valid));
-  }
-  if (lane == 0) {
-    ChunkRec& rec = p.recs[chunk];
-    rec.first_row = chunk_first;
-    rec.cont_in = cont_in;
-    rec.last_row = last_valid;
-    // the chunk's last run continues into the next chunk: its partial is the carry
-    const bool cont_out = after != INT_MAX && after == last_valid && carry_row == last_valid;
-    rec.cont_out = cont_out;
-    if (cont_out) {
-      rec.tail = carry;
-      if (cont_in && last_valid == chunk_first) rec.head = carry;
-    }
-  }
-}
-
 // ------------------------------------------------------------------ row-interleaved tiles
 // The warp-chunk kernel above gathers, in one instruction, entries of the
 // same few rows (lane l holds W consecutive entries): on a stencil the 27
@@ -403,15 +325,6 @@ CooFn coo_tile_fn(int bi, int ri) {
   return tab[bi][ri];
 }
 #undef COOT_ROW
-
-#define COOW_ROW(B, W) {&k_coo_wo<B, 32, T, W>, &k_coo_wo<B, 64, T, W>, &k_coo_wo<B, 128, T, W>, &k_coo_wo<B, 255, T, W>}
-template <class T, int W>
-CooFn coo_wo_fn(int bi, int ri) {
-  static const CooFn tab[5][4] = {COOW_ROW(64, W), COOW_ROW(128, W), COOW_ROW(256, W), COOW_ROW(512, W),
-                                  COOW_ROW(1024, W)};
-  return tab[bi][ri];
-}
-#undef COOW_ROW
 
 #define COO_ROW(B, W) {&k_coo<B, 32, T, W>, &k_coo<B, 64, T, W>, &k_coo<B, 128, T, W>, &k_coo<B, 255, T, W>}
 #define COO_TAB(W) {COO_ROW(64, W), COO_ROW(128, W), COO_ROW(256, W), COO_ROW(512, W), COO_ROW(1024, W)}

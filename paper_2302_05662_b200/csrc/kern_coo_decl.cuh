@@ -23,11 +23,6 @@ using CooFn = void (*)(const CooParams);
 template <class T, int W>
 CooFn coo_fn(int bi, int ri);
 
-// Warp-order chunks (k_coo_wo): launch knob kCooWarpOrder | W, W ∈ {2, 4, 8}.
-constexpr int kCooWarpOrder = 0x400;
-template <class T, int W>
-CooFn coo_wo_fn(int bi, int ri);
-
 // Row-interleaved tile kernel (k_coo_tile): launch knob kCooTile | EPT, a
 // block stages B·EPT consecutive entries in shared memory and walks them
 // thread-per-row. nullptr for (block, EPT) pairs over the shared-memory cap.

@@ -71,6 +71,22 @@ __device__ __forceinline__ void load_c8(const uint8_t* p, int (&d)[N]) {
   }
 }
 
+// N (<= 4) 8-bit codes of one lane as one 32-bit word (code r in byte r).
+template <int N>
+__device__ __forceinline__ uint32_t load_c8_word(const uint8_t* p) {
+  if constexpr (N == 1) {
+    unsigned short v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(l2_evict_first()));
+    return 0xffffff00u | (uint32_t)(v & 0xff);
+  } else if constexpr (N == 2) {
+    unsigned short v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(l2_evict_first()));
+    return 0xffff0000u | (uint32_t)v;
+  } else {
+    return (uint32_t)ld_stream(reinterpret_cast<const int*>(p));
+  }
+}
+
 // ENC selects the stored column encoding: 0 int32 columns (pad −1); 1 16-bit
 // offsets d = col − origin − row (pad −32768); 2 8-bit codes into the
 // matrix's offset dictionary (pad 255), decoded through a 256-entry table in
@@ -84,10 +100,15 @@ __device__ __forceinline__ void load_c8(const uint8_t* p, int (&d)[N]) {
 template <int B, int R, class T, int C, int ENC, bool CARRY>
 __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const SlicedParams p) {
   constexpr bool D16 = ENC == 1, D8 = ENC == 2, DOFF = ENC != 0;
+  // 8-bit codes of up to 4 rows per lane stay packed in one register per
+  // k-step until the gather (decoded through the shared table there): the
+  // batch holds U words instead of U·RPL columns (register pressure at the
+  // 64-register cap of 1024-thread blocks)
   constexpr int RPL = C / 32;                                       // rows per lane
   constexpr int VW = (int)(16 / sizeof(T)) < RPL ? (int)(16 / sizeof(T)) : RPL;  // elems per vector load
   constexpr int NV = RPL / VW;
   constexpr int U = RPL >= 8 ? 1 : 8 / RPL;                         // k-unroll (loads in flight)
+  constexpr bool PACK = D8 && RPL <= 4;
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * (B / 32);
@@ -104,20 +125,27 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
     for (int i = threadIdx.x; i < 256; i += B) s_tab[i] = i < 255 ? p.tab8[i] : 0;
     __syncthreads();
   }
-  const double alpha = epi_alpha(p.e);
-  double yy = 0.0, xy = 0.0;
+  // the power-step partial sums live in shared memory, not in registers
+  // across the slice loop (the loop runs at the 64-register cap of
+  // 1024-thread blocks; every register kept live there is a spill)
+  __shared__ double s_pw[2][B];
+  s_pw[0][threadIdx.x] = 0.0;
+  s_pw[1][threadIdx.x] = 0.0;
   // persistent: each warp walks slices warp0, warp0 + nwarps, ... so the
   // per-block epilogue (power-step partial sums) is paid once per block.
   for (int64_t slice = warp0; slice < p.nslices; slice += nwarps) {
-    int64_t base, stride, width;
+    // slot offsets need 64 bits (c5: 3.6·10⁹ slots); a k-step stride (n_pad
+    // or C) and a slice width fit 32 (fewer live registers in the loop)
+    int64_t base;
+    int stride, width;
     if (p.sp) {
       base = p.sp[slice];
-      width = (p.sp[slice + 1] - base) / C;
+      width = (int)((p.sp[slice + 1] - base) / C);
       stride = C;
     } else {
       base = slice * C;
-      width = p.ell_K;
-      stride = p.ell_stride;
+      width = (int)p.ell_K;
+      stride = (int)p.ell_stride;
     }
     const int32_t* __restrict__ cp = DOFF ? nullptr : p.col + base + lane * RPL;
     const int16_t* __restrict__ dp = D16 ? p.col16 + base + lane * RPL : nullptr;
@@ -135,17 +163,25 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
     }
     // One batch = U consecutive k-steps of the lane's RPL rows (values +
     // column indices), predicated past the slice width.
-    auto load_batch = [&](int64_t k, T (&v)[U][RPL], int (&c)[U][RPL]) {
+    constexpr int CU = PACK ? 1 : U, CR = PACK ? 1 : RPL;  // unpacked column array (unused when packed)
+    auto load_batch = [&](int k, T (&v)[U][RPL], int (&c)[CU][CR], uint32_t (&cw)[U]) {
+      // running row pointers (one 64-bit add per k-step) instead of per-step
+      // offsets k·stride + u·stride, which the compiler would keep live
+      const int64_t ks = (int64_t)k * stride;
+      const T* vrow = vp + ks;
+      const int32_t* crow = DOFF ? nullptr : cp + ks;
+      const int16_t* drow = D16 ? dp + ks : nullptr;
+      const uint8_t* brow = D8 ? bp + ks : nullptr;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < U; ++u, vrow += stride) {
         const bool ok = k + u < width;  // predicated tail batch
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
           T tv[VW];
           int tc[VW];
           if (ok) {
-            load_vals<T, VW>(vp + (k + u) * stride + q * VW, tv);
-            if constexpr (!DOFF) load_cols<VW>(cp + (k + u) * stride + q * VW, tc);
+            load_vals<T, VW>(vrow + q * VW, tv);
+            if constexpr (!DOFF) load_cols<VW>(crow + q * VW, tc);
           } else {
 #pragma unroll
             for (int w = 0; w < VW; ++w) {
@@ -159,27 +195,33 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
             if constexpr (!DOFF) c[u][q * VW + w] = tc[w];
           }
         }
+        if constexpr (!DOFF) crow += stride;
         if constexpr (D16) {
           int dd[RPL];
           if (ok) {
-            load_d16<RPL>(dp + (k + u) * stride, dd);
+            load_d16<RPL>(drow, dd);
           } else {
 #pragma unroll
             for (int r = 0; r < RPL; ++r) dd[r] = -32768;
           }
 #pragma unroll
           for (int r = 0; r < RPL; ++r) c[u][r] = dd[r] == -32768 ? -1 : rowv[r] + dd[r];
+          drow += stride;
         }
-        if constexpr (D8) {
+        if constexpr (PACK) {
+          cw[u] = ok ? load_c8_word<RPL>(brow) : 0xffffffffu;
+          brow += stride;
+        } else if constexpr (D8) {
           int dd[RPL];
           if (ok) {
-            load_c8<RPL>(bp + (k + u) * stride, dd);
+            load_c8<RPL>(brow, dd);
           } else {
 #pragma unroll
             for (int r = 0; r < RPL; ++r) dd[r] = 255;
           }
 #pragma unroll
           for (int r = 0; r < RPL; ++r) c[u][r] = dd[r] == 255 ? -1 : rowv[r] + s_tab[dd[r]];
+          brow += stride;
         }
       }
     };
@@ -188,29 +230,49 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
     // slower on c2 and c4: lower occupancy costs more than it hides).
     // CARRY = 1 guards the reload with a branch, CARRY = 0 predicates it.
     T v[U][RPL];
-    int c[U][RPL];
-    if (width > 0) load_batch(0, v, c);
-    for (int64_t k = 0; k < width; k += U) {
+    int c[CU][CR];
+    uint32_t cw[U];
+    if (width > 0) load_batch(0, v, c, cw);
+    for (int k = 0; k < width; k += U) {
       T vn[U][RPL];
-      int cn[U][RPL];
+      int cn[CU][CR];
+      uint32_t cwn[U];
       T xv[U][RPL];
+      if constexpr (PACK) {
+        int col[U][RPL];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int r = 0; r < RPL; ++r) xv[u][r] = c[u][r] >= 0 ? ld_x(x + c[u][r]) : T(0);
+          for (int r = 0; r < RPL; ++r) {
+            const uint32_t code = (cw[u] >> (8 * r)) & 0xffu;
+            col[u][r] = code == 255u ? -1 : rowv[r] + s_tab[code];
+          }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) xv[u][r] = col[u][r] >= 0 ? ld_x(x + col[u][r]) : T(0);
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) xv[u][r] = c[u][r] >= 0 ? ld_x(x + c[u][r]) : T(0);
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int r = 0; r < RPL; ++r) acc[r] = fma((double)v[u][r], (double)xv[u][r], acc[r]);
       if (!CARRY || k + U < width) {
-        load_batch(k + U, vn, cn);  // predicated: nothing is read past the width
+        load_batch(k + U, vn, cn, cwn);  // predicated: nothing is read past the width
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int u = 0; u < U; ++u) {
 #pragma unroll
-          for (int r = 0; r < RPL; ++r) {
-            v[u][r] = vn[u][r];
-            c[u][r] = cn[u][r];
-          }
+          for (int r = 0; r < RPL; ++r) v[u][r] = vn[u][r];
+          cw[u] = cwn[u];
+        }
+#pragma unroll
+        for (int u = 0; u < CU; ++u)
+#pragma unroll
+          for (int r = 0; r < CR; ++r) c[u][r] = cn[u][r];
       }
     }
     const int64_t r0 = slice * C + lane * RPL;
@@ -219,16 +281,16 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
       const int64_t ri = r0 + r;
       if (ri < p.rows) {
         const int64_t row = p.perm ? (int64_t)p.perm[ri] : ri;
-        const T out = epi_value<T>(p.e, alpha, acc[r], y, row);
+        const T out = epi_value<T>(p.e, epi_alpha(p.e), acc[r], y, row);
         y[row] = out;
         if (p.e.mode == 1) {
-          yy += (double)out * (double)out;
-          xy += (double)x[p.e.row_offset + row] * (double)out;
+          s_pw[0][threadIdx.x] += (double)out * (double)out;
+          s_pw[1][threadIdx.x] += (double)x[p.e.row_offset + row] * (double)out;
         }
       }
     }
   }
-  if (p.e.mode == 1) power_reduce(p.e, yy, xy);
+  if (p.e.mode == 1) power_reduce(p.e, s_pw[0][threadIdx.x], s_pw[1][threadIdx.x]);
 }
 
 

@@ -128,16 +128,11 @@ void coo_launch(spmv_matrix* h, const int32_t* row, const int32_t* col, const vo
     smem = kern::coo_tile_smem<T>(L.block, ept);
     per_chunk = (int64_t)L.block * ept;
   } else {
-    const bool wo = (W & kern::kCooWarpOrder) != 0;
-    const int w = W & 0xff;
-    per_chunk = 32LL * w;
-    switch (w) {
-      case 2: fn = wo ? (const void*)kern::coo_wo_fn<T, 2>(bi, ri) : (const void*)kern::coo_fn<T, 2>(bi, ri); break;
-      case 4: fn = wo ? (const void*)kern::coo_wo_fn<T, 4>(bi, ri) : (const void*)kern::coo_fn<T, 4>(bi, ri); break;
-      case 8: fn = wo ? (const void*)kern::coo_wo_fn<T, 8>(bi, ri) : (const void*)kern::coo_fn<T, 8>(bi, ri); break;
-      default:
-        fail(SPMV_ERR_INVALID_ARG,
-             "COO entries per lane must be 2, 4 or 8 (| kCooWarpOrder), or kCooTile | 4, 8, 16, 32");
+    switch (W) {
+      case 2: fn = (const void*)kern::coo_fn<T, 2>(bi, ri); break;
+      case 4: fn = (const void*)kern::coo_fn<T, 4>(bi, ri); break;
+      case 8: fn = (const void*)kern::coo_fn<T, 8>(bi, ri); break;
+      default: fail(SPMV_ERR_INVALID_ARG, "COO entries per lane must be 2, 4 or 8, or kCooTile | 4, 8, 16, 32");
     }
   }
   const LaunchAttrs attrs(fn, L.carveout_pct, smem);

@@ -61,6 +61,7 @@ void run_ell_arrays(spmv_matrix* h, const int32_t* col, const void* val, int64_t
   kern::SlicedParams p{};
   const int C = L.knob & 0xffff;
   if (C == 0 || n_pad % C != 0) fail(SPMV_ERR_UNSUPPORTED, "ELL rows-per-warp must divide n_pad (a multiple of 128)");
+  if (n_pad > INT32_MAX) fail(SPMV_ERR_UNSUPPORTED, "ELL: n_pad must fit 31 bits (the kernel's k-step stride)");
   p.col = col;
   p.col16 = col16;
   p.col8 = col8;

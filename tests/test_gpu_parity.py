@@ -250,8 +250,8 @@ def test_spmv_parity(name, dtype, fname, fmt, params):
     ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM), [16, 32, 64]),
     ("ELL", P.FMT_ELL, {}, [32, 64, 128, 64 | (1 << 16), 256 | (1 << 16)]),
     ("SELL", P.FMT_SELL, {}, [0, 64, 64 | (1 << 16)]),
-    ("COO", P.FMT_COO, {}, [2, 4, 8, 0x402, 0x404, 0x408, 0x104, 0x108, 0x110]),
-    ("HYB", P.FMT_HYB, {}, [2, 4, 8, 0x402, 0x404, 0x408, 0x104, 0x108, 0x110]),
+    ("COO", P.FMT_COO, {}, [2, 4, 8, 0x104, 0x108, 0x110]),
+    ("HYB", P.FMT_HYB, {}, [2, 4, 8, 0x104, 0x108, 0x110]),
     ("BELL", P.FMT_BELL, {"bell_b": 3}, [0])])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_launch_variants_parity(fname, fmt, params, knobs, dtype):
@@ -302,10 +302,9 @@ def test_csr_stream_tma_all_launches(case, dtype):
 
 @pytest.mark.parametrize("case", ["mixed_tiles", "long_rows", "rmat10", "stencil27_9", "ragged_empty"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("fmt", [P.FMT_COO, P.FMT_HYB, "merge", "merge-stream", "coo-wo", "hyb-wo"])
+@pytest.mark.parametrize("fmt", [P.FMT_COO, P.FMT_HYB, "merge", "merge-stream"])
 def test_coo_tile_all_launches(case, dtype, fmt):
-    """Row-interleaved COO tiles (knob 0x100 | EPT) and warp-order COO chunks
-    (0x400 | W, a 5-shuffle segmented scan per step with a carried run) over every block size and
+    """Row-interleaved COO tiles (knob 0x100 | EPT) over every block size and
     tile depth: rows crossing tiles (fixup records), rows longer than the
     thread pass takes (warp-cooperative pass), empty rows, the ragged last
     tile; plain COO, the HYB tail (accumulate mode) and merge-path CSR tiles
@@ -316,13 +315,12 @@ def test_coo_tile_all_launches(case, dtype, fmt):
     h = create(coo, dtype)
     try:
         ref = oracle_csr(coo)
-        flag = {"merge-stream": 0x200, "coo-wo": 0x400, "hyb-wo": 0x400}.get(fmt, 0x100)
-        epts = (2, 4, 8) if flag == 0x400 else (4, 8, 16, 32)
+        flag = 0x200 if fmt == "merge-stream" else 0x100
+        epts = (4, 8, 16, 32)
         if fmt in ("merge", "merge-stream"):
             fmt = P.FMT_CSR
             P.spmv_convert(h, fmt, csr_alg=P.CSR_MERGE)
         else:
-            fmt = {"coo-wo": P.FMT_COO, "hyb-wo": P.FMT_HYB}.get(fmt, fmt)
             P.spmv_convert(h, fmt)
         for block in (64, 128, 256, 512, 1024):
             for ept in epts:
