@@ -125,12 +125,17 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
     for (int i = threadIdx.x; i < 256; i += B) s_tab[i] = i < 255 ? p.tab8[i] : 0;
     __syncthreads();
   }
-  // the power-step partial sums live in shared memory, not in registers
-  // across the slice loop (the loop runs at the 64-register cap of
-  // 1024-thread blocks; every register kept live there is a spill)
-  __shared__ double s_pw[2][B];
-  s_pw[0][threadIdx.x] = 0.0;
-  s_pw[1][threadIdx.x] = 0.0;
+  // the power-step partial sums live in shared memory (one slot per warp,
+  // filled by a warp reduction at each slice end), not in registers across
+  // the slice loop: the loop runs at the 64-register cap of 1024-thread
+  // blocks, and every register kept live there is a spill. Per-warp slots
+  // keep the block's static shared memory small (a per-thread array would
+  // cut the residency of small blocks at carveout 0).
+  __shared__ double s_pw[B / 32][2];
+  if (lane == 0) {
+    s_pw[threadIdx.x >> 5][0] = 0.0;
+    s_pw[threadIdx.x >> 5][1] = 0.0;
+  }
   // persistent: each warp walks slices warp0, warp0 + nwarps, ... so the
   // per-block epilogue (power-step partial sums) is paid once per block.
   for (int64_t slice = warp0; slice < p.nslices; slice += nwarps) {
@@ -276,6 +281,7 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
       }
     }
     const int64_t r0 = slice * C + lane * RPL;
+    double yy = 0.0, xy = 0.0;
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       const int64_t ri = r0 + r;
@@ -284,13 +290,22 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
         const T out = epi_value<T>(p.e, epi_alpha(p.e), acc[r], y, row);
         y[row] = out;
         if (p.e.mode == 1) {
-          s_pw[0][threadIdx.x] += (double)out * (double)out;
-          s_pw[1][threadIdx.x] += (double)x[p.e.row_offset + row] * (double)out;
+          yy += (double)out * (double)out;
+          xy += (double)x[p.e.row_offset + row] * (double)out;
         }
       }
     }
+    if (p.e.mode == 1) {  // warp-uniform
+      yy = warp_sum(yy);
+      xy = warp_sum(xy);
+      if (lane == 0) {
+        s_pw[threadIdx.x >> 5][0] += yy;
+        s_pw[threadIdx.x >> 5][1] += xy;
+      }
+    }
   }
-  if (p.e.mode == 1) power_reduce(p.e, s_pw[0][threadIdx.x], s_pw[1][threadIdx.x]);
+  if (p.e.mode == 1)
+    power_reduce(p.e, lane == 0 ? s_pw[threadIdx.x >> 5][0] : 0.0, lane == 0 ? s_pw[threadIdx.x >> 5][1] : 0.0);
 }
 
 
