@@ -166,7 +166,7 @@ class Energy:
             return None
 
     def start_sampler(self, period_s=0.01):
-        if self.h is None:
+        if self.h is None or os.environ.get("BENCH_NO_POWER_SAMPLES"):
             return
 
         def run():
@@ -930,6 +930,7 @@ def run_rank(args, ctx: Ctx, shared: dict):
         host_phase_ms["between_steps"] = round(statistics.median(gaps), 3)
     # every timed step's device time and the device gaps between steps
     steps_ms = [round(st[0].elapsed_time(st[-1]), 3) for st in pe[: args.steps] if len(st) > 1]
+    steps_phase_ms = [[round(st[i].elapsed_time(st[i + 1]), 2) for i in range(len(st) - 1)] for st in pe[: args.steps]]
     dev_gaps = [round(pe[k][-1].elapsed_time(pe[k + 1][0]), 3) for k in range(min(len(pe), args.steps) - 1)]
     ms_max = ctx.reduce(ms, "max")
     nnz_total = ctx.reduce(float(nnz_local), "sum")
@@ -1083,6 +1084,7 @@ def run_rank(args, ctx: Ctx, shared: dict):
             "step_phases_ms": phase_ms,
             "host_phases_ms": host_phase_ms,
             "steps_ms": steps_ms, "device_gaps_ms": dev_gaps,
+            "steps_phase_ms": {"order": ev_names, "per_step": steps_phase_ms},
             "mflops_per_w": round(mflops_w, 1) if mflops_w else None,
             "energy": energy_rec,
             "cpu_baseline": None,
