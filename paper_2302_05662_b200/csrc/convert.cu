@@ -120,60 +120,6 @@ __global__ void k_ell_fill(const RP* __restrict__ rp, const int32_t* __restrict_
   }
 }
 
-// ELL fill through shared memory for narrow layouts (K <= kFillStageK): a
-// block of 128 threads owns 128 consecutive rows; their entries are one
-// contiguous range [rp[r0], rp[r0+128]), read coalesced into shared memory,
-// then each thread writes its row's K slots column-major (coalesced across the
-// block for every k). The thread-per-row kernel above reads each row's
-// entries straight from global memory: consecutive threads' k-th entries are
-// ~K entries apart, one L1TEX wavefront per lane.
-constexpr int kFillStageK = 64;
-constexpr int kFillRows = 128;
-__host__ __device__ constexpr int64_t fill_stage_slots(int64_t K) {
-  return (kFillRows * K + (kFillRows * K >> 5) + 16) / 16 * 16;
-}
-template <class RP, class V, class IDX>
-__global__ void __launch_bounds__(kFillRows) k_ell_fill_staged(const RP* __restrict__ rp, const int32_t* __restrict__ col,
-                                                                const V* __restrict__ val, int64_t rows, int64_t K,
-                                                                int64_t n_pad, IDX* __restrict__ colE,
-                                                                V* __restrict__ valE, int64_t origin, Dict8View dv) {
-  extern __shared__ __align__(16) unsigned char fill_smem[];
-  // staged entry e sits at e + e/32 (one skew slot per 32 entries, so rows of
-  // 32 entries — K apart in the stage — do not all land on one bank)
-  const int64_t cap = fill_stage_slots(K);
-  V* s_val = reinterpret_cast<V*>(fill_smem);
-  int32_t* s_col = reinterpret_cast<int32_t*>(fill_smem + (size_t)cap * sizeof(V));
-  auto sk = [](int64_t e) { return e + (e >> 5); };
-  const int t = threadIdx.x;
-  for (int64_t r0 = (int64_t)blockIdx.x * kFillRows; r0 < n_pad; r0 += (int64_t)gridDim.x * kFillRows) {
-    const int64_t i = r0 + t;
-    const int64_t lo = r0 < rows ? (int64_t)rp[r0] : 0;
-    const int64_t hi = r0 < rows ? (int64_t)rp[r0 + kFillRows < rows ? r0 + kFillRows : rows] : 0;
-    __syncthreads();  // the previous tile's readers are done
-    for (int64_t e = lo + t; e < hi; e += kFillRows) {
-      s_col[sk(e - lo)] = col[e];
-      s_val[sk(e - lo)] = val[e];
-    }
-    __syncthreads();
-    int64_t a = 0, L = 0;
-    if (i < rows) {
-      a = (int64_t)rp[i] - lo;
-      L = (int64_t)rp[i + 1] - lo - a;
-      if (L > K) L = K;
-    }
-    for (int64_t k = 0; k < K; ++k) {
-      const int64_t pos = k * n_pad + i;
-      if (k < L) {
-        colE[pos] = enc_col<IDX>(s_col[sk(a + k)], i, origin, dv);
-        valE[pos] = s_val[sk(a + k)];
-      } else {
-        colE[pos] = pad_col<IDX>();
-        valE[pos] = V(0);
-      }
-    }
-  }
-}
-
 // Largest |column − (origin + row)| over the first and last entry of every
 // row (columns are sorted within a row, so these bound all of them).
 template <class RP>
@@ -450,20 +396,7 @@ void ell_typed(spmv_matrix* h, int enc) {
   const V* val = static_cast<const V*>(h->val);
   lat_begin(h, SPMV_FMT_ELL);  // c_latency = device time of the conversion kernels (allocation excluded)
   const unsigned g = grid_for(n_pad, 256);
-  if (K <= kFillStageK) {
-    const size_t smem = (size_t)fill_stage_slots(K) * (sizeof(V) + 4);
-    const unsigned gs = grid_for(n_pad, kFillRows, (int64_t)kNumSMs * 16);
-    auto stage = [&](auto* colT) {
-      using IDX = std::remove_pointer_t<decltype(colT)>;
-      const void* fn = (const void*)k_ell_fill_staged<RP, V, IDX>;
-      const LaunchAttrs attrs(fn, -1, smem);
-      LAUNCH((k_ell_fill_staged<RP, V, IDX>), gs, kFillRows, smem, s, rp, h->col, val, h->rows, K, n_pad, colT, valE,
-             enc == 0 ? int64_t(0) : h->col_origin, dv);
-    };
-    if (enc == 2) stage(colE8);
-    else if (enc == 1) stage(colE16);
-    else stage(colE);
-  } else if (enc == 2)
+  if (enc == 2)
     LAUNCH((k_ell_fill<RP, V, uint8_t>), g, 256, 0, s, rp, h->col, val, h->rows, K, n_pad, colE8, valE,
            h->col_origin, dv);
   else if (enc == 1)
