@@ -781,6 +781,17 @@ def run_rank(args, ctx: Ctx, shared: dict):
     P.spmv_destroy(h)
     offline_s = time.perf_counter() - t_off
     offline = {"format": fmt, "params": params, "launch": launch}
+    # The offline phase left the stream-ordered pool holding its own mix of
+    # block sizes (full-matrix formats, slab candidates, tuning scratch). On
+    # c5 (≈ 79 GB of library memory per step next to ≈ 65 GB of inputs) a
+    # step's 29 GB value array then does not fit the fragmented cache, the pool
+    # grows into the device limit and the allocator's trim-and-retry path
+    # remaps everything (0.2–1.3 s stalls inside create/convert/select of the
+    # first steps, `steps_phase_ms`). Release the offline phase's memory so the
+    # warm-up steps build the pool from the step's own allocation pattern.
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    P.lib().spmv_trim_pool(int(local))
 
     comm = ctx.comm
     bufs = {
