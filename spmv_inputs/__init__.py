@@ -211,6 +211,42 @@ def random_coo(rows: int, cols: int, nnz: int, seed: int, dtype=np.float64,
     return COO(rows, cols, r, c, v.astype(dtype))
 
 
+def dense_band(n: int, half: int, seed: int = MATRIX_SEED, dtype=np.float64) -> COO:
+    """Row i holds every column of [i - half, i + half) inside [0, n): a
+    banded matrix with long, contiguous rows (2·half entries away from the
+    edges) — the long-row case of the §8(d) families."""
+    w = 2 * half
+    r = np.repeat(np.arange(n, dtype=np.int64), w)
+    c = r - half + np.tile(np.arange(w, dtype=np.int64), n)
+    keep = (c >= 0) & (c < n)
+    r, c = r[keep].astype(np.int32), c[keep].astype(np.int32)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    v = value_of(rng.integers(0, np.iinfo(np.uint64).max, size=r.shape[0], dtype=np.uint64, endpoint=True))
+    return COO(n, n, r, c, v.astype(dtype))
+
+
+def lap2d_long_rows(N: int, every: int, extra: int, seed: int = MATRIX_SEED, dtype=np.float64) -> COO:
+    """2D 5-point stencil on an N×N grid where every `every`-th row also holds
+    columns i+2 .. i+1+extra (extra < N-2; none of them is a stencil column):
+    short regular rows mixed with a few long local rows (the short/long-row
+    mix of the §8(d) families). Rows sorted, columns sorted within a row."""
+    assert extra < N - 2
+    base = lap2d(N, random_values=True, dtype=np.float64)
+    n = base.rows
+    long_rows = np.arange(0, n, every, dtype=np.int64)
+    er = np.repeat(long_rows, extra)
+    ec = er + 2 + np.tile(np.arange(extra, dtype=np.int64), long_rows.shape[0])
+    keep = ec < n
+    er, ec = er[keep], ec[keep]
+    r = np.concatenate([base.row.astype(np.int64), er])
+    c = np.concatenate([base.col.astype(np.int64), ec])
+    order = np.argsort(r * n + c, kind="stable")
+    r, c = r[order].astype(np.int32), c[order].astype(np.int32)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    v = value_of(rng.integers(0, np.iinfo(np.uint64).max, size=r.shape[0], dtype=np.uint64, endpoint=True))
+    return COO(n, n, r, c, v.astype(dtype))
+
+
 def shuffled(coo: COO, seed: int) -> COO:
     rng = np.random.Generator(np.random.PCG64(seed))
     p = rng.permutation(coo.nnz)

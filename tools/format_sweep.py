@@ -15,6 +15,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2302_05662_b200 as P  # noqa: E402
@@ -61,16 +62,39 @@ def time_kernel(h, fmt, x, y, reps=None):
     return statistics.median(ts) * 1e-3
 
 
+# Extra matrices for the "best-suited matrix" pass bar: each
+# family's large member, every format measured on every one of them, all
+# arrays > L2 (126 MB).
+EXTRA = {
+    # short regular rows (5 per row): COO's entry-order gathers stay within 3 x lines per 32 entries
+    "lap2d_4096": lambda: si.stencil_device(si.LAP2D, 4096, random_values=True),
+    # long contiguous rows (64 per row): warp-per-row CSR-vector reads whole lines of col/val and x
+    "band64_2M": lambda: si.dense_band(1 << 21, 32),
+    # short/long-row mix (5-point rows + every 2048th row with 2048 more local entries): HYB / merge-path
+    "lap2d_long_4096": lambda: si.lap2d_long_rows(4096, 2048, 2048),
+}
+
+
+def load(name):
+    if name in EXTRA:
+        coo = EXTRA[name]()
+        return coo
+    return si.config_device(name)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="c1,c2,c3,c4")
+    ap.add_argument("--configs", default="c1,c2,c3,c4", help="BASELINE configs and/or " + ",".join(EXTRA))
     ap.add_argument("--out", default="gpurun_out/format_sweep")
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--formats", default="", help="comma list of variant names (default all)")
     args = ap.parse_args()
     results = []
     for cfg in args.configs.split(","):
-        coo = si.config_device(cfg)
+        coo = load(cfg)
+        if isinstance(coo.val, np.ndarray):
+            coo = si.COO(coo.rows, coo.cols, torch.from_numpy(coo.row).cuda(), torch.from_numpy(coo.col).cuda(),
+                         torch.from_numpy(coo.val).cuda())
         dt = coo.val.dtype
         vb = 4 if dt == torch.float32 else 8
         x = si.vector_device(coo.cols, dtype=dt)
