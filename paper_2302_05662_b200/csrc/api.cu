@@ -386,7 +386,8 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
     case SPMV_FMT_CSR:
       if (h->csr_alg == SPMV_CSR_MERGE)  // per-warp merge walk, or row-interleaved tiles of block·IPT items
         return {4, 8, 16, kern::kMergeTile | 4, kern::kMergeTile | 8, kern::kMergeTile | 16, kern::kMergeTile | 32,
-                kern::kMergeStream | 4, kern::kMergeStream | 8, kern::kMergeStream | 16, kern::kMergeStream | 32};
+                kern::kMergeStream | 4, kern::kMergeStream | 8, kern::kMergeStream | 16, kern::kMergeStream | 32,
+                kern::kMergeNnz | 4, kern::kMergeNnz | 8};
       if (h->csr_alg == SPMV_CSR_STREAM) return {16, 32, 64};
       {
         int t = csr_default_lanes(h);
@@ -852,6 +853,7 @@ static void destroy_handle(spmv_matrix* h) {
   dfree(h->seg_scratch, h->stream);
   dfree(h->fix_scratch, h->stream);
   dfree(h->merge_coords, h->stream);
+  dfree(h->csr_empty, h->stream);
   dfree(h->dict8_map, h->stream);
   dfree(h->dict8_tab, h->stream);
   dfree(h->pi_partials, h->stream);

@@ -728,6 +728,30 @@ void build_bell(spmv_matrix* h, int64_t b) {
   });
 }
 
+template <class RP>
+void csr_empty_typed(spmv_matrix* h) {
+  cudaStream_t s = h->stream;
+  const int64_t rows = h->rows;
+  Scratch sc(s);
+  const RP* rp = static_cast<const RP*>(h->row_ptr);
+  int64_t* flag = sc.get<int64_t>(rows);
+  int64_t* off = sc.get<int64_t>(rows + 1);
+  LAUNCH(k_row_counts<RP>, grid_for(rows, 256), 256, 0, s, rp, rows, 0, (int64_t)0, flag);
+  exclusive_scan_i64(flag, off, rows, s);
+  const int64_t n_empty = read_i64(off + rows, s);
+  int32_t* empty = sc.get<int32_t>(n_empty);
+  if (n_empty > 0) LAUNCH(k_compact_empty<RP>, grid_for(rows, 256), 256, 0, s, rp, (const int64_t*)off, rows, empty);
+  sc.keep(empty);
+  h->csr_empty = empty;
+  h->csr_n_empty = n_empty;
+}
+
+void build_csr_empty(spmv_matrix* h) {
+  if (h->csr_n_empty >= 0) return;
+  if (h->rp64) csr_empty_typed<int64_t>(h);
+  else csr_empty_typed<int32_t>(h);
+}
+
 void build_coo(spmv_matrix* h) {
   dispatch(h, [&](auto rpt, auto vt) {
     using RP = std::remove_pointer_t<decltype(rpt)>;

@@ -100,6 +100,11 @@ struct spmv_matrix {
   int64_t* merge_coords = nullptr;
   int64_t merge_coords_n = 0;
   int merge_coords_ipt = 0;  // merge items per chunk the cached coordinates were computed for
+                             // (negative: entries per chunk of the nnz-split partition)
+  // rows without entries, ascending (CSR; the nnz-split merge variant writes
+  // them in a separate pass), built on first use (csr_n_empty = -1 until then)
+  int32_t* csr_empty = nullptr;
+  int64_t csr_n_empty = -1;
   double* pi_partials = nullptr;
   unsigned* pi_counter = nullptr;
   size_t pi_partials_n = 0;
@@ -122,6 +127,8 @@ void compute_features(spmv_matrix* h);
 
 // convert.cu
 void build_coo(spmv_matrix* h);
+// h->csr_empty / csr_n_empty (rows of the CSR without entries); once per handle.
+void build_csr_empty(spmv_matrix* h);
 // index16 (column encoding): 0 = int32 columns, 1 = 16-bit offsets, 2 = 8-bit
 // codes into the offset dictionary (SPMV_ERR_UNSUPPORTED if the encoding does
 // not fit), -1 = the narrowest that fits (8-bit, then 16-bit, then int32).

@@ -772,6 +772,175 @@ constexpr CsrFn merge_stream_ptr() {
   else return &k_csr_merge_stream<B, R, T, I, RP>;
 }
 
+// nnz-split CSR (the merge-path family's load balance over the nonzeros:
+// knob kMergeNnz | W). A warp owns the 32·W consecutive entries [base, base +
+// 32·W) (every warp the same work, however long or short the rows: P:159's
+// imbalance is gone); lane l loads its W entries [base + l·W, ...) with
+// 128-bit loads of col and val (the vector loads of COO, without COO's row
+// array) and gathers x for all W. The row of each entry comes from the row
+// pointers: the cached partition gives the row holding the warp's first
+// entry and the row holding the entry after its last, the lane binary-searches
+// its first row in that window and, when an entry passes the row's end,
+// the next row the same way (empty rows in between cost nothing).
+// Runs of one row inside the lane are summed there; runs crossing lanes are
+// combined by a 5-step warp segmented scan keyed by the row (COO's
+// reduction), rows crossing warps by chunk records + k_seg_fixup, rows
+// without entries by a separate pass over the handle's empty-row list.
+template <int B, int R, class T, int W, class RP>
+__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_nnz(const CsrParams p) {
+  constexpr int VW = (int)(16 / sizeof(T));  // values per 128-bit load
+  const int lane = threadIdx.x & 31;
+  const int64_t chunk = ((int64_t)blockIdx.x * B + threadIdx.x) >> 5;
+  if (chunk >= p.nchunks) return;  // warp-uniform
+  const RP* __restrict__ rp = static_cast<const RP*>(p.rp);
+  const T* __restrict__ val = static_cast<const T*>(p.val);
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  T* __restrict__ y = static_cast<T*>(p.y);
+  const double alpha = epi_alpha(p.e);
+  const int64_t base = chunk * 32 * W;
+  const int64_t end = base + 32 * W;
+  const int64_t k0 = base + (int64_t)lane * W;
+  const int64_t rlo = p.coords[chunk], rhi = p.coords[chunk + 1];  // rows holding entries base and end
+  int c[W];
+  T v[W];
+  if (k0 + W <= p.nnz) {
+#pragma unroll
+    for (int q = 0; q < W; q += 4) {
+      int t4[4];
+      load_cols<4>(p.col + k0 + q, t4);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[q + u] = t4[u];
+    }
+#pragma unroll
+    for (int q = 0; q < W; q += VW) {
+      T tv[VW];
+      load_vals<T, VW>(val + k0 + q, tv);
+#pragma unroll
+      for (int u = 0; u < VW; ++u) v[q + u] = tv[u];
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const bool ok = k0 + q < p.nnz;
+      c[q] = ok ? p.col[k0 + q] : -1;
+      v[q] = ok ? val[k0 + q] : T(0);
+    }
+  }
+  double prod[W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) prod[q] = c[q] >= 0 ? (double)v[q] * (double)ld_x(x + c[q]) : 0.0;
+  // rows of the lane's entries (overlaps the gathers): first row by binary
+  // search in [rlo, rhi] (rp[lo] <= k0 < rp[hi + 1]), then forward
+  int r[W];
+  if (k0 < p.nnz) {
+    int64_t lo = rlo, hi = rhi;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if ((int64_t)__ldg(rp + mid) <= k0) lo = mid;
+      else hi = mid - 1;
+    }
+    int64_t row = lo, next = (int64_t)__ldg(rp + row + 1);
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const int64_t k = k0 + q;
+      if (k < p.nnz) {
+        if (k >= next) {  // a later row (empty rows in between are skipped by the search)
+          int64_t a = row + 1, b = rhi;
+          while (a < b) {
+            const int64_t mid = (a + b + 1) >> 1;
+            if ((int64_t)__ldg(rp + mid) <= k) a = mid;
+            else b = mid - 1;
+          }
+          row = a;
+          next = (int64_t)__ldg(rp + row + 1);
+        }
+        r[q] = (int)row;
+      } else {
+        r[q] = INT_MAX;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; ++q) r[q] = INT_MAX;
+  }
+  const int chunk_first = (int)rlo;
+  const bool cont_in = base > 0 && (int64_t)__ldg(rp + rlo) < base;
+  // lane-local runs (as k_coo): rows strictly inside the lane are complete here
+  const int first = r[0];
+  double first_sum = 0.0, run = 0.0;
+  bool first_closed = false;
+  int cur = r[0];
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    if (r[q] != cur) {
+      if (!first_closed) {
+        first_sum = run;
+        first_closed = true;
+      } else {
+        y[cur] = epi_value<T>(p.e, alpha, run, y, cur);
+      }
+      cur = r[q];
+      run = 0.0;
+    }
+    run += prod[q];
+  }
+  const int last = cur;
+  if (!first_closed) first_sum = run;
+  double s = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double su = __shfl_up_sync(0xffffffffu, s, o);
+    const int ku = __shfl_up_sync(0xffffffffu, last, o);
+    if (lane >= o && ku == last) s += su;
+  }
+  const double s_prev = __shfl_up_sync(0xffffffffu, s, 1);
+  const int k_prev = __shfl_up_sync(0xffffffffu, last, 1);
+  const double carry_in = (lane > 0 && k_prev == first) ? s_prev : 0.0;
+  int next_first = __shfl_down_sync(0xffffffffu, r[0], 1);
+  if (lane == 31) next_first = end < p.nnz ? (int)rhi : INT_MAX;
+  if (first_closed && first != INT_MAX) {
+    const double tot = carry_in + first_sum;
+    if (cont_in && first == chunk_first) p.recs[chunk].head = tot;
+    else y[first] = epi_value<T>(p.e, alpha, tot, y, first);
+  }
+  if (last != INT_MAX) {
+    if (next_first != last) {
+      if (cont_in && last == chunk_first) p.recs[chunk].head = s;
+      else y[last] = epi_value<T>(p.e, alpha, s, y, last);
+    } else if (lane == 31) {
+      p.recs[chunk].tail = s;
+      if (cont_in && last == chunk_first) p.recs[chunk].head = s;
+    }
+  }
+  const unsigned valid = __ballot_sync(0xffffffffu, r[0] != INT_MAX);
+  const int lastv = __shfl_sync(0xffffffffu, last, 31 - __clz((int)valid));
+  if (lane == 31) {
+    ChunkRec& rec = p.recs[chunk];
+    rec.first_row = chunk_first;
+    rec.cont_in = cont_in;
+    rec.last_row = lastv;
+    rec.cont_out = (next_first == last) && last != INT_MAX;
+  }
+}
+
+// nnz-split partition: coords[c] = the row holding entry c·per (rows when
+// c·per >= nnz): the largest r with rp[r] <= c·per.
+template <class RP>
+__global__ void k_nnz_partition(const RP* __restrict__ rp, int64_t rows, int64_t nnz, int64_t per, int64_t nchunks,
+                                int64_t* __restrict__ coords) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= nchunks; c += stride) {
+    const int64_t k = c * per < nnz ? c * per : nnz;
+    int64_t lo = 0, hi = rows;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if ((int64_t)rp[mid] <= k) lo = mid;
+      else hi = mid - 1;
+    }
+    coords[c] = k >= nnz ? rows : lo;
+  }
+}
+
 template <int B, int R, class T, int I, class RP>
 constexpr CsrFn merge_tile_ptr() {
   if constexpr (merge_tile_smem<T>(B, I) > 200 * 1024) return nullptr;
@@ -840,6 +1009,16 @@ CsrFn csr_merge_tile_fn(int bi, int ri) {
   return tab[bi][ri];
 }
 #undef CSRMT_ROW
+
+#define CSRN_ROW(B, W) {&k_csr_nnz<B, 32, T, W, RP>, &k_csr_nnz<B, 64, T, W, RP>, \
+                        &k_csr_nnz<B, 128, T, W, RP>, &k_csr_nnz<B, 255, T, W, RP>}
+template <class T, class RP, int W>
+CsrFn csr_nnz_fn(int bi, int ri) {
+  static const CsrFn tab[5][4] = {CSRN_ROW(64, W), CSRN_ROW(128, W), CSRN_ROW(256, W), CSRN_ROW(512, W),
+                                  CSRN_ROW(1024, W)};
+  return tab[bi][ri];
+}
+#undef CSRN_ROW
 
 #define CSRM_ROW(B, I) {&k_csr_merge<B, 32, T, I, RP>, &k_csr_merge<B, 64, T, I, RP>, \
                         &k_csr_merge<B, 128, T, I, RP>, &k_csr_merge<B, 255, T, I, RP>}

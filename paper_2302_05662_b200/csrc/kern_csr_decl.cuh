@@ -83,6 +83,14 @@ template <class T, class RP>
 constexpr size_t merge_stream_smem(int block, int ipt) {
   return (size_t)kStreamStages * MergeStage<T, RP>::bytes(block * ipt);
 }
+// nnz-split CSR of the merge-path family (k_csr_nnz): knob kMergeNnz | W,
+// a warp owns 32·W consecutive entries (W = 4 or 8).
+constexpr int kMergeNnz = 0x400;
+template <class T, class RP, int W>
+CsrFn csr_nnz_fn(int bi, int ri);
+// nnz-split partition: coords[c] = row holding entry c·per (rows past the end), c = 0..nchunks.
+void nnz_partition(const void* rp, bool rp64, int64_t rows, int64_t nnz, int64_t per, int64_t nchunks,
+                   int64_t* coords, cudaStream_t s);
 // Merge-path partition pre-pass: coords[2c], coords[2c+1] = start of chunk c.
 void merge_partition(const void* rp, bool rp64, int64_t rows, int64_t nnz, int64_t items_per_chunk,
                      int64_t nchunks, int64_t* coords, cudaStream_t s);

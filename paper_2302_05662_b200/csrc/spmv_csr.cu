@@ -68,6 +68,39 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
     return;
   }
+  if (L.knob & kern::kMergeNnz) {
+    // nnz-split chunks: 32·W entries per warp; empty rows from the handle's list
+    const int W = L.knob & 0xff;
+    const void* fn;
+    switch (W) {
+      case 4: fn = (const void*)kern::csr_nnz_fn<T, RP, 4>(bi, ri); break;
+      case 8: fn = (const void*)kern::csr_nnz_fn<T, RP, 8>(bi, ri); break;
+      default: fail(SPMV_ERR_INVALID_ARG, "nnz-split CSR entries per lane must be 4 or 8");
+    }
+    if (((uintptr_t)h->col | (uintptr_t)h->val) & 15)
+      fail(SPMV_ERR_UNSUPPORTED, "nnz-split CSR: col/val must be 16-byte aligned for the vector loads");
+    build_csr_empty(h);
+    run_rows_scale(h, h->csr_empty, h->csr_n_empty, e, y);  // disjoint from every row the chunks write
+    if (h->nnz <= 0) return;
+    const int64_t per = 32LL * W;
+    const int64_t nchunks = (h->nnz + per - 1) / per;
+    const LaunchAttrs attrs(fn, L.carveout_pct);
+    p.recs = static_cast<ChunkRec*>(ensure_seg_scratch(h, (size_t)nchunks * sizeof(ChunkRec)));
+    if (!h->merge_coords || h->merge_coords_ipt != -per || h->merge_coords_n != nchunks) {
+      dfree(h->merge_coords, h->stream);
+      h->merge_coords = nullptr;
+      h->merge_coords = static_cast<int64_t*>(dalloc((size_t)(nchunks + 1) * sizeof(int64_t), h->stream));
+      kern::nnz_partition(h->row_ptr, h->rp64, h->rows, h->nnz, per, nchunks, h->merge_coords, h->stream);
+      h->merge_coords_ipt = (int)-per;
+      h->merge_coords_n = nchunks;
+    }
+    p.coords = h->merge_coords;
+    p.nchunks = nchunks;
+    void* args[] = {&p};
+    launch_checked(fn, dim3((unsigned)((nchunks * 32 + L.block - 1) / L.block)), dim3(L.block), args, 0, h->stream);
+    run_seg_fixup(h, p.recs, nchunks, e, y);
+    return;
+  }
   const bool tile = (L.knob & kern::kMergeTile) != 0, pipe = (L.knob & kern::kMergeStream) != 0;
   const int ipt = L.knob & 0xff;
   if (tile && pipe) fail(SPMV_ERR_INVALID_ARG, "merge-path knob: kMergeTile and kMergeStream are exclusive");

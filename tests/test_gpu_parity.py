@@ -246,7 +246,8 @@ def test_spmv_parity(name, dtype, fname, fmt, params):
 
 @pytest.mark.parametrize("fname,fmt,params,knobs", [
     ("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR), [1, 2, 4, 8, 16, 32]),
-    ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), [4, 8, 16, 0x104, 0x108, 0x110, 0x204, 0x208, 0x210]),
+    ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), [4, 8, 16, 0x104, 0x108, 0x110, 0x204, 0x208, 0x210,
+                                                         0x404, 0x408]),
     ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM), [16, 32, 64]),
     ("ELL", P.FMT_ELL, {}, [32, 64, 128, 64 | (1 << 16), 256 | (1 << 16)]),
     ("SELL", P.FMT_SELL, {}, [0, 64, 64 | (1 << 16)]),
@@ -331,6 +332,39 @@ def test_coo_tile_all_launches(case, dtype, fmt):
                 except P.SpmvError as ex:   # tile over the shared-memory cap / block + producer warp > 1024
                     assert ex.status == P.ERR_UNSUPPORTED and (block * ept >= 4096 or block == 1024)
                     torch.cuda.synchronize()
+    finally:
+        P.spmv_destroy(h)
+
+
+@pytest.mark.parametrize("case", ["mixed_tiles", "long_rows", "rmat10", "stencil27_9", "ragged_empty"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_csr_nnz_split_all_launches(case, dtype):
+    """nnz-split CSR of the merge-path family (knob 0x400 | W): warps of 32·W
+    entries with vector loads, rows from the row pointers (binary search in
+    the cached partition window, then forward), lane runs + warp segmented
+    scan, rows crossing warps through the fixup, hub rows spanning many warps
+    (long-run fixup), empty rows from the handle's list, the ragged last warp:
+    O9 parity, NaN y with beta = 0, bitwise repeatable; switching back to a
+    merge-path variant recomputes its own partition."""
+    coo = CASES[case]
+    h = create(coo, dtype)
+    try:
+        ref = oracle_csr(coo)
+        P.spmv_convert(h, P.FMT_CSR, csr_alg=P.CSR_MERGE)
+        for block in (64, 128, 256, 512, 1024):
+            for W in (4, 8):
+                P.spmv_set_launch(h, P.FMT_CSR, block, 64 if block <= 512 else 32, -1, 0x400 | W)
+                check_y(h, coo, dtype, P.FMT_CSR, 2.5, -0.5, ref)
+                y1 = check_y(h, coo, dtype, P.FMT_CSR, 1.0, 0.0, ref, nan_y=True)
+                y2 = check_y(h, coo, dtype, P.FMT_CSR, 1.0, 0.0, ref, nan_y=True)
+                assert y1.tobytes() == y2.tobytes()
+                P.spmv_set_launch(h, P.FMT_CSR, 128, 64, -1, 8)           # per-warp merge walk in between
+                check_y(h, coo, dtype, P.FMT_CSR, 1.0, 0.0, ref, nan_y=True)
+        with pytest.raises(P.SpmvError) as ex:
+            P.spmv_set_launch(h, P.FMT_CSR, 128, 64, -1, 0x400 | 16)
+            check_y(h, coo, dtype, P.FMT_CSR, 1.0, 0.0, ref)
+        assert ex.value.status == P.ERR_INVALID_ARG
+        torch.cuda.synchronize()
     finally:
         P.spmv_destroy(h)
 
