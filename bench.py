@@ -69,7 +69,7 @@ def parse(argv=None):
                     help="per-step run-time selection: predict (timed select phase) or replay the offline choice")
     ap.add_argument("--no-tune-launch", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--per-config", default="c2,c3,c4", help="N=1 extra configs measured after the headline "
+    ap.add_argument("--per-config", default="c1,c2,c3,c4", help="N=1 extra configs measured after the headline "
                                                                 "('none' to skip)")
     ap.add_argument("--launch", default="", help="block,maxreg,carveout,knob (skips the launch sweep)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -631,6 +631,52 @@ def time_plain(P, h, fmt, x, y, min_ms=200.0):
     return statistics.median(ts) * 1e-3, reps
 
 
+def c1_graph_leg(args, P, si):
+    """c1 (64×64 5-point Laplacian, 20 K nonzeros) is launch-bound (SURVEY
+    §8(d)): the E-step power loop on the tuned format, eager (one launch per
+    step from the C++ loop) vs replayed as a CUDA graph
+    (spmv_power_iterate_graph), µs per step from CUDA events on the stream."""
+    import torch
+    try:
+        coo = si.config_device("c1")
+        n = coo.rows
+        h = P.spmv_create(n, coo.cols, coo.row, coo.col, coo.val)
+        P.spmv_features(h)
+        rep = P.spmv_tune(h, P.TUNE_FORMAT | P.TUNE_LAUNCH, expected_iterations=args.iters)
+        fmt = rep.format
+        E = args.iters
+        x0 = si.vector_device(n, dtype=coo.val.dtype)
+        b0, b1 = torch.zeros_like(x0), torch.zeros_like(x0)
+        sums = torch.zeros(E + 1, 2, dtype=torch.float64, device="cuda")
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+        def timed(fn, reps=20):
+            for _ in range(3):
+                fn()
+            ts = []
+            for _ in range(5):
+                e0.record(st)
+                for _ in range(reps):
+                    fn()
+                e1.record(st)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1) / reps / E * 1e3)
+            return round(statistics.median(ts), 3)
+
+        eager = timed(lambda: P.spmv_power_iterate(h, x0, b0, b1, E, sums))
+        graph = timed(lambda: P.spmv_power_iterate_graph(h, x0, b0, b1, E, sums))
+        label = P.FORMAT_NAMES[fmt]
+        launch = list(P.spmv_get_launch(h, fmt))
+        P.spmv_destroy(h)
+        return {"nnz": int(coo.nnz), "n": int(n), "format": label, "launch": launch,
+                "power_steps": E, "us_per_step_eager": eager, "us_per_step_graph": graph,
+                "speedup_graph": round(eager / graph, 3) if graph else None,
+                "GFLOPs_graph": round(2 * coo.nnz / (graph * 1e-6) / 1e9, 2) if graph else None}
+    except Exception as ex:  # report, never fall back
+        return {"error": repr(ex)[:200]}
+
+
 def per_config_leg(args, P, si, peak):
     """c2/c3/c4 at N = 1: measured run-time + compile-time modes (spmv_tune
     FORMAT|LAUNCH), the chosen kernel timed as a plain SpMV; c3/c4 also
@@ -640,6 +686,10 @@ def per_config_leg(args, P, si, peak):
     gc = None
     for cfg in [c for c in args.per_config.split(",") if c and c != "none"]:
         t_cfg = time.perf_counter()
+        if cfg == "c1":
+            out[cfg] = c1_graph_leg(args, P, si)
+            out[cfg]["leg_seconds"] = round(time.perf_counter() - t_cfg, 1)
+            continue
         try:
             coo = si.config_device(cfg)
             dt = coo.val.dtype

@@ -357,6 +357,22 @@ spmv_status_t spmv_power_iterate(spmv_handle_t h, const void* x0, void* buf0, vo
  *   all-gather of whole chunks; kept only if every rank then receives less
  *   than half of what the all-gather moves (collective decision).
  * Collective: every rank of comm must call it. Synchronous. */
+/* The single-GPU power iteration of spmv_power_iterate (comm = NULL) as a
+ * CUDA graph: the first call with a given (x0, buf0, buf1, n_full, steps,
+ * sums) runs the loop eagerly — its result is that call's result, and lazily
+ * built scratch, partitions and kernel attributes are set up outside any
+ * capture — then captures the same launches (on a private stream) and
+ * instantiates them; later calls with the same arguments replay the graph on
+ * the handle's stream with one cudaGraphLaunch (the E·(1..3) kernel launches
+ * of a loop cost one host call: what matters for small, launch-bound
+ * matrices). Any spmv_convert / set_format / set_launch / tune /
+ * set_stream / release_csr invalidates the graph (re-captured on the next
+ * call). The graph lives with the handle (freed by spmv_destroy). No timing
+ * outputs; *final_buf as in spmv_power_iterate. Errors as spmv_power_iterate;
+ * SPMV_ERR_CUDA if capture or instantiation fails. */
+spmv_status_t spmv_power_iterate_graph(spmv_handle_t h, const void* x0, void* buf0, void* buf1, int64_t n_full,
+                                       int64_t steps, double* sums, int* final_buf);
+
 #define SPMV_PLAN_OVERLAP 1u
 #define SPMV_PLAN_HALO 2u
 typedef struct spmv_dist_plan* spmv_dist_plan_t;
@@ -413,6 +429,19 @@ size_t spmv_decision_log(spmv_handle_t h, char* buf, size_t len);
 /* Conversion timings measured on the device by the last spmv_create /
  * spmv_convert / spmv_features calls, seconds (c_latency per format, f_latency). */
 spmv_status_t spmv_overheads(spmv_handle_t h, double* f_latency_s, double* c_latency_s /*[SPMV_NUM_FORMATS]*/);
+
+/* Free the handle's CSR arrays (row_ptr, col, val) and the COO arrays that
+ * share them, keeping the active format (ELL, SELL, HYB or BELL: formats
+ * with their own arrays) and the computed features: after conversion the
+ * SpMV and the power iteration read only the active format (P:145 — the
+ * format is the kernel's input), so a pipeline that converts once and then
+ * iterates can hold one copy of the matrix instead of two. Afterwards every
+ * call that reads CSR (spmv_convert, spmv_tune, spmv_features if not yet
+ * computed, spmv_create_row_slice, spmv_dist_plan_create, runs/copies of CSR
+ * or COO) returns SPMV_ERR_NOT_CONVERTED. Stream-ordered frees, no host
+ * synchronisation. Errors: SPMV_ERR_INVALID_ARG if h is NULL or the active
+ * format is CSR or COO; releasing twice is a no-op. */
+spmv_status_t spmv_release_csr(spmv_handle_t h);
 
 /* Number of CUDA kernels this library has launched in this process. */
 uint64_t spmv_launch_count(void);

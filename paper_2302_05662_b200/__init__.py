@@ -144,6 +144,8 @@ def lib():
         "spmv_overheads": ([H, ctypes.POINTER(d), ctypes.POINTER(d)], i32),
         "spmv_launch_count": ([], ctypes.c_uint64),
         "spmv_trim_pool": ([i32], i32),
+        "spmv_release_csr": ([H], i32),
+        "spmv_power_iterate_graph": ([H, vp, vp, vp, i64, i64, vp, ctypes.POINTER(ctypes.c_int)], i32),
         "spmv_power_iterate": ([H, vp, vp, vp, i64, i64, vp, vp, i64, vp, ctypes.POINTER(ctypes.c_float),
                                 ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int)], i32),
         "spmv_predict": ([ctypes.POINTER(Features), i32, ctypes.POINTER(Prediction)], i32),
@@ -227,6 +229,11 @@ def spmv_create(rows, cols, row_idx, col_idx, vals, device: int = 0, stream=None
     return h
 
 
+def spmv_release_csr(h):
+    """Free the CSR/COO arrays after conversion (include/spmv.h)."""
+    _check(lib().spmv_release_csr(h), h)
+
+
 def spmv_convert(h, fmt, csr_alg=0, csr_T=0, sell_C=0, sell_sigma=0, hyb_K=-1, bell_b=0, index16=0):
     p = FormatParams(csr_alg, csr_T, sell_C, sell_sigma, hyb_K, bell_b, index16)
     _check(lib().spmv_convert(h, fmt, ctypes.byref(p)), h)
@@ -276,6 +283,15 @@ def spmv_tune(h, flags=TUNE_ALL, expected_iterations=100, objective="latency"):
 
 def spmv_power_step(h, x, y, sums_prev, sums_out, row_offset=0):
     _check(lib().spmv_power_step(h, _ptr(x), _ptr(y), _ptr(sums_prev), _ptr(sums_out), int(row_offset)), h)
+
+
+def spmv_power_iterate_graph(h, x0, buf0, buf1, steps, sums):
+    """The single-GPU power loop replayed as a CUDA graph (see spmv.h).
+    Returns the index (0/1) of the buffer holding z_E."""
+    fb = ctypes.c_int(0)
+    _check(lib().spmv_power_iterate_graph(h, _ptr(x0), _ptr(buf0), _ptr(buf1), int(buf0.numel()), int(steps),
+                                          _ptr(sums), ctypes.byref(fb)), h)
+    return fb.value
 
 
 def spmv_power_iterate(h, x0, buf0, buf1, steps, sums, comm=None, chunk=0, chunk_buf=None,

@@ -203,14 +203,20 @@ spmv_launch_t resolve_launch(const spmv_matrix* h, int fmt, const spmv_launch_t&
 
 static bool built(const spmv_matrix* h, int fmt) {
   switch (fmt) {
-    case SPMV_FMT_CSR: return true;
-    case SPMV_FMT_COO: return h->coo_built;
+    case SPMV_FMT_CSR: return !h->csr_released;
+    case SPMV_FMT_COO: return h->coo_built && !h->csr_released;
     case SPMV_FMT_ELL: return h->ell_built;
     case SPMV_FMT_SELL: return h->sell_built;
     case SPMV_FMT_HYB: return h->hyb_built;
     case SPMV_FMT_BELL: return h->bell_built;
   }
   return false;
+}
+
+// Entry points that read the CSR arrays (conversions, features, tuning, row slices).
+static void need_csr(const spmv_matrix* h, const char* what) {
+  if (h->csr_released)
+    fail(SPMV_ERR_NOT_CONVERTED, std::string(what) + ": the CSR arrays were released (spmv_release_csr)");
 }
 
 // Launch one SpMV of format fmt (no validation).
@@ -846,9 +852,33 @@ static void tune_predict(spmv_matrix* h, int64_t iters, TuneScratch& ts, spmv_tu
   }
 }
 
+// ---------------------------------------------------------------- CUDA-graph power loop
+namespace {
+struct PowerGraph {
+  cudaGraphExec_t exec = nullptr;
+  uint64_t gen = 0;
+  const void* x0 = nullptr;
+  void* b0 = nullptr;
+  void* b1 = nullptr;
+  int64_t n = 0, steps = 0;
+  double* sums = nullptr;
+  int final_buf = 0;
+  uint64_t kernels = 0;  // kernel nodes (library launches) per replay
+};
+}  // namespace
+
+void destroy_power_graph(spmv_matrix* h) {
+  auto* g = static_cast<PowerGraph*>(h->power_graph);
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  delete g;
+  h->power_graph = nullptr;
+}
+
 static void destroy_handle(spmv_matrix* h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  destroy_power_graph(h);
   for (int f = 0; f < SPMV_NUM_FORMATS; ++f) free_format(h, f);
   dfree(h->seg_scratch, h->stream);
   dfree(h->fix_scratch, h->stream);
@@ -950,6 +980,7 @@ spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format
   if (fmt < 0 || fmt >= SPMV_NUM_FORMATS) return SPMV_ERR_INVALID_ARG;
   API_TRY
   DeviceGuard g(h->device);
+  need_csr(h, "spmv_convert");
   spmv_format_params_t q{};
   q.hyb_K = -1;
   if (p) q = *p;
@@ -1011,6 +1042,7 @@ spmv_status_t spmv_convert(spmv_handle_t h, spmv_format_t fmt, const spmv_format
     }
   }
   h->active = fmt;  // builds are stream-ordered: no synchronisation here
+  ++h->gen;
   API_CATCH(h)
 }
 
@@ -1018,6 +1050,7 @@ spmv_status_t spmv_set_format(spmv_handle_t h, spmv_format_t fmt) {
   if (!h || fmt < 0 || fmt >= SPMV_NUM_FORMATS) return SPMV_ERR_INVALID_ARG;
   if (!built(h, fmt)) return SPMV_ERR_NOT_CONVERTED;
   h->active = fmt;
+  ++h->gen;
   return SPMV_OK;
 }
 
@@ -1032,8 +1065,28 @@ spmv_status_t spmv_features(spmv_handle_t h, spmv_features_t* out) {
   if (!h || !out) return SPMV_ERR_INVALID_ARG;
   API_TRY
   DeviceGuard g(h->device);
-  compute_features(h);
+  if (!h->have_features) need_csr(h, "spmv_features");
+  if (!h->csr_released) compute_features(h);
   *out = h->feat;
+  API_CATCH(h)
+}
+
+spmv_status_t spmv_release_csr(spmv_handle_t h) {
+  if (!h) return SPMV_ERR_INVALID_ARG;
+  if (h->active == SPMV_FMT_CSR || h->active == SPMV_FMT_COO) return SPMV_ERR_INVALID_ARG;
+  if (h->csr_released) return SPMV_OK;
+  API_TRY
+  DeviceGuard g(h->device);
+  free_format(h, SPMV_FMT_COO);  // shares col/val with CSR
+  for (void** q : {&h->row_ptr, (void**)&h->col, &h->val, (void**)&h->merge_coords, (void**)&h->csr_empty}) {
+    dfree(*q, h->stream);
+    *q = nullptr;
+  }
+  h->merge_coords_n = 0;
+  h->merge_coords_ipt = 0;
+  h->csr_n_empty = -1;
+  h->csr_released = true;
+  ++h->gen;
   API_CATCH(h)
 }
 
@@ -1070,6 +1123,7 @@ spmv_status_t spmv_set_launch(spmv_handle_t h, spmv_format_t fmt, const spmv_lau
   if (L.maxreg) reg_index(L.maxreg);
   if (L.carveout_pct > 100) fail(SPMV_ERR_INVALID_ARG, "carveout must be -1 or 0..100");
   h->launch[fmt] = L;
+  ++h->gen;
   API_CATCH(h)
 }
 
@@ -1095,6 +1149,8 @@ spmv_status_t spmv_tune(spmv_handle_t h, uint32_t flags, int64_t expected_iterat
   if (h->rows == 0 || h->nnz == 0) return SPMV_ERR_INVALID_ARG;
   API_TRY
   DeviceGuard g(h->device);
+  need_csr(h, "spmv_tune");
+  ++h->gen;  // format and launch choices may change
   if (obj != 0 && !nvml_available()) fail(SPMV_ERR_NVML, "energy/power objectives need libnvidia-ml");
   spmv_tune_report_t rep{};
   rep.format = h->active;
@@ -1163,6 +1219,64 @@ spmv_status_t spmv_power_iterate(spmv_handle_t h, const void* x0, void* buf0, vo
   API_CATCH(h)
 }
 
+spmv_status_t spmv_power_iterate_graph(spmv_handle_t h, const void* x0, void* buf0, void* buf1, int64_t n_full,
+                                       int64_t steps, double* sums, int* final_buf) {
+  const NvtxRange nvtx_range("spmv_power_iterate_graph");
+  if (!h || !x0 || !buf0 || !buf1 || !sums || steps < 0 || n_full < h->rows || buf0 == buf1) return SPMV_ERR_INVALID_ARG;
+  if (!built(h, h->active)) return SPMV_ERR_NOT_CONVERTED;
+  API_TRY
+  DeviceGuard g(h->device);
+  auto* pg = static_cast<PowerGraph*>(h->power_graph);
+  if (pg && pg->exec && pg->gen == h->gen && pg->x0 == x0 && pg->b0 == buf0 && pg->b1 == buf1 && pg->n == n_full &&
+      pg->steps == steps && pg->sums == sums) {
+    CK(cudaGraphLaunch(pg->exec, h->stream));
+    g_launches.fetch_add(pg->kernels, std::memory_order_relaxed);
+    if (final_buf) *final_buf = pg->final_buf;
+    return SPMV_OK;
+  }
+  destroy_power_graph(h);
+  // first call with these arguments: run the loop eagerly (its result is this
+  // call's result; lazily built scratch, partitions and kernel attributes are
+  // set up outside the capture), then capture the same loop for the replays
+  int fb = 0;
+  power_iterate(h, x0, buf0, buf1, n_full, steps, sums, nullptr, 0, nullptr, nullptr, nullptr, &fb);
+  cudaStream_t cs = nullptr;  // capture on a private stream (the legacy stream cannot be captured)
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaStream_t saved = h->stream;
+  h->stream = cs;
+  const uint64_t l0 = g_launches.load();
+  cudaGraph_t graph = nullptr;
+  try {
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int fb2 = 0;
+    try {
+      power_iterate(h, x0, buf0, buf1, n_full, steps, sums, nullptr, 0, nullptr, nullptr, nullptr, &fb2);
+    } catch (...) {
+      cudaStreamEndCapture(cs, &graph);
+      throw;
+    }
+    CK(cudaStreamEndCapture(cs, &graph));
+  } catch (...) {
+    if (graph) cudaGraphDestroy(graph);
+    h->stream = saved;
+    g_launches.fetch_sub(g_launches.load() - l0);
+    cudaStreamDestroy(cs);
+    throw;
+  }
+  h->stream = saved;
+  const uint64_t nk = g_launches.load() - l0;
+  g_launches.fetch_sub(nk);  // captured, not launched: counted at each replay
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  cudaStreamDestroy(cs);
+  cuda_check(e, "cudaGraphInstantiate");
+  pg = new PowerGraph{exec, h->gen, x0, buf0, buf1, n_full, steps, sums, fb, nk};
+  h->power_graph = pg;
+  if (final_buf) *final_buf = fb;
+  API_CATCH(h)
+}
+
 spmv_status_t spmv_dist_plan_create(spmv_dist_plan_t* out, spmv_handle_t h, void* comm, int64_t chunk,
                                     uint32_t flags) {
   const NvtxRange nvtx_range("spmv_dist_plan_create");
@@ -1172,6 +1286,7 @@ spmv_status_t spmv_dist_plan_create(spmv_dist_plan_t* out, spmv_handle_t h, void
   if (!built(h, h->active)) return SPMV_ERR_NOT_CONVERTED;
   API_TRY
   DeviceGuard g(h->device);
+  need_csr(h, "spmv_dist_plan_create");
   *out = plan_create(h, comm, chunk, flags);
   API_CATCH(h)
 }
@@ -1220,6 +1335,7 @@ spmv_status_t spmv_create_row_slice(spmv_handle_t* out, spmv_handle_t h, int64_t
   if (!h || row_begin < 0 || row_end < row_begin || row_end > h->rows) return SPMV_ERR_INVALID_ARG;
   API_TRY
   DeviceGuard g(h->device);
+  need_csr(h, "spmv_create_row_slice");
   *out = make_row_slice(h, row_begin, row_end);
   API_CATCH(h)
 }
@@ -1284,9 +1400,9 @@ spmv_status_t spmv_copy_array(spmv_handle_t h, spmv_array_t which, void* dst, in
   const int64_t vb = h->vbytes;
   bool need = true;
   switch (which) {
-    case SPMV_ARR_CSR_ROW_PTR: src = h->row_ptr; bytes = (h->rows + 1) * (h->rp64 ? 8 : 4); break;
-    case SPMV_ARR_CSR_COL: src = h->col; bytes = h->nnz * 4; break;
-    case SPMV_ARR_CSR_VAL: src = h->val; bytes = h->nnz * vb; break;
+    case SPMV_ARR_CSR_ROW_PTR: need = !h->csr_released; src = h->row_ptr; bytes = (h->rows + 1) * (h->rp64 ? 8 : 4); break;
+    case SPMV_ARR_CSR_COL: need = !h->csr_released; src = h->col; bytes = h->nnz * 4; break;
+    case SPMV_ARR_CSR_VAL: need = !h->csr_released; src = h->val; bytes = h->nnz * vb; break;
     case SPMV_ARR_COO_ROW: need = h->coo_built; src = h->coo_row; bytes = h->nnz * 4; break;
     case SPMV_ARR_COO_EMPTY_ROWS: need = h->coo_built; src = h->coo_empty; bytes = h->coo_n_empty * 4; break;
     case SPMV_ARR_ELL_COL: need = h->ell_built && h->ell_col; src = h->ell_col; bytes = h->ell_K * h->ell_npad * 4; break;
@@ -1345,6 +1461,7 @@ spmv_status_t spmv_set_stream(spmv_handle_t h, void* s) {
   DeviceGuard g(h->device);
   CK(cudaStreamSynchronize(h->stream));
   h->stream = static_cast<cudaStream_t>(s);
+  ++h->gen;
   API_CATCH(h)
 }
 

@@ -105,6 +105,14 @@ struct spmv_matrix {
   // them in a separate pass), built on first use (csr_n_empty = -1 until then)
   int32_t* csr_empty = nullptr;
   int64_t csr_n_empty = -1;
+  // spmv_release_csr: the CSR (and COO) arrays were freed after conversion to
+  // a format with its own arrays; everything that reads them now fails
+  bool csr_released = false;
+  // CUDA-graph replay of the single-GPU power loop (spmv_power_iterate_graph):
+  // the instantiated graph and its key; gen counts every change that can
+  // alter the launched kernels (convert, set_format, set_launch, tune, ...)
+  void* power_graph = nullptr;
+  uint64_t gen = 0;
   double* pi_partials = nullptr;
   unsigned* pi_counter = nullptr;
   size_t pi_partials_n = 0;

@@ -12,6 +12,7 @@
 
 #pragma once
 #include "kern_sliced_decl.cuh"
+#include <climits>
 
 namespace spmv {
 namespace kern {
@@ -122,7 +123,10 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ int s_tab[D8 ? 256 : 1];
   if constexpr (D8) {
-    for (int i = threadIdx.x; i < 256; i += B) s_tab[i] = i < 255 ? p.tab8[i] : 0;
+    // the pad code's entry makes every padded column negative (origin + row
+    // < 2^31, so origin + row + INT_MIN is in [INT_MIN, -1]): the gather's
+    // col >= 0 test skips padding without a separate code == 255 test
+    for (int i = threadIdx.x; i < 256; i += B) s_tab[i] = i < 255 ? p.tab8[i] : INT_MIN;
     __syncthreads();
   }
   // the power-step partial sums live in shared memory (one slot per warp,
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
             for (int r = 0; r < RPL; ++r) dd[r] = 255;
           }
 #pragma unroll
-          for (int r = 0; r < RPL; ++r) c[u][r] = dd[r] == 255 ? -1 : rowv[r] + s_tab[dd[r]];
+          for (int r = 0; r < RPL; ++r) c[u][r] = rowv[r] + s_tab[dd[r]];  // < 0 for the pad code
           brow += stride;
         }
       }
@@ -250,7 +254,7 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
 #pragma unroll
           for (int r = 0; r < RPL; ++r) {
             const uint32_t code = (cw[u] >> (8 * r)) & 0xffu;
-            col[u][r] = code == 255u ? -1 : rowv[r] + s_tab[code];
+            col[u][r] = rowv[r] + s_tab[code];  // < 0 for the pad code
           }
 #pragma unroll
         for (int u = 0; u < U; ++u)

@@ -57,6 +57,7 @@ def test_create_rejects_bad_arguments_without_device():
     assert L.spmv_destroy(None) == P.OK
     assert L.spmv_run(None, 1.0, None, 0.0, None) == P.ERR_INVALID_ARG
     assert L.spmv_tune(None, 3, 1, None) == P.ERR_INVALID_ARG
+    assert L.spmv_release_csr(None) == P.ERR_INVALID_ARG
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])

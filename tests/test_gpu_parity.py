@@ -369,6 +369,40 @@ def test_csr_nnz_split_all_launches(case, dtype):
         P.spmv_destroy(h)
 
 
+@pytest.mark.parametrize("case,fmt,params", [("ragged_empty", P.FMT_ELL, {}), ("stencil27_9", P.FMT_ELL, {"index16": 2}),
+                                             ("ragged_empty", P.FMT_SELL, {}), ("ragged_empty", P.FMT_HYB, {}),
+                                             ("ragged_empty", P.FMT_BELL, {"bell_b": 2})])
+def test_release_csr(case, fmt, params):
+    """spmv_release_csr frees CSR/COO after conversion: the active format still
+    runs (O9 parity, power steps), features stay cached, everything that reads
+    CSR returns NOT_CONVERTED; refused while CSR or COO is active."""
+    coo = CASES[case]
+    h = create(coo)
+    try:
+        ref = oracle_csr(coo)
+        feats = P.spmv_features(h)
+        P.spmv_convert(h, P.FMT_COO)
+        with pytest.raises(P.SpmvError) as ex:
+            P.spmv_release_csr(h)
+        assert ex.value.status == P.ERR_INVALID_ARG
+        P.spmv_convert(h, fmt, **params)
+        P.spmv_release_csr(h)
+        P.spmv_release_csr(h)                                   # no-op
+        check_y(h, coo, "f64", fmt, 2.5, -0.5, ref)
+        assert P.spmv_features(h) == feats
+        for call in (lambda: P.spmv_convert(h, P.FMT_ELL), lambda: P.spmv_tune(h, P.TUNE_LAUNCH, 10),
+                     lambda: P.spmv_set_format(h, P.FMT_CSR), lambda: P.spmv_set_format(h, P.FMT_COO),
+                     lambda: P.spmv_create_row_slice(h, 0, 10),
+                     lambda: P.spmv_copy_array(h, P.ARR_CSR_COL, np.empty(coo.nnz, np.int32))):
+            with pytest.raises(P.SpmvError) as ex:
+                call()
+            assert ex.value.status == P.ERR_NOT_CONVERTED
+        torch.cuda.synchronize()
+        check_y(h, coo, "f64", fmt, 1.0, 0.0, ref, nan_y=True)
+    finally:
+        P.spmv_destroy(h)
+
+
 def test_determinism_bitwise():
     coo = CASES["long_rows"]
     h = create(coo)

@@ -262,3 +262,64 @@ def test_plan_errors():
     P.spmv_dist_plan_destroy(plan)
     P.spmv_dist_destroy(comms[0])
     P.spmv_destroy(h)
+
+
+GRAPH_VARIANTS = [(P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR), None), (P.FMT_CSR, dict(csr_alg=P.CSR_STREAM), None),
+                  (P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), None), (P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), 0x408),
+                  (P.FMT_ELL, {}, None), (P.FMT_ELL, dict(index16=2), None), (P.FMT_SELL, {}, None),
+                  (P.FMT_HYB, dict(hyb_K=3), None), (P.FMT_COO, {}, None), (P.FMT_BELL, dict(bell_b=2), None)]
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("fmt,params,knob", GRAPH_VARIANTS)
+def test_power_iterate_graph(fmt, params, knob):
+    """spmv_power_iterate_graph (the single-GPU loop as a CUDA graph, SURVEY
+    c1): the first call runs eagerly then captures; replays are bitwise equal
+    to the eager loop (same kernels, same order) and count their kernels in
+    spmv_launch_count; a launch change re-captures; the result matches the
+    oracle's power iteration (O11) step by step through the eager loop."""
+    coo = si.lap2d(64, random_values=True)   # c1: launch-bound
+    n = coo.rows
+    E = 20
+    h = P.spmv_create(n, n, torch.from_numpy(coo.row).cuda(), torch.from_numpy(coo.col).cuda(),
+                      torch.from_numpy(coo.val).cuda())
+    try:
+        P.spmv_convert(h, fmt, **params)
+        if knob is not None:
+            P.spmv_set_launch(h, fmt, 128, 64, -1, knob)
+        x0 = torch.from_numpy(vec(n, 5, "f64")).cuda()
+        b0, b1 = torch.zeros(n, dtype=torch.float64, device="cuda"), torch.zeros(n, dtype=torch.float64, device="cuda")
+        s_e = torch.zeros(E + 1, 2, dtype=torch.float64, device="cuda")
+        fb, _, _ = P.spmv_power_iterate(h, x0, b0, b1, E, s_e)
+        torch.cuda.synchronize()
+        z_e = (b0 if fb == 0 else b1).clone()
+        l0 = P.launch_count()
+        P.spmv_power_iterate(h, x0, b0, b1, E, s_e)
+        torch.cuda.synchronize()
+        per_loop = P.launch_count() - l0
+        g0, g1 = torch.zeros_like(b0), torch.zeros_like(b0)
+        s_g = torch.zeros_like(s_e)
+        for rep in range(3):
+            g0.fill_(float("nan")), g1.fill_(float("nan")), s_g.fill_(float("nan"))
+            c0 = P.launch_count()
+            fg = P.spmv_power_iterate_graph(h, x0, g0, g1, E, s_g)
+            torch.cuda.synchronize()
+            assert fg == fb
+            assert torch.equal((g0 if fg == 0 else g1), z_e), rep
+            assert torch.equal(s_g, s_e), rep
+            assert P.launch_count() - c0 == per_loop, (rep, P.launch_count() - c0, per_loop)
+        P.spmv_set_launch(h, fmt, *P.spmv_get_launch(h, fmt))     # invalidates: re-captured, same result
+        fg = P.spmv_power_iterate_graph(h, x0, g0, g1, E, s_g)
+        fg = P.spmv_power_iterate_graph(h, x0, g0, g1, E, s_g)
+        torch.cuda.synchronize()
+        assert torch.equal((g0 if fg == 0 else g1), z_e) and torch.equal(s_g, s_e)
+        res = {}
+        zz0, zz1 = torch.zeros_like(b0), torch.zeros_like(b0)
+        for k in (1, 2, 3):
+            sk = torch.zeros(k + 1, 2, dtype=torch.float64, device="cuda")
+            f = P.spmv_power_iterate_graph(h, x0, zz0, zz1, k, sk)
+            torch.cuda.synchronize()
+            res[k] = ((zz0 if f == 0 else zz1).cpu().numpy().copy(), sk.cpu().numpy())
+        check_vs_oracle(coo, res, x0, 3)
+    finally:
+        P.spmv_destroy(h)
