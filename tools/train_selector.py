@@ -165,6 +165,20 @@ def main():
             out.append(r["times"][r["best"]] / t_p)
         return float(np.exp(np.mean(np.log(out)))), float(np.min(out))
 
+    def near_best(ids, model, tol=0.05):
+        # a prediction within tol of the best measured time counts as right:
+        # several formats are within a few % of each other on many matrices
+        # (stencil27_64: CSR-stream 18.4 µs, HYB 18.5 µs), so exact-label
+        # accuracy understates how often the selector picks a fast format
+        ok = 0
+        for i in ids:
+            r = recs[i]
+            p = CLASSES[int(model.predict(X[i:i + 1])[0])]
+            ok += r["times"].get(p, float("inf")) <= (1.0 + tol) * r["times"][r["best"]]
+        return ok / max(len(ids), 1)
+
+    nb_te = near_best(te_i, clf)
+    nb_tr = near_best(tr_i, clf)
     pr_te = perf_ratio(te_i, clf)
     pr_all = perf_ratio(idx, clf)
     # final model on all data with the chosen hyper-parameters
@@ -222,7 +236,8 @@ def main():
                                      "2*min(bandwidth, 2^22)/1e6", "rows*std/1e6"],
              "c_latency_lin": clat_lin, "f_latency_lin": flat_lin,
              "stats": {"n_matrices": len(recs), "train": len(tr_i), "test": len(te_i), "cv_score": gs.best_score_,
-                       "acc_train": acc_tr, "acc_test": acc_te, "perf_ratio_test_geomean": pr_te[0],
+                       "acc_train": acc_tr, "acc_test": acc_te, "near_best_5pct_train": nb_tr,
+                       "near_best_5pct_test": nb_te, "perf_ratio_test_geomean": pr_te[0],
                        "perf_ratio_test_min": pr_te[1], "perf_ratio_all_geomean": pr_all[0],
                        "perf_ratio_all_min": pr_all[1], "perf_ratio_deployed_all_geomean": pr_final[0],
                        "perf_ratio_deployed_all_min": pr_final[1], "ratio_r2": ratio_r2, "c_latency_r2": clat_r2,
@@ -293,7 +308,9 @@ def write_report(m, recs, X, clf):
            "(`tools/selector_corpus.py` on one B200: every candidate format converted, launch-tuned and timed).", "",
            f"* matrices: {s['n_matrices']} (train {s['train']} / test {s['test']}, 80/20 as P:899)",
            f"* classifier: decision tree {m['params']} (5-fold CV score {s['cv_score']:.3f})",
-           f"* accuracy: train {s['acc_train']:.3f}, **test {s['acc_test']:.3f}**",
+           f"* accuracy: train {s['acc_train']:.3f}, **test {s['acc_test']:.3f}**; a pick within 5 % of the best measured "
+           f"time: train {s['near_best_5pct_train']:.3f}, **test {s['near_best_5pct_test']:.3f}** (many formats are "
+           f"within a few % of each other: exact-label accuracy counts those near-ties as errors)",
            f"* performance ratio t(best)/t(predicted): test geomean **{s['perf_ratio_test_geomean']:.4f}** "
            f"(min {s['perf_ratio_test_min']:.3f}); all geomean {s['perf_ratio_all_geomean']:.4f} "
            f"(min {s['perf_ratio_all_min']:.3f}) for the 80% model; the deployed model (same hyper-parameters, "
