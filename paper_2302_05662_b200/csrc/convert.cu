@@ -9,6 +9,7 @@
 //   HYB  (north star; Bell–Garland): ELL part of width K_h + COO tail;
 //   COO: expanded row array + the list of empty rows.
 #include <algorithm>
+#include <cstdlib>
 
 #include "handle.cuh"
 #include "primitives.cuh"
@@ -41,41 +42,37 @@ __device__ __forceinline__ IDX pad_col() {
 template <class RP>
 __global__ void k_dict_flags(const RP* __restrict__ rp, const int32_t* __restrict__ col, int64_t rows,
                              int64_t origin, int64_t m, int64_t* __restrict__ flags) {
-  // warp per 32 consecutive rows: their entries are one contiguous range, read
-  // coalesced; the row of an entry is found among the 32 row starts the lanes
-  // hold (binary search over shuffles)
+  // thread per row, a warp on 32 consecutive rows: at step k the lanes read
+  // the k-th entry of their rows (the warp's rows share cache lines, so the
+  // strided column reads hit L1 after the first), four loads in flight. On a
+  // banded matrix the lanes of a step carry the same offset: a per-warp cache
+  // of seen offsets in shared memory (512 slots, multiplicative hash: no two
+  // offsets of the 5-/27-point stencils of any tested size share a slot;
+  // with the earlier 32-slot xor hash 20 of c5's 27 offsets collided and the
+  // pass ran at 1.1 TB/s) is a broadcast read, and the rare first sighting
+  // reads the flag before writing it (no same-address store storm).
+  constexpr int kSlots = 512;
   const int lane = threadIdx.x & 31, warp_in_block = threadIdx.x >> 5;
-  __shared__ int64_t s_seen[8][32];  // 256-thread blocks
-  s_seen[warp_in_block][lane] = INT64_MIN;
+  __shared__ int32_t s_seen[8][kSlots];  // 256-thread blocks; |d| < 2^31, INT_MIN = empty
+  for (int i = lane; i < kSlots; i += 32) s_seen[warp_in_block][i] = INT_MIN;
   __syncwarp();
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r0 = w0 * 32; r0 < rows; r0 += nw * 32) {
-    const int64_t my = r0 + lane < rows ? (int64_t)rp[r0 + lane] : (int64_t)rp[rows];
-    const int64_t end = (int64_t)rp[r0 + 32 < rows ? r0 + 32 : rows];
-    const int64_t beg = __shfl_sync(0xffffffffu, my, 0);
-    for (int64_t k0 = beg; k0 < end; k0 += 128) {
-      int cv[4];  // four column loads in flight per lane (the loop is latency-bound otherwise)
+    const int64_t r = r0 + lane;
+    const int64_t a = r < rows ? (int64_t)rp[r] : 0, b = r < rows ? (int64_t)rp[r + 1] : 0;
+    const int64_t base = origin + r;
+    for (int64_t k = a; __any_sync(0xffffffffu, k < b); k += 4) {
+      int cv[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) cv[j] = k0 + 32 * j + lane < end ? col[k0 + 32 * j + lane] : 0;
+      for (int j = 0; j < 4; ++j) cv[j] = k + j < b ? col[k + j] : 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int64_t k = k0 + 32 * j + lane;
-        int lo = 0;  // largest row j with start_j <= k (rows without entries share a start: the last wins)
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const int64_t sj = __shfl_sync(0xffffffffu, my, lo + step);
-          if (sj <= k) lo += step;
-        }
-        if (k < end) {
-          // a banded matrix hits the same few dozen offsets in every warp: a
-          // per-warp cache of recently seen offsets (32 hashed slots in shared
-          // memory) skips the flag array for all but the first sightings; on
-          // a miss, read before write (stores to one address serialise in L2)
-          const int64_t d = (int64_t)cv[j] - origin - (r0 + lo);
-          const int slot = (int)((d ^ (d >> 5) ^ (d >> 10)) & 31);
+        if (k + j < b) {
+          const int32_t d = (int32_t)((int64_t)cv[j] - base);
+          const int slot = (int)(((uint32_t)d * 0x165667B1u) >> 23);
           if (s_seen[warp_in_block][slot] != d) {
-            int64_t* f = flags + (d + m);
+            int64_t* f = flags + ((int64_t)d + m);
             if (*f == 0) *f = 1;
             s_seen[warp_in_block][slot] = d;
           }
@@ -395,7 +392,13 @@ void ell_typed(spmv_matrix* h, int enc) {
   const RP* rp = static_cast<const RP*>(h->row_ptr);
   const V* val = static_cast<const V*>(h->val);
   lat_begin(h, SPMV_FMT_ELL);  // c_latency = device time of the conversion kernels (allocation excluded)
-  const unsigned g = grid_for(n_pad, 256);
+  // 3 resident 256-thread blocks per SM: the warps' strided row reads then
+  // stay in L1 (c5 ELL-8 fill 17.8 ms vs 20.3 ms with a full grid, 31.4 with 1)
+  static const int fill_bps = [] {
+    const char* e = getenv("SPMV_ELL_FILL_BPS");  // measurement override
+    return e ? atoi(e) : 3;
+  }();
+  const unsigned g = grid_for(n_pad, 256, (int64_t)kNumSMs * (fill_bps > 0 ? fill_bps : 32));
   if (enc == 2)
     LAUNCH((k_ell_fill<RP, V, uint8_t>), g, 256, 0, s, rp, h->col, val, h->rows, K, n_pad, colE8, valE,
            h->col_origin, dv);
