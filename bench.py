@@ -1055,6 +1055,7 @@ def run_rank(args, ctx: Ctx, shared: dict):
         free_b, _ = torch.cuda.mem_get_info(dev)
         step_b = 3 * coo.nnz * (8 + vb)  # COO + format + scratch, per step in flight (upper estimate)
         depth = 2 if world == 1 and not args.e2e_serial and 2 * step_b < 0.8 * free_b else 1
+        step_times = []  # host time of every e2e step (the c5 steps vary: see DESIGN §7)
 
         def make_lane(i):
             return {"stream": torch.cuda.Stream(device=dev),
@@ -1065,6 +1066,13 @@ def run_rank(args, ctx: Ctx, shared: dict):
         ingest_lock = threading.Lock()
 
         def e2e_step(lane):
+            t_s = time.perf_counter()
+            try:
+                e2e_step_body(lane)
+            finally:
+                step_times.append(round((time.perf_counter() - t_s) * 1e3, 1))
+
+        def e2e_step_body(lane):
             torch.cuda.set_device(dev)
             st = lane["stream"]
             with torch.cuda.stream(st):
@@ -1110,7 +1118,7 @@ def run_rank(args, ctx: Ctx, shared: dict):
         e2e = {"value": round(flops / t_e2e / 1e9, 3), "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(coo.nnz * (8 + vb) + x0.numel() * vb),
                "d2h_bytes_per_step": int(lanes[0]["y_host"].numel() * vb + lanes[0]["s_host"].numel() * 8),
-               "steps_in_flight": depth}
+               "steps_in_flight": depth, "step_host_ms_last": step_times[-args.steps:]}
         if depth > 1:  # the serial figure too (one step at a time), comparable across configs/rounds
             t_ser = timed_e2e(1, max(2, args.steps // 2))
             e2e["serial_value"] = round(2.0 * nnz_total * E * max(2, args.steps // 2) / t_ser / 1e9, 3)

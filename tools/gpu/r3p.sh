@@ -1,0 +1,16 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+A="--per-config none --no-cpu-baseline --steps 4"
+for v in a b c d; do
+  case $v in
+    a) E="" ;;
+    b) E="BENCH_E2E_RELEASE_INPUT=1" ;;
+    c) E="BENCH_E2E_RELEASE_INPUT=1 BENCH_E2E_RELEASE_CSR=1" ;;
+    d) E="BENCH_E2E_RELEASE_INPUT=1 BENCH_E2E_RELEASE_CSR=1 BENCH_E2E_DEPTH=2" ;;
+  esac
+  env $E timeout 1200 python bench.py $A > gpurun_out/r3p_$v.json 2> gpurun_out/r3p_$v.err
+  python -c "
+import json;d=json.loads(open('gpurun_out/r3p_$v.json').read().strip().splitlines()[-1])
+print('$v', d['value'], d['e2e'])" 2>&1 | tail -n 1
+done
