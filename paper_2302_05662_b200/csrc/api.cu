@@ -393,7 +393,7 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
       if (h->csr_alg == SPMV_CSR_MERGE)  // per-warp merge walk, or row-interleaved tiles of block·IPT items
         return {4, 8, 16, kern::kMergeTile | 4, kern::kMergeTile | 8, kern::kMergeTile | 16, kern::kMergeTile | 32,
                 kern::kMergeStream | 4, kern::kMergeStream | 8, kern::kMergeStream | 16, kern::kMergeStream | 32,
-                kern::kMergeNnz | 4, kern::kMergeNnz | 8};
+                kern::kMergeNnz | 4, kern::kMergeNnz | 8, kern::kMergeRowmap | 8};
       if (h->csr_alg == SPMV_CSR_STREAM) return {16, 32, 64};
       {
         int t = csr_default_lanes(h);
@@ -884,6 +884,9 @@ static void destroy_handle(spmv_matrix* h) {
   dfree(h->fix_scratch, h->stream);
   dfree(h->merge_coords, h->stream);
   dfree(h->csr_empty, h->stream);
+  dfree(h->rm_bits, h->stream);
+  dfree(h->rm_rows, h->stream);
+  dfree(h->rm_ord0, h->stream);
   dfree(h->dict8_map, h->stream);
   dfree(h->dict8_tab, h->stream);
   dfree(h->pi_partials, h->stream);
@@ -1078,13 +1081,15 @@ spmv_status_t spmv_release_csr(spmv_handle_t h) {
   API_TRY
   DeviceGuard g(h->device);
   free_format(h, SPMV_FMT_COO);  // shares col/val with CSR
-  for (void** q : {&h->row_ptr, (void**)&h->col, &h->val, (void**)&h->merge_coords, (void**)&h->csr_empty}) {
+  for (void** q : {&h->row_ptr, (void**)&h->col, &h->val, (void**)&h->merge_coords, (void**)&h->csr_empty,
+                   (void**)&h->rm_bits, (void**)&h->rm_rows, (void**)&h->rm_ord0}) {
     dfree(*q, h->stream);
     *q = nullptr;
   }
   h->merge_coords_n = 0;
   h->merge_coords_ipt = 0;
   h->csr_n_empty = -1;
+  h->rm_nchunks = -1;
   h->csr_released = true;
   ++h->gen;
   API_CATCH(h)

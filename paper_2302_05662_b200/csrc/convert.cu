@@ -749,6 +749,60 @@ void csr_empty_typed(spmv_matrix* h) {
   h->csr_n_empty = n_empty;
 }
 
+template <class RP>
+__global__ void k_rowmap_marks(const RP* __restrict__ rp, const int64_t* __restrict__ off_empty, int64_t rows,
+                               uint32_t* __restrict__ bits, int32_t* __restrict__ nz_rows) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const int64_t a = rp[r];
+    if ((int64_t)rp[r + 1] == a) continue;
+    atomicOr(bits + (a >> 5), 1u << (a & 31));
+    nz_rows[r - off_empty[r]] = (int32_t)r;
+  }
+}
+
+// starts in chunk c (256 entries = 8 words)
+__global__ void k_rowmap_counts(const uint32_t* __restrict__ bits, int64_t nchunks, int64_t* __restrict__ cnt) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += stride) {
+    int64_t n = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) n += __popc(bits[c * 8 + j]);
+    cnt[c] = n;
+  }
+}
+
+template <class RP>
+void csr_rowmap_typed(spmv_matrix* h) {
+  cudaStream_t s = h->stream;
+  const int64_t rows = h->rows, nchunks = (h->nnz + 255) / 256;
+  Scratch sc(s);
+  const RP* rp = static_cast<const RP*>(h->row_ptr);
+  int64_t* flag = sc.get<int64_t>(rows);
+  int64_t* off = sc.get<int64_t>(rows + 1);
+  LAUNCH(k_row_counts<RP>, grid_for(rows, 256), 256, 0, s, rp, rows, 0, (int64_t)0, flag);
+  exclusive_scan_i64(flag, off, rows, s);
+  uint32_t* bits = sc.get<uint32_t>(nchunks * 8);
+  int32_t* nz_rows = sc.get<int32_t>(rows);
+  int64_t* cnt = sc.get<int64_t>(nchunks);
+  int64_t* ord0 = sc.get<int64_t>(nchunks + 1);
+  CK(cudaMemsetAsync(bits, 0, (size_t)nchunks * 8 * sizeof(uint32_t), s));
+  LAUNCH(k_rowmap_marks<RP>, grid_for(rows, 256), 256, 0, s, rp, (const int64_t*)off, rows, bits, nz_rows);
+  LAUNCH(k_rowmap_counts, grid_for(nchunks, 256), 256, 0, s, (const uint32_t*)bits, nchunks, cnt);
+  exclusive_scan_i64(cnt, ord0, nchunks, s);
+  for (void* p : {(void*)bits, (void*)nz_rows, (void*)ord0}) sc.keep(p);
+  h->rm_bits = bits;
+  h->rm_rows = nz_rows;
+  h->rm_ord0 = ord0;
+  h->rm_nchunks = nchunks;
+}
+
+void build_csr_rowmap(spmv_matrix* h) {
+  if (h->rm_nchunks >= 0) return;
+  if (h->rp64) csr_rowmap_typed<int64_t>(h);
+  else csr_rowmap_typed<int32_t>(h);
+}
+
 void build_csr_empty(spmv_matrix* h) {
   if (h->csr_n_empty >= 0) return;
   if (h->rp64) csr_empty_typed<int64_t>(h);

@@ -105,6 +105,13 @@ struct spmv_matrix {
   // them in a separate pass), built on first use (csr_n_empty = -1 until then)
   int32_t* csr_empty = nullptr;
   int64_t csr_n_empty = -1;
+  // row map of the nnz-split kernel with a cached row map (knob 0x800): a bit
+  // per entry (1 = first entry of its row), the ids of the non-empty rows in
+  // order, and per 256-entry chunk the number of row starts before it
+  uint32_t* rm_bits = nullptr;
+  int32_t* rm_rows = nullptr;
+  int64_t* rm_ord0 = nullptr;
+  int64_t rm_nchunks = -1;
   // spmv_release_csr: the CSR (and COO) arrays were freed after conversion to
   // a format with its own arrays; everything that reads them now fails
   bool csr_released = false;
@@ -137,6 +144,8 @@ void compute_features(spmv_matrix* h);
 void build_coo(spmv_matrix* h);
 // h->csr_empty / csr_n_empty (rows of the CSR without entries); once per handle.
 void build_csr_empty(spmv_matrix* h);
+// h->rm_* (row map of the nnz-split kernel, 256-entry chunks); once per handle.
+void build_csr_rowmap(spmv_matrix* h);
 // index16 (column encoding): 0 = int32 columns, 1 = 16-bit offsets, 2 = 8-bit
 // codes into the offset dictionary (SPMV_ERR_UNSUPPORTED if the encoding does
 // not fit), -1 = the narrowest that fits (8-bit, then 16-bit, then int32).

@@ -4,6 +4,7 @@ namespace spmv {
 namespace kern {
 template CsrFn csr_merge_fn<double, int32_t, 4>(int, int);
 template CsrFn csr_nnz_fn<double, int32_t, 4>(int, int);
+template CsrFn csr_nnz_map_fn<double, int32_t>(int, int);
 template CsrFn csr_nnz_fn<double, int32_t, 8>(int, int);
 template CsrFn csr_merge_fn<double, int32_t, 8>(int, int);
 template CsrFn csr_merge_fn<double, int32_t, 16>(int, int);

@@ -18,6 +18,9 @@ struct CsrParams {
   ChunkRec* recs;
   const int64_t* coords;  // merge-path chunk start coordinates (x, y) pairs, nchunks+1
   int64_t nchunks;
+  const uint32_t* rm_bits;  // row map (k_csr_nnz_map): row-start bit per entry
+  const int32_t* rm_rows;   //   ids of the non-empty rows, in order
+  const int64_t* rm_ord0;   //   row starts before each 256-entry chunk
 };
 
 using CsrFn = void (*)(const CsrParams);
@@ -88,6 +91,11 @@ constexpr size_t merge_stream_smem(int block, int ipt) {
 constexpr int kMergeNnz = 0x400;
 template <class T, class RP, int W>
 CsrFn csr_nnz_fn(int bi, int ri);
+// nnz-split CSR with a cached row map (k_csr_nnz_map): knob kMergeRowmap | 8,
+// a warp owns 256 consecutive entries; rows from the row-start bits.
+constexpr int kMergeRowmap = 0x800;
+template <class T, class RP>
+CsrFn csr_nnz_map_fn(int bi, int ri);
 // nnz-split partition: coords[c] = row holding entry c·per (rows past the end), c = 0..nchunks.
 void nnz_partition(const void* rp, bool rp64, int64_t rows, int64_t nnz, int64_t per, int64_t nchunks,
                    int64_t* coords, cudaStream_t s);

@@ -68,6 +68,29 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
     return;
   }
+  if (L.knob & kern::kMergeRowmap) {
+    // nnz-split chunks of 256 entries with the cached row map; empty rows from the handle's list
+    if ((L.knob & 0xff) != 8) fail(SPMV_ERR_INVALID_ARG, "row-map CSR takes 8 entries per lane");
+    const void* fn = (const void*)kern::csr_nnz_map_fn<T, RP>(bi, ri);
+    if (((uintptr_t)h->col | (uintptr_t)h->val) & 15)
+      fail(SPMV_ERR_UNSUPPORTED, "row-map CSR: col/val must be 16-byte aligned for the vector loads");
+    if (h->nnz >= ((int64_t)1 << 31)) fail(SPMV_ERR_UNSUPPORTED, "row-map CSR: nnz must be < 2^31");
+    build_csr_empty(h);
+    run_rows_scale(h, h->csr_empty, h->csr_n_empty, e, y);  // disjoint from every row the chunks write
+    if (h->nnz <= 0) return;
+    build_csr_rowmap(h);
+    const int64_t nchunks = h->rm_nchunks;
+    const LaunchAttrs attrs(fn, L.carveout_pct);
+    p.recs = static_cast<ChunkRec*>(ensure_seg_scratch(h, (size_t)nchunks * sizeof(ChunkRec)));
+    p.nchunks = nchunks;
+    p.rm_bits = h->rm_bits;
+    p.rm_rows = h->rm_rows;
+    p.rm_ord0 = h->rm_ord0;
+    void* args[] = {&p};
+    launch_checked(fn, dim3((unsigned)((nchunks * 32 + L.block - 1) / L.block)), dim3(L.block), args, 0, h->stream);
+    run_seg_fixup(h, p.recs, nchunks, e, y);
+    return;
+  }
   if (L.knob & kern::kMergeNnz) {
     // nnz-split chunks: 32·W entries per warp; empty rows from the handle's list
     const int W = L.knob & 0xff;

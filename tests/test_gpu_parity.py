@@ -247,7 +247,7 @@ def test_spmv_parity(name, dtype, fname, fmt, params):
 @pytest.mark.parametrize("fname,fmt,params,knobs", [
     ("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR), [1, 2, 4, 8, 16, 32]),
     ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), [4, 8, 16, 0x104, 0x108, 0x110, 0x204, 0x208, 0x210,
-                                                         0x404, 0x408]),
+                                                         0x404, 0x408, 0x808]),
     ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM), [16, 32, 64]),
     ("ELL", P.FMT_ELL, {}, [32, 64, 128, 64 | (1 << 16), 256 | (1 << 16)]),
     ("SELL", P.FMT_SELL, {}, [0, 64, 64 | (1 << 16)]),
@@ -341,7 +341,8 @@ def test_coo_tile_all_launches(case, dtype, fmt):
 def test_csr_nnz_split_all_launches(case, dtype):
     """nnz-split CSR of the merge-path family (knob 0x400 | W): warps of 32·W
     entries with vector loads, rows from the row pointers (binary search in
-    the cached partition window, then forward), lane runs + warp segmented
+    the cached partition window, then forward) or (knob 0x808) from the cached
+    row map (row-start bits + non-empty row list), lane runs + warp segmented
     scan, rows crossing warps through the fixup, hub rows spanning many warps
     (long-run fixup), empty rows from the handle's list, the ragged last warp:
     O9 parity, NaN y with beta = 0, bitwise repeatable; switching back to a
@@ -352,8 +353,8 @@ def test_csr_nnz_split_all_launches(case, dtype):
         ref = oracle_csr(coo)
         P.spmv_convert(h, P.FMT_CSR, csr_alg=P.CSR_MERGE)
         for block in (64, 128, 256, 512, 1024):
-            for W in (4, 8):
-                P.spmv_set_launch(h, P.FMT_CSR, block, 64 if block <= 512 else 32, -1, 0x400 | W)
+            for knob in (0x404, 0x408, 0x808):   # nnz-split by search, and with the cached row map
+                P.spmv_set_launch(h, P.FMT_CSR, block, 64 if block <= 512 else 32, -1, knob)
                 check_y(h, coo, dtype, P.FMT_CSR, 2.5, -0.5, ref)
                 y1 = check_y(h, coo, dtype, P.FMT_CSR, 1.0, 0.0, ref, nan_y=True)
                 y2 = check_y(h, coo, dtype, P.FMT_CSR, 1.0, 0.0, ref, nan_y=True)
