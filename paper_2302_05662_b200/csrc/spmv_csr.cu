@@ -74,7 +74,6 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     const void* fn = (const void*)kern::csr_nnz_map_fn<T, RP>(bi, ri);
     if (((uintptr_t)h->col | (uintptr_t)h->val) & 15)
       fail(SPMV_ERR_UNSUPPORTED, "row-map CSR: col/val must be 16-byte aligned for the vector loads");
-    if (h->nnz >= ((int64_t)1 << 31)) fail(SPMV_ERR_UNSUPPORTED, "row-map CSR: nnz must be < 2^31");
     build_csr_empty(h);
     run_rows_scale(h, h->csr_empty, h->csr_n_empty, e, y);  // disjoint from every row the chunks write
     if (h->nnz <= 0) return;
