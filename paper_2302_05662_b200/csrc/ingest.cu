@@ -77,10 +77,18 @@ __global__ void __launch_bounds__(256) k_check(const int32_t* __restrict__ R, co
         }
       }
     }
-    int pr = -1, pc = -1;
-    if (k0 > 0) {
-      pr = R[k0 - 1];
-      pc = Cc[k0 - 1];
+    // the predecessor of entry k0 is the last entry of the previous lane
+    // (consecutive lanes own consecutive groups of 4): a shuffle, and only
+    // lane 0 reads it from memory (the previous lane's streaming loads did not
+    // allocate in L1, so a load would be one more L2 request per thread)
+    const int lane = threadIdx.x & 31;
+    const int64_t kw = k0 - 4LL * lane;  // the warp's first entry in this iteration
+    const int64_t left = (nnz - kw + 3) / 4;  // lanes of the warp still in the loop (a prefix)
+    const unsigned am = left >= 32 ? 0xffffffffu : ((1u << left) - 1u);
+    int pr = __shfl_up_sync(am, r[3], 1), pc = __shfl_up_sync(am, c[3], 1);
+    if (lane == 0) {
+      pr = k0 > 0 ? R[k0 - 1] : -1;
+      pc = k0 > 0 ? Cc[k0 - 1] : -1;
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
