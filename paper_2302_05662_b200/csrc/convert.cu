@@ -117,67 +117,6 @@ __global__ void k_ell_fill(const RP* __restrict__ rp, const int32_t* __restrict_
   }
 }
 
-// ELL fill through shared memory: a warp owns 32 consecutive rows, reads
-// their contiguous entry range coalesced (four loads in flight per lane) into
-// its shared-memory slice, then writes the column-major slots k·n_pad + row
-// (32 consecutive rows per store: coalesced) from the slice — no strided
-// global reads at all. kWarps warps per block, slice = 32·K entries.
-template <class RP, class V, class IDX>
-__global__ void __launch_bounds__(128) k_ell_fill_warp(const RP* __restrict__ rp, const int32_t* __restrict__ col,
-                                                       const V* __restrict__ val, int64_t rows, int64_t K,
-                                                       int64_t n_pad, IDX* __restrict__ colE, V* __restrict__ valE,
-                                                       int64_t origin, Dict8View dv) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t cap = 32 * K;
-  V* s_val = reinterpret_cast<V*>(smem_raw) + (int64_t)wib * cap;
-  int32_t* s_col = reinterpret_cast<int32_t*>(reinterpret_cast<V*>(smem_raw) + 4 * cap) + (int64_t)wib * cap;
-  const int64_t groups = n_pad / 32;
-  const int64_t nwarps = (int64_t)gridDim.x * 4;
-  for (int64_t g = (int64_t)blockIdx.x * 4 + wib; g < groups; g += nwarps) {
-    const int64_t r0 = g * 32;
-    const int64_t lo = r0 < rows ? r0 : rows, hi = r0 + 32 < rows ? r0 + 32 : rows;
-    const int64_t a0 = (int64_t)rp[lo], a1 = (int64_t)rp[hi];
-    const int64_t E = a1 - a0;
-    for (int64_t e = lane; e < E; e += 128) {
-      int32_t c4[4];
-      V v4[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t q = e + 32 * j;
-        c4[j] = q < E ? col[a0 + q] : 0;
-        v4[j] = q < E ? val[a0 + q] : V(0);
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t q = e + 32 * j;
-        if (q < E) {
-          s_col[q] = c4[j];
-          s_val[q] = v4[j];
-        }
-      }
-    }
-    __syncwarp();
-    const int64_t r = r0 + lane;
-    int64_t st = 0, L = 0;
-    if (r < rows) {
-      st = (int64_t)rp[r] - a0;
-      L = (int64_t)rp[r + 1] - (int64_t)rp[r];
-    }
-    for (int64_t k = 0; k < K; ++k) {
-      const int64_t pos = k * n_pad + r;
-      if (k < L) {
-        colE[pos] = enc_col<IDX>(s_col[st + k], r, origin, dv);
-        valE[pos] = s_val[st + k];
-      } else {
-        colE[pos] = pad_col<IDX>();
-        valE[pos] = V(0);
-      }
-    }
-    __syncwarp();
-  }
-}
-
 // Largest |column − (origin + row)| over the first and last entry of every
 // row (columns are sorted within a row, so these bound all of them).
 template <class RP>
@@ -460,17 +399,7 @@ void ell_typed(spmv_matrix* h, int enc) {
     return e ? atoi(e) : 3;
   }();
   const unsigned g = grid_for(n_pad, 256, (int64_t)kNumSMs * (fill_bps > 0 ? fill_bps : 32));
-  static const bool fill_warp = getenv("SPMV_ELL_FILL_WARP") != nullptr;  // experiment switch
-  const size_t wsm = (size_t)4 * 32 * K * (sizeof(V) + 4);
-  if (fill_warp && enc == 2 && wsm <= 96 * 1024) {
-    const void* fn = (const void*)&k_ell_fill_warp<RP, V, uint8_t>;
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
-    int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_ell_fill_warp<RP, V, uint8_t>, 128, wsm));
-    const int64_t gw = std::min<int64_t>((int64_t)kNumSMs * std::max(nb, 1), (n_pad / 32 + 3) / 4);
-    LAUNCH((k_ell_fill_warp<RP, V, uint8_t>), (unsigned)gw, 128, wsm, s, rp, h->col, val, h->rows, K, n_pad, colE8,
-           valE, h->col_origin, dv);
-  } else if (enc == 2)
+  if (enc == 2)
     LAUNCH((k_ell_fill<RP, V, uint8_t>), g, 256, 0, s, rp, h->col, val, h->rows, K, n_pad, colE8, valE,
            h->col_origin, dv);
   else if (enc == 1)
