@@ -163,6 +163,41 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
   return r;
 }
 
+// 256-bit streaming loads (sm_100: one LDG.256 per lane, the L2 evict-first
+// priority as an instruction qualifier — no policy register to move into a
+// uniform register per load). p must be 32-byte aligned.
+__device__ __forceinline__ void ld_stream256(const int* p, int (&o)[8]) {
+  asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]), "=r"(o[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void ld_stream256(const float* p, float (&o)[8]) {
+  asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3]), "=f"(o[4]), "=f"(o[5]), "=f"(o[6]), "=f"(o[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void ld_stream256(const double* p, double (&o)[4]) {
+  asm("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+      : "l"(p));
+}
+// W (a multiple of the 256-bit width) consecutive values of one lane.
+template <int W>
+__device__ __forceinline__ void ld_stream256_w(const int* p, int (&o)[W]) {
+#pragma unroll
+  for (int q = 0; q < W; q += 8) ld_stream256(p + q, *reinterpret_cast<int(*)[8]>(&o[q]));
+}
+template <int W>
+__device__ __forceinline__ void ld_stream256_w(const float* p, float (&o)[W]) {
+#pragma unroll
+  for (int q = 0; q < W; q += 8) ld_stream256(p + q, *reinterpret_cast<float(*)[8]>(&o[q]));
+}
+template <int W>
+__device__ __forceinline__ void ld_stream256_w(const double* p, double (&o)[W]) {
+#pragma unroll
+  for (int q = 0; q < W; q += 4) ld_stream256(p + q, *reinterpret_cast<double(*)[4]>(&o[q]));
+}
+
 // Gathers of x: read-only path, keep in L1, evict-last in L2 (x is reused by
 // every row that touches the column; the matrix stream is evicted first).
 __device__ __forceinline__ double ld_x(const double* p) {

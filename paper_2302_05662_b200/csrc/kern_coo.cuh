@@ -65,7 +65,16 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_coo(const CooPa
   const int64_t k0 = base + (int64_t)lane * W;
   int r[W], c[W];
   T v[W];
-  if (k0 + W <= p.nnz) {
+  // W = 8 on 32-byte aligned arrays: one 256-bit load per array (two for
+  // fp64 values) instead of two 128-bit loads (warp-uniform choice)
+  const bool v256 = W == 8 && ((((uintptr_t)p.row | (uintptr_t)p.col | (uintptr_t)p.val) & 31) == 0);
+  if (k0 + W <= p.nnz && v256) {
+    if constexpr (W == 8) {
+      ld_stream256_w<W>(p.row + k0, r);
+      ld_stream256_w<W>(p.col + k0, c);
+      ld_stream256_w<W>(val + k0, v);
+    }
+  } else if (k0 + W <= p.nnz) {
     load_wi<W>(p.row + k0, r);
     load_wi<W>(p.col + k0, c);
     load_w<T, W>(val + k0, v);

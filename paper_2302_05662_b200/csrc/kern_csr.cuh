@@ -951,7 +951,11 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_nnz_map(con
   const int64_t ord0 = __ldg(p.rm_ord0 + chunk);
   int c[W];
   T v[W];
-  if (k0 + W <= p.nnz) {
+  const bool v256 = ((((uintptr_t)p.col | (uintptr_t)p.val) & 31) == 0);  // warp-uniform
+  if (k0 + W <= p.nnz && v256) {
+    ld_stream256_w<W>(p.col + k0, c);
+    ld_stream256_w<W>(val + k0, v);
+  } else if (k0 + W <= p.nnz) {
 #pragma unroll
     for (int q = 0; q < W; q += 4) {
       int t4[4];
