@@ -108,8 +108,6 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
   constexpr int RPL = C / 32;                                       // rows per lane
   constexpr int VW = (int)(16 / sizeof(T)) < RPL ? (int)(16 / sizeof(T)) : RPL;  // elems per vector load
   constexpr int NV = RPL / VW;
-  constexpr int V256W = (int)(32 / sizeof(T));       // elements per 256-bit load
-  constexpr bool V256 = RPL % V256W == 0;            // a lane's k-step values fill whole 256-bit loads
   constexpr int U = RPL >= 8 ? 1 : 8 / RPL;                         // k-unroll (loads in flight)
   constexpr bool PACK = D8 && RPL <= 4;
   const int lane = threadIdx.x & 31;
@@ -191,16 +189,7 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
           T tv[VW];
           int tc[VW];
           if (ok) {
-            // lanes owning ≥ 32 B of values per k-step (fp64 C ≥ 128, fp32
-            // C = 256) read them with 256-bit evict-first loads (the slot
-            // offsets are multiples of C: 32-byte aligned); the 16-byte
-            // vector pairs are merged into one load
-            if constexpr (V256) {
-              if (q % (V256W / VW) == 0)
-                ld_stream256(vrow + q * VW, *reinterpret_cast<T(*)[V256W]>(&v[u][q * VW]));
-            } else {
-              load_vals<T, VW>(vrow + q * VW, tv);
-            }
+            load_vals<T, VW>(vrow + q * VW, tv);
             if constexpr (!DOFF) load_cols<VW>(crow + q * VW, tc);
           } else {
 #pragma unroll
@@ -211,7 +200,7 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_sliced(const Sl
           }
 #pragma unroll
           for (int w = 0; w < VW; ++w) {
-            if (!V256 || !ok) v[u][q * VW + w] = tv[w];
+            v[u][q * VW + w] = tv[w];
             if constexpr (!DOFF) c[u][q * VW + w] = tc[w];
           }
         }
