@@ -991,10 +991,11 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_nnz_map(con
   int r[W];
   {
     int64_t ord = ord0 + (incl - cnt) - 1;  // ordinal of the row holding the entry before the lane's first
-    int row = ord >= 0 ? __ldg(p.rm_rows + ord) : 0;
+    auto row_of = [&](int64_t o) { return p.rm_identity ? (int)o : __ldg(p.rm_rows + o); };
+    int row = ord >= 0 ? row_of(ord) : 0;
 #pragma unroll
     for (int q = 0; q < W; ++q) {
-      if ((byte >> q) & 1u) row = __ldg(p.rm_rows + (++ord));
+      if ((byte >> q) & 1u) row = row_of(++ord);
       r[q] = k0 + q < p.nnz ? row : INT_MAX;
     }
   }
@@ -1037,7 +1038,8 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_nnz_map(con
   if (lane == 31) {
     if (end < p.nnz) {  // the row holding entry `end`: a start there, else the row of the last start before it
       const bool st = (__ldg(p.rm_bits + (end >> 5)) >> (end & 31)) & 1u;
-      next_first = __ldg(p.rm_rows + (__ldg(p.rm_ord0 + chunk + 1) - (st ? 0 : 1)));
+      const int64_t o = __ldg(p.rm_ord0 + chunk + 1) - (st ? 0 : 1);
+      next_first = p.rm_identity ? (int)o : __ldg(p.rm_rows + o);
     } else {
       next_first = INT_MAX;
     }

@@ -21,6 +21,7 @@ struct CsrParams {
   const uint32_t* rm_bits;  // row map (k_csr_nnz_map): row-start bit per entry
   const int32_t* rm_rows;   //   ids of the non-empty rows, in order
   const int64_t* rm_ord0;   //   row starts before each 256-entry chunk
+  int rm_identity;          //   no empty rows: the j-th non-empty row is row j (no list lookups)
 };
 
 using CsrFn = void (*)(const CsrParams);

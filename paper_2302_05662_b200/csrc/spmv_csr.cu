@@ -85,6 +85,7 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     p.rm_bits = h->rm_bits;
     p.rm_rows = h->rm_rows;
     p.rm_ord0 = h->rm_ord0;
+    p.rm_identity = h->csr_n_empty == 0;
     void* args[] = {&p};
     launch_checked(fn, dim3((unsigned)((nchunks * 32 + L.block - 1) / L.block)), dim3(L.block), args, 0, h->stream);
     run_seg_fixup(h, p.recs, nchunks, e, y);
