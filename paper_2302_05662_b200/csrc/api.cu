@@ -426,6 +426,8 @@ static std::vector<int> knob_set(const spmv_matrix* h, int fmt) {
         std::vector<int> v{t};
         if (t / 2 >= 1) v.push_back(t / 2);
         if (t * 2 <= 32) v.push_back(t * 2);
+        for (int q : {t / 2, t})  // quad (128-bit) loads: a lane covers 4 entries per step
+          if (q >= 4) v.push_back(kern::kCsrQuad | q);
         return v;
       }
     case SPMV_FMT_ELL:  // rows per warp × batch loop (kern::kSlicedCarry)

@@ -8,5 +8,9 @@ template CsrFn csr_vector_fn<double, int32_t, 4>(int, int);
 template CsrFn csr_vector_fn<double, int32_t, 8>(int, int);
 template CsrFn csr_vector_fn<double, int32_t, 16>(int, int);
 template CsrFn csr_vector_fn<double, int32_t, 32>(int, int);
+template CsrFn csr_vector4_fn<double, int32_t, 4>(int, int);
+template CsrFn csr_vector4_fn<double, int32_t, 8>(int, int);
+template CsrFn csr_vector4_fn<double, int32_t, 16>(int, int);
+template CsrFn csr_vector4_fn<double, int32_t, 32>(int, int);
 }  // namespace kern
 }  // namespace spmv

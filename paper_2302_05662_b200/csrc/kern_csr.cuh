@@ -92,6 +92,107 @@ __global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_vector(cons
   if (p.e.mode == 1) power_reduce(p.e, yy, xy);
 }
 
+// CSR-vector with quad loads (knob kCsrQuad | LANES): like k_csr_vector, but
+// a lane reads 4 consecutive entries of its row per step with one 128-bit
+// column load and 128-bit value loads, aligned to the array's 4-entry quads
+// (entries of the quad outside the row are masked, never gathered): 4× fewer
+// load instructions for long rows, the same bytes. A quad reaching past the
+// last nonzero is read entry by entry.
+template <int B, int R, class T, int LANES, class RP>
+__global__ void __launch_bounds__(B) __maxnreg__(regcap(B, R)) k_csr_vector4(const CsrParams p) {
+  constexpr int UR = LANES >= 16 ? 2 : 1;
+  const RP* __restrict__ rp = static_cast<const RP*>(p.rp);
+  const T* __restrict__ val = static_cast<const T*>(p.val);
+  const T* __restrict__ x = static_cast<const T*>(p.x);
+  T* __restrict__ y = static_cast<T*>(p.y);
+  const int64_t g0 = ((int64_t)blockIdx.x * B + threadIdx.x) / LANES;
+  const int64_t ngroups = (int64_t)gridDim.x * (B / LANES);
+  const int li = (int)(threadIdx.x & (LANES - 1));
+  const double alpha = epi_alpha(p.e);
+  double yy = 0.0, xy = 0.0;
+  const int64_t gw0 = g0 - (int64_t)((threadIdx.x & 31) / LANES);
+  for (int64_t it = 0;; ++it) {
+    if ((gw0 + it * ngroups) * UR >= p.rows) break;
+    const int64_t row0 = (g0 + it * ngroups) * UR;
+    int64_t a[UR], b[UR], q0[UR], nq[UR];
+    int64_t m = 0;
+#pragma unroll
+    for (int j = 0; j < UR; ++j) {
+      const bool ok = row0 + j < p.rows;
+      a[j] = ok ? (int64_t)rp[row0 + j] : 0;
+      b[j] = ok ? (int64_t)rp[row0 + j + 1] : 0;
+      q0[j] = a[j] >> 2;
+      nq[j] = b[j] > a[j] ? ((b[j] + 3) >> 2) - q0[j] : 0;
+      m = max(m, nq[j]);
+    }
+    double acc[UR];
+#pragma unroll
+    for (int j = 0; j < UR; ++j) acc[j] = 0.0;
+    for (int64_t oq = li; oq < m; oq += LANES) {
+      int c[UR][4];
+      T v[UR][4];
+#pragma unroll
+      for (int j = 0; j < UR; ++j) {
+        const int64_t e0 = (q0[j] + oq) * 4;
+        if (oq < nq[j] && e0 + 4 <= p.nnz) {
+          const int4 cc = ld_stream(reinterpret_cast<const int4*>(p.col + e0));
+          c[j][0] = cc.x; c[j][1] = cc.y; c[j][2] = cc.z; c[j][3] = cc.w;
+          if constexpr (sizeof(T) == 8) {
+            const double2 v0 = ld_stream(reinterpret_cast<const double2*>(val + e0));
+            const double2 v1 = ld_stream(reinterpret_cast<const double2*>(val + e0 + 2));
+            v[j][0] = v0.x; v[j][1] = v0.y; v[j][2] = v1.x; v[j][3] = v1.y;
+          } else {
+            const float4 v0 = ld_stream(reinterpret_cast<const float4*>(val + e0));
+            v[j][0] = v0.x; v[j][1] = v0.y; v[j][2] = v0.z; v[j][3] = v0.w;
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int64_t e = e0 + t;
+            const bool ok = oq < nq[j] && e < p.nnz;
+            c[j][t] = ok ? ld_stream(p.col + e) : -1;
+            v[j][t] = ok ? ld_stream(val + e) : T(0);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int64_t e = e0 + t;
+          if (e < a[j] || e >= b[j]) c[j][t] = -1;  // another row's entry: masked
+        }
+      }
+      T xv[UR][4];
+#pragma unroll
+      for (int j = 0; j < UR; ++j)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) xv[j][t] = c[j][t] >= 0 ? ld_x(x + c[j][t]) : T(0);
+#pragma unroll
+      for (int j = 0; j < UR; ++j)
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (c[j][t] >= 0) acc[j] = fma((double)v[j][t], (double)xv[j][t], acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < UR; ++j)
+#pragma unroll
+      for (int o = LANES / 2; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+    if (li == 0) {
+#pragma unroll
+      for (int j = 0; j < UR; ++j) {
+        const int64_t row = row0 + j;
+        if (row < p.rows) {
+          const T out = epi_value<T>(p.e, alpha, acc[j], y, row);
+          y[row] = out;
+          if (p.e.mode == 1) {
+            yy += (double)out * (double)out;
+            xy += (double)x[p.e.row_offset + row] * (double)out;
+          }
+        }
+      }
+    }
+  }
+  if (p.e.mode == 1) power_reduce(p.e, yy, xy);
+}
+
 // ------------------------------------------------------------------ CSR-stream
 // Thread per row over a shared-memory copy of the tile's CSR segment, fed by a
 // TMA pipeline. A tile is B consecutive rows; its entries [rp[r0], rp[r0+B])
@@ -1107,6 +1208,16 @@ __global__ void k_merge_partition(const RP* __restrict__ rp, int64_t rows, int64
     coords[2 * c + 1] = yy;
   }
 }
+
+#define CSRV4_ROW(B, L) {&k_csr_vector4<B, 32, T, L, RP>, &k_csr_vector4<B, 64, T, L, RP>, \
+                         &k_csr_vector4<B, 128, T, L, RP>, &k_csr_vector4<B, 255, T, L, RP>}
+template <class T, class RP, int L>
+CsrFn csr_vector4_fn(int bi, int ri) {
+  static const CsrFn tab[5][4] = {CSRV4_ROW(64, L), CSRV4_ROW(128, L), CSRV4_ROW(256, L), CSRV4_ROW(512, L),
+                                  CSRV4_ROW(1024, L)};
+  return tab[bi][ri];
+}
+#undef CSRV4_ROW
 
 #define CSRV_ROW(B, L) {&k_csr_vector<B, 32, T, L, RP>, &k_csr_vector<B, 64, T, L, RP>, \
                         &k_csr_vector<B, 128, T, L, RP>, &k_csr_vector<B, 255, T, L, RP>}

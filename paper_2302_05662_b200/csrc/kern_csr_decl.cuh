@@ -29,6 +29,10 @@ template <class T, class RP, int LANES>
 CsrFn csr_vector_fn(int bi, int ri);
 template <class T, class RP, int IPT>
 CsrFn csr_merge_fn(int bi, int ri);
+// CSR-vector with quad (128-bit) loads: knob kCsrQuad | LANES, LANES in {4, 8, 16, 32}
+constexpr int kCsrQuad = 0x100;
+template <class T, class RP, int LANES>
+CsrFn csr_vector4_fn(int bi, int ri);
 template <class T, class RP, int EPT>
 CsrFn csr_stream_fn(int bi, int ri);
 // Shared-memory stage of the CSR-stream pipeline holding `cap` entries: the

@@ -42,6 +42,32 @@ void csr_typed(spmv_matrix* h, const Epilogue& e, const void* x, void* y, const 
     launch_checked(fn, dim3((unsigned)grid), dim3(threads), args, smem, h->stream);
     return;
   }
+  if (!merge && (L.knob & kern::kCsrQuad)) {
+    const int lanes = L.knob & 0xff;
+    const void* fn;
+    switch (lanes) {
+      case 4: fn = (const void*)kern::csr_vector4_fn<T, RP, 4>(bi, ri); break;
+      case 8: fn = (const void*)kern::csr_vector4_fn<T, RP, 8>(bi, ri); break;
+      case 16: fn = (const void*)kern::csr_vector4_fn<T, RP, 16>(bi, ri); break;
+      case 32: fn = (const void*)kern::csr_vector4_fn<T, RP, 32>(bi, ri); break;
+      default: fail(SPMV_ERR_INVALID_ARG, "CSR-vector quad loads take 4, 8, 16 or 32 lanes per row");
+    }
+    if (((uintptr_t)h->col | (uintptr_t)h->val) & 15)
+      fail(SPMV_ERR_UNSUPPORTED, "CSR-vector quad loads: col/val must be 16-byte aligned");
+    const LaunchAttrs attrs(fn, L.carveout_pct);
+    const int ur = lanes >= 16 ? 2 : 1;
+    const int64_t groups = (h->rows + ur - 1) / ur;
+    const int64_t grid = persistent_grid(fn, L.block, (groups * lanes + L.block - 1) / L.block);
+    if (grid <= 0) return;
+    if (e.mode == 1) {
+      ensure_pi_scratch(h, (size_t)grid);
+      p.e.partials = h->pi_partials;
+      p.e.counter = h->pi_counter;
+    }
+    void* args[] = {&p};
+    launch_checked(fn, dim3((unsigned)grid), dim3(L.block), args, 0, h->stream);
+    return;
+  }
   if (!merge) {
     const int lanes = L.knob;
     const void* fn;

@@ -245,7 +245,7 @@ def test_spmv_parity(name, dtype, fname, fmt, params):
 
 
 @pytest.mark.parametrize("fname,fmt,params,knobs", [
-    ("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR), [1, 2, 4, 8, 16, 32]),
+    ("CSR-vector", P.FMT_CSR, dict(csr_alg=P.CSR_VECTOR), [1, 2, 4, 8, 16, 32, 0x104, 0x108, 0x110, 0x120]),
     ("CSR-merge", P.FMT_CSR, dict(csr_alg=P.CSR_MERGE), [4, 8, 16, 0x104, 0x108, 0x110, 0x204, 0x208, 0x210,
                                                          0x404, 0x408, 0x808]),
     ("CSR-stream", P.FMT_CSR, dict(csr_alg=P.CSR_STREAM), [16, 32, 64]),
